@@ -1,0 +1,225 @@
+/*
+ * qgtc_b200.h -- C-ABI of the B200-native QGTC hot path (sm_100a).
+ *
+ * The reference (`bitgnn`, /root/reference/pkg/src/bitgnn) is a pure
+ * Python/numpy package with no FFI; its drop-in boundary is the Python API.
+ * Each entry point below replaces the compute of one reference function
+ * (cited as file:line); the Python mirror package `paper_2111_09547_b200`
+ * binds them with ctypes and keeps the reference names, argument meaning and
+ * exceptions.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers (caller-owned; no hidden allocation).
+ *    `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *    and asynchronous.
+ *  - Packed planes use the reference layouts verbatim (bitpack.py:3-14):
+ *      column-wise: words[plane][padded_rows][padded_cols/32]
+ *      row-wise:    words[plane][padded_cols][padded_rows/32]
+ *    bit j of a word is element 32*w + j; every padding bit is zero.
+ *  - Return value: QG_OK or a QG_ERR_* code for host-side argument errors
+ *    (raised eagerly, before any launch, like the reference's ShapeError /
+ *    ValueError).  Data-dependent conditions detected on the device
+ *    (non-finite input, non-binary plane, int32 overflow) are reported
+ *    through caller-provided device status words, read by the caller after
+ *    the stream synchronises.
+ *  - `status` words are int64 "first bad linear index" cells updated with
+ *    atomicMin; initialise them with qg_status_reset (0x7f.. pattern).
+ */
+#ifndef QGTC_B200_H
+#define QGTC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QG_OK 0
+#define QG_ERR_ARG 1          /* null pointer / negative size / bad enum   */
+#define QG_ERR_SHAPE 2        /* operand dims or orientations incompatible */
+#define QG_ERR_BITS 3         /* bit width outside [1, 8]                   */
+#define QG_ERR_CUDA 4         /* launch failure (cudaGetLastError)          */
+#define QG_ERR_UNSUPPORTED 5  /* shape the selected algorithm cannot run    */
+
+#define QG_COLUMN_WISE 0
+#define QG_ROW_WISE 1
+
+#define QG_SRC_F32 0
+#define QG_SRC_F64 1
+#define QG_SRC_U8 2           /* codes already quantized; validated < 2**bits */
+
+#define QG_ACT_NONE 0
+#define QG_ACT_RELU 1
+#define QG_ACT_TANH 2
+
+#define QG_OUT_REAL 0         /* fp64 matrix [rows][cols]                   */
+#define QG_OUT_PLANES 1       /* requantized packed planes (+ row sums)     */
+
+#define QG_GEMM_PER_PLANE 0   /* out_i32[p][rows][cols] = L(1-bit) . R_p     */
+#define QG_GEMM_I32 1         /* out_i32[rows][cols] = sum (L_i . R_j) << (i+j) */
+#define QG_GEMM_EPILOGUE 2    /* reduced accumulator -> fused epilogue      */
+
+#define QG_ALGO_AUTO 0
+#define QG_ALGO_TCGEN05 1     /* tcgen05.mma kind::i8, planes recomposed on chip */
+#define QG_ALGO_POPC 2        /* CUDA-core AND+POPC over packed words (exact int64) */
+
+/* Library identity / sanity: returns the number of exported compute entry points. */
+int qg_version(void);
+
+/* Reset `n` int64 status cells to "no error" (0x7f7f.. > any index). */
+int qg_status_reset(int64_t* status, int64_t n, void* stream);
+
+/*
+ * Fused Eq.2 quantization + bit decomposition + packing (bit_qnt).
+ * Replaces quantize_matrix (quantize.py:93-105) + bit_decompose
+ * (quantize.py:108-112) + pack_planes (bitpack.py:213-228), and the row/column
+ * code sums the engine derives from them (engine.py:150, 203, 280).
+ *   src:        row-major rows x cols (leading dim ld) of f32/f64 reals, or u8 codes
+ *   code = clip(floor((x - alpha_min) / scale), 0, 2**bits - 1), fp64, no FMA
+ *   planes:     bits x words_per_plane output, fully written (padding = 0)
+ *   codes:      optional u8 [rows][cols] copy of the codes (QuantMatrix.values)
+ *   row_sums:   optional int64 [rows], ACCUMULATED (caller zeroes)
+ *   col_sums:   optional int64 [cols], ACCUMULATED (caller zeroes)
+ *   status:     first non-finite (f32/f64) or out-of-range (u8) index r*cols+c
+ */
+int qg_quantize_pack(const void* src, int src_kind, int64_t rows, int64_t cols, int64_t ld,
+                     double alpha_min, double scale, int bits, int orientation, int pad_to,
+                     uint32_t* planes, uint8_t* codes, int64_t* row_sums, int64_t* col_sums,
+                     int64_t* status, void* stream);
+
+/*
+ * Pack `nplanes` logical 0/1 planes (u8 [nplanes][rows][cols]).  Replaces
+ * pack_colwise / pack_rowwise / pack_planes (bitpack.py:169-228); status
+ * receives the first non-binary index p*rows*cols + r*cols + c
+ * (_as_binary, bitpack.py:153-160).
+ */
+int qg_pack_planes(const uint8_t* planes01, int64_t nplanes, int64_t rows, int64_t cols,
+                   int orientation, int pad_to, uint32_t* words, int64_t* status, void* stream);
+
+/*
+ * Unpack to logical planes and/or codes.  Replaces unpack / to_planes
+ * (bitpack.py:194-233) and to_val (quantize.py:115-129).
+ *   out_planes: optional u8 [nplanes][rows][cols]
+ *   out_codes:  optional int32 [rows][cols] = sum_p plane_p << p
+ */
+int qg_unpack(const uint32_t* words, int64_t nplanes, int64_t rows, int64_t cols,
+              int64_t padded_rows, int64_t padded_cols, int orientation,
+              uint8_t* out_planes, int32_t* out_codes, void* stream);
+
+/*
+ * Re-orient a stack through 32x32 warp bit transposes (no logical planes in
+ * HBM).  Replaces repack (bitpack.py:236-238) and the engine's _oriented
+ * (engine.py:173-176).  dst dims are the destination padded dims.
+ */
+int qg_repack(const uint32_t* src, int64_t nplanes, int64_t src_pr, int64_t src_pc,
+              int src_orientation, uint32_t* dst, int64_t dst_pr, int64_t dst_pc, void* stream);
+
+/*
+ * Zero-tile scan of a column-wise 1-bit operand over 8x128 tiles plus
+ * popcount row degrees.  Replaces scan_zero_tiles (bitgemm.py:214-233) and
+ * SubgraphBatch.degrees (graph.py:292-295).
+ *   zero_flags: optional u8 [pr/8][pc/128] (1 = all-zero tile)
+ *   degrees:    optional int64 [rows]
+ *   zero_count: optional int64 [1], ACCUMULATED (caller zeroes)
+ *   blk_list / blk_count: optional per-128-row-block lists of non-zero
+ *     128-bit K tiles (the zero-tile-jumping schedule of the GEMM kernels):
+ *     blk_list[rb * (pc/128) + i], i < blk_count[rb].
+ */
+int qg_tile_scan(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,
+                 uint8_t* zero_flags, int64_t* degrees, int64_t* zero_count,
+                 int32_t* blk_list, int32_t* blk_count, void* stream);
+
+/* Per-plane zero 8x128 tile counts of a column-wise stack (GEMM counters,
+ * bitgemm.py:426-427); zero_counts int64 [nplanes], ACCUMULATED. */
+int qg_plane_zero_tiles(const uint32_t* words, int64_t nplanes, int64_t padded_rows,
+                        int64_t padded_cols, int64_t* zero_counts, void* stream);
+
+/* Fused epilogue parameters (EpilogueSpec, bitgemm.py:125-153; the
+ * coefficients are the reference's fp64 term grouping, bitgemm.py:156-179,
+ * precomputed on the host so the device evaluates the identical expression). */
+typedef struct {
+  int32_t act;                 /* QG_ACT_*                                        */
+  int32_t use_row, use_col, use_const;
+  double k_acc;                /* sa * sb                                         */
+  double k_row;                /* sa * amb      (times lhs_row_sums[r])           */
+  double k_col;                /* sb * ama      (times rhs_col_sums[c])           */
+  double k_const;              /* (inner_dim * ama) * amb                         */
+  const int64_t* row_sums;     /* [rows]                                          */
+  const int64_t* col_sums;     /* [cols]                                          */
+  const double* bias;          /* [cols] or NULL                                  */
+  const double* bn_mean;       /* [cols] or NULL (all four or none)               */
+  const double* bn_denom;      /* sqrt(var + eps), host-computed                  */
+  const double* bn_gamma;
+  const double* bn_beta;
+  int32_t out_kind;            /* QG_OUT_REAL / QG_OUT_PLANES                     */
+  int32_t q_bits;              /* requant grid (quantize.py:93-105)               */
+  double q_amin, q_scale;
+  int32_t q_orientation;       /* QG_COLUMN_WISE / QG_ROW_WISE                    */
+  int32_t pad_;
+  int64_t q_prows, q_pcols;    /* padded dims of the output stack                 */
+  double* out_real;            /* [rows][cols] for QG_OUT_REAL                    */
+  uint32_t* q_planes;          /* q_bits x words; caller zero-fills               */
+  int64_t* q_row_sums;         /* optional [rows], ACCUMULATED (caller zeroes)    */
+  int64_t* status;             /* optional: first non-finite requant input index  */
+} qg_epilogue;
+
+/*
+ * Stand-alone epilogue over an int32 accumulator [rows][cols].  Replaces
+ * apply_epilogue (bitgemm.py:182-211).  The fused GEMM path evaluates the
+ * same device function, so fused == unfused bit for bit.
+ */
+int qg_epilogue_apply(const int32_t* acc, int64_t rows, int64_t cols, const qg_epilogue* epi,
+                      void* stream);
+
+/* Any-bitwidth bit-GEMM arguments.  L is column-wise (M x K, lbits planes),
+ * R is row-wise (K x N, rbits planes) with the same padded K. */
+typedef struct {
+  const uint32_t* lhs; int32_t lbits; int32_t pad0;
+  int64_t m, m_padded;         /* logical / padded rows of L                      */
+  int64_t k, k_padded;         /* logical / padded shared dim (k_padded % 128 == 0) */
+  const uint32_t* rhs; int32_t rbits; int32_t pad1;
+  int64_t n, n_padded;         /* logical / padded cols of R                      */
+  const int32_t* blk_list;     /* optional zero-tile-jumping schedule (qg_tile_scan) */
+  const int32_t* blk_count;
+  int32_t mode;                /* QG_GEMM_*                                       */
+  int32_t algo;                /* QG_ALGO_*                                       */
+  int32_t* out_i32;            /* PER_PLANE: [rbits][m][n]; I32: [m][n]          */
+  const qg_epilogue* epi;      /* EPILOGUE mode                                   */
+  int32_t* overflow;           /* optional device flag, set to 1 on int32 overflow */
+  int32_t* scratch_i32;        /* [m][n] scratch for the POPC epilogue path       */
+  int32_t cross_bit;           /* PER_PLANE: 1 = one plane per CTA (cross-bit reuse),
+                                  0 = planes stacked along N so each L tile is
+                                  expanded once for all planes (cross-tile reuse) */
+  int32_t pad2;
+} qg_gemm_args;
+
+/*
+ * Bit-GEMM.  Replaces bmm_1bit_by_nbit (bitgemm.py:306-371; mode PER_PLANE),
+ * gemm_sbit_by_tbit (bitgemm.py:374-475; modes I32 / EPILOGUE) and
+ * reduce_bitplanes + apply_epilogue inside the engine (engine.py:235-317).
+ * The TCGEN05 algorithm recomposes plane stacks into u8 codes in shared
+ * memory (sum_p 2^p plane_p, exact) and runs tcgen05.mma kind::i8; it is
+ * selected only when (2^lbits-1)(2^rbits-1)k < 2^31 so the s32 tensor
+ * accumulator cannot wrap.  POPC is exact in int64 and flags overflow like
+ * _narrow_int32 (bitgemm.py:282-288).
+ */
+int qg_bitgemm(const qg_gemm_args* args, void* stream);
+
+/* Shifted reduction sum_p acc[p] << p (int64 in) narrowed to int32 with an
+ * overflow flag.  Replaces reduce_bitplanes (bitgemm.py:291-298). */
+int qg_reduce_planes(const int64_t* accs, int64_t nplanes, int64_t n, int32_t* out,
+                     int32_t* overflow, void* stream);
+
+/* Set adjacency bits from an edge list into zero-initialised column-wise
+ * words (row = src, col = dst).  Replaces the dense total x total build +
+ * pack_colwise of build_batch (graph.py:334-342) without a dense matrix. */
+int qg_edges_to_bits(const int64_t* src, const int64_t* dst, int64_t n_edges, int64_t rows,
+                     uint32_t* words, int64_t padded_rows, int64_t padded_cols, void* stream);
+
+/* popcount32 (bitgemm.py:58-60) on the device. */
+int qg_popcount32(const uint32_t* in, int64_t n, int32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QGTC_B200_H */

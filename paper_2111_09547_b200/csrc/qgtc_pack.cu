@@ -1,0 +1,509 @@
+// bit_qnt and layout kernels: fused quantize + bit-decompose + pack, plane
+// packing, unpack/to_val, warp bit-transpose repack, zero-tile scan.
+// All HBM-bound; every warp access is a coalesced 128 B row segment.
+#include <algorithm>
+#include "qgtc_common.cuh"
+
+namespace qg {
+
+// ------------------------------------------------------------ quantize+pack
+template <typename SrcT>
+__device__ __forceinline__ uint32_t load_code(const SrcT* src, int kind, int64_t r, int64_t c, int64_t ld,
+                                              int64_t cols, double amin, double scale, uint32_t maxv,
+                                              int64_t* status, int64_t status_base) {
+  if constexpr (sizeof(SrcT) == 1) {
+    uint32_t v = src[r * ld + c];
+    if (v > maxv) { status_min(status, status_base + r * cols + c); v &= maxv; }
+    return v;
+  } else {
+    double x = (double)src[r * ld + c];
+    if (!isfinite(x)) status_min(status, status_base + r * cols + c);
+    return quantize_code(x, amin, scale, maxv);
+  }
+}
+
+// Column-wise: one warp per (row, chunk of 32 words).  Lane l reads column
+// 32*w + l for each word w of the chunk; ballots form the words; lane j keeps
+// word j of the chunk so the final stores are coalesced.
+template <typename SrcT, int BITS>
+__global__ void __launch_bounds__(256) quantize_pack_col_kernel(
+    const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale,
+    int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
+    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpr = pcols >> 5;
+  const int64_t chunks = (wpr + 31) >> 5;
+  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (item >= prows * chunks) return;
+  const int64_t r = item / chunks;
+  const int64_t w0 = (item % chunks) * 32;
+  const int nw = (int)(wpr - w0 < 32 ? wpr - w0 : 32);
+  const uint32_t maxv = (1u << BITS) - 1u;
+  uint32_t mine[BITS];
+#pragma unroll
+  for (int p = 0; p < BITS; ++p) mine[p] = 0;
+  int64_t rsum = 0;
+  const bool rvalid = r < rows;
+  for (int it = 0; it < nw; ++it) {
+    const int64_t c = (w0 + it) * 32 + lane;
+    uint32_t code = 0;
+    if (rvalid && c < cols) {
+      code = load_code<SrcT>(src, 0, r, c, ld, cols, amin, scale, maxv, status, status_base);
+      rsum += code;
+      if (codes) codes[r * cols + c] = (uint8_t)code;
+    }
+#pragma unroll
+    for (int p = 0; p < BITS; ++p) {
+      uint32_t b = __ballot_sync(QG_FULL, (code >> p) & 1u);
+      if (lane == it) mine[p] = b;
+    }
+  }
+  if (lane < nw) {
+    const int64_t wpp = prows * wpr;
+#pragma unroll
+    for (int p = 0; p < BITS; ++p) planes[p * wpp + r * wpr + w0 + lane] = mine[p];
+  }
+  if (row_sums && rvalid) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(QG_FULL, rsum, o);
+    if (lane == 0 && rsum) atomicAdd(reinterpret_cast<unsigned long long*>(row_sums + r), (unsigned long long)rsum);
+  }
+}
+
+// Row-wise: one warp per (32-row group v, 32 consecutive columns).  Lane l owns
+// column c0+l and walks the 32 rows (each step is a coalesced row segment).
+template <typename SrcT, int BITS>
+__global__ void __launch_bounds__(256) quantize_pack_row_kernel(
+    const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale,
+    int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
+    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpc = prows >> 5;             // words per column
+  const int64_t cgroups = (pcols + 31) >> 5;
+  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (item >= wpc * cgroups) return;
+  const int64_t v = item / cgroups;
+  const int64_t c = (item % cgroups) * 32 + lane;
+  const uint32_t maxv = (1u << BITS) - 1u;
+  uint32_t word[BITS];
+#pragma unroll
+  for (int p = 0; p < BITS; ++p) word[p] = 0;
+  for (int i = 0; i < 32; ++i) {
+    const int64_t r = v * 32 + i;
+    uint32_t code = 0;
+    if (r < rows && c < cols) {
+      code = load_code<SrcT>(src, 0, r, c, ld, cols, amin, scale, maxv, status, status_base);
+      if (codes) codes[r * cols + c] = (uint8_t)code;
+    }
+#pragma unroll
+    for (int p = 0; p < BITS; ++p) word[p] |= ((code >> p) & 1u) << i;
+    if (row_sums && r < rows) {
+      int64_t s = code;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(QG_FULL, s, o);
+      if (lane == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(row_sums + r), (unsigned long long)s);
+    }
+  }
+  if (c < pcols) {
+    const int64_t wpp = pcols * wpc;
+#pragma unroll
+    for (int p = 0; p < BITS; ++p) planes[p * wpp + c * wpc + v] = word[p];
+  }
+}
+
+template <typename SrcT>
+__global__ void col_sums_kernel(const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld,
+                                double amin, double scale, uint32_t maxv, int64_t* __restrict__ col_sums) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  int64_t s = 0;
+  for (int64_t r = 0; r < rows; ++r) {
+    if constexpr (sizeof(SrcT) == 1) {
+      s += (src[r * ld + c] < maxv ? (uint32_t)src[r * ld + c] : maxv);
+    } else {
+      s += quantize_code((double)src[r * ld + c], amin, scale, maxv);
+    }
+  }
+  col_sums[c] += s;
+}
+
+template <typename SrcT, int BITS>
+int launch_quantize_pack(const SrcT* src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale,
+                         int orientation, int64_t prows, int64_t pcols, uint32_t* planes, uint8_t* codes,
+                         int64_t* row_sums, int64_t* col_sums, int64_t* status, int64_t status_base,
+                         cudaStream_t st) {
+  int64_t warps;
+  if (orientation == QG_COLUMN_WISE) {
+    warps = prows * (((pcols >> 5) + 31) >> 5);
+  } else {
+    warps = (prows >> 5) * ((pcols + 31) >> 5);
+  }
+  if (warps > 0) {
+    const int64_t blocks = (warps * 32 + 255) / 256;
+    if (orientation == QG_COLUMN_WISE)
+      quantize_pack_col_kernel<SrcT, BITS><<<(unsigned)blocks, 256, 0, st>>>(
+          src, rows, cols, ld, amin, scale, prows, pcols, planes, codes, row_sums, status, status_base);
+    else
+      quantize_pack_row_kernel<SrcT, BITS><<<(unsigned)blocks, 256, 0, st>>>(
+          src, rows, cols, ld, amin, scale, prows, pcols, planes, codes, row_sums, status, status_base);
+  }
+  if (col_sums && cols > 0 && rows > 0)
+    col_sums_kernel<SrcT><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(src, rows, cols, ld, amin, scale,
+                                                                          (1u << BITS) - 1u, col_sums);
+  return QG_OK;
+}
+
+template <typename SrcT>
+int dispatch_quantize_pack(const SrcT* src, int64_t rows, int64_t cols, int64_t ld, double amin,
+                           double scale, int bits, int orientation, int64_t prows, int64_t pcols,
+                           uint32_t* planes, uint8_t* codes, int64_t* row_sums, int64_t* col_sums,
+                           int64_t* status, int64_t status_base, cudaStream_t st) {
+  switch (bits) {
+#define QG_CASE(B) \
+  case B:          \
+    return launch_quantize_pack<SrcT, B>(src, rows, cols, ld, amin, scale, orientation, prows, pcols, planes, \
+                                         codes, row_sums, col_sums, status, status_base, st);
+    QG_CASE(1) QG_CASE(2) QG_CASE(3) QG_CASE(4) QG_CASE(5) QG_CASE(6) QG_CASE(7) QG_CASE(8)
+#undef QG_CASE
+    default:
+      return QG_ERR_BITS;
+  }
+}
+
+// ---------------------------------------------------------------- unpack
+__global__ void unpack_kernel(const uint32_t* __restrict__ words, int64_t nplanes, int64_t rows, int64_t cols,
+                              int64_t prows, int64_t pcols, int orientation, uint8_t* __restrict__ out_planes,
+                              int32_t* __restrict__ out_codes) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const int64_t r = idx / cols, c = idx % cols;
+  const int64_t wpp = prows * pcols / 32;
+  int64_t off;
+  int bit;
+  if (orientation == QG_COLUMN_WISE) {
+    off = r * (pcols >> 5) + (c >> 5);
+    bit = (int)(c & 31);
+  } else {
+    off = c * (prows >> 5) + (r >> 5);
+    bit = (int)(r & 31);
+  }
+  int32_t code = 0;
+  for (int64_t p = 0; p < nplanes; ++p) {
+    uint32_t b = (__ldg(words + p * wpp + off) >> bit) & 1u;
+    if (out_planes) out_planes[p * rows * cols + idx] = (uint8_t)b;
+    code |= (int32_t)(b << p);
+  }
+  if (out_codes) out_codes[idx] = code;
+}
+
+// ---------------------------------------------------------------- repack
+// Warp-level 32x32 bit transpose through ballots: lane i loads the source word
+// of line i; ballot j collects bit j of every lane = destination word j.
+__global__ void __launch_bounds__(256) repack_kernel(const uint32_t* __restrict__ src, int64_t nplanes,
+                                                     int64_t spr, int64_t spc, int src_orientation,
+                                                     uint32_t* __restrict__ dst, int64_t dpr, int64_t dpc) {
+  const int lane = threadIdx.x & 31;
+  // block grid over (row groups of 32) x (column groups of 32) of the padded union
+  const int64_t rmax = max(spr, dpr), cmax = max(spc, dpc);
+  const int64_t rg = (rmax + 31) >> 5, cg = (cmax + 31) >> 5;
+  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (item >= rg * cg * nplanes) return;
+  const int64_t p = item / (rg * cg);
+  const int64_t rem = item % (rg * cg);
+  const int64_t v = rem / cg;   // 32-row group
+  const int64_t w = rem % cg;   // 32-col group
+  const int64_t swpp = spr * spc / 32, dwpp = dpr * dpc / 32;
+  uint32_t x = 0;
+  if (src_orientation == QG_COLUMN_WISE) {
+    // lane i: row 32v+i, word w (cols 32w..)
+    const int64_t r = v * 32 + lane;
+    if (r < spr && w < (spc >> 5)) x = src[p * swpp + r * (spc >> 5) + w];
+  } else {
+    // lane i: column 32w+i, word v (rows 32v..)
+    const int64_t c = w * 32 + lane;
+    if (c < spc && v < (spr >> 5)) x = src[p * swpp + c * (spr >> 5) + v];
+  }
+  uint32_t mine = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    uint32_t b = __ballot_sync(QG_FULL, (x >> j) & 1u);
+    if (lane == j) mine = b;
+  }
+  if (src_orientation == QG_COLUMN_WISE) {
+    // destination row-wise: lane j holds column 32w+j, rows 32v..32v+31
+    const int64_t c = w * 32 + lane;
+    if (c < dpc && v < (dpr >> 5)) dst[p * dwpp + c * (dpr >> 5) + v] = mine;
+  } else {
+    // destination column-wise: lane j holds row 32v+j, cols 32w..32w+31
+    const int64_t r = v * 32 + lane;
+    if (r < dpr && w < (dpc >> 5)) dst[p * dwpp + r * (dpc >> 5) + w] = mine;
+  }
+}
+
+// -------------------------------------------------------------- tile scan
+// One warp per 8-row tile group; lane handles K tiles lane, lane+32, ...
+// Each row contributes a 16 B (uint4) load per K tile: 32 lanes read 512
+// consecutive bytes of one row -> fully coalesced.
+__global__ void __launch_bounds__(256) tile_scan_kernel(const uint32_t* __restrict__ a, int64_t rows,
+                                                        int64_t prows, int64_t pcols,
+                                                        uint8_t* __restrict__ flags, int64_t* __restrict__ degrees,
+                                                        int64_t* __restrict__ zero_count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (rt >= (prows >> 3)) return;
+  const int64_t ct = pcols >> 7, wpr = pcols >> 5;
+  uint32_t deg[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) deg[i] = 0;
+  int64_t zeros = 0;
+  for (int64_t t = lane; t < ct; t += 32) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(a + (rt * 8 + i) * wpr + t * 4));
+      any |= q.x | q.y | q.z | q.w;
+      deg[i] += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    }
+    if (flags) flags[rt * ct + t] = any == 0;
+    zeros += any == 0;
+  }
+  if (degrees) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t d = deg[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(QG_FULL, d, o);
+      if (lane == 0 && rt * 8 + i < rows) degrees[rt * 8 + i] = d;
+    }
+  }
+  if (zero_count) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) zeros += __shfl_xor_sync(QG_FULL, zeros, o);
+    if (lane == 0 && zeros) atomicAdd(reinterpret_cast<unsigned long long*>(zero_count), (unsigned long long)zeros);
+  }
+}
+
+// Zero-tile-jumping schedule: per 128-row block, the ordered list of K tiles
+// with at least one set bit.  One warp per row block, ballot + popc prefix.
+__global__ void block_list_kernel(const uint32_t* __restrict__ a, int64_t prows, int64_t pcols,
+                                  int32_t* __restrict__ blk_list, int32_t* __restrict__ blk_count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nrb = (prows + 127) >> 7;
+  if (rb >= nrb) return;
+  const int64_t ct = pcols >> 7, wpr = pcols >> 5;
+  const int64_t r_lo = rb * 128, r_hi = (prows < r_lo + 128 ? prows : r_lo + 128);
+  int32_t count = 0;
+  for (int64_t t0 = 0; t0 < ct; t0 += 32) {
+    const int64_t t = t0 + lane;
+    uint32_t any = 0;
+    if (t < ct) {
+      for (int64_t r = r_lo; r < r_hi && !any; ++r) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a + r * wpr + t * 4));
+        any = q.x | q.y | q.z | q.w;
+      }
+    }
+    const uint32_t m = __ballot_sync(QG_FULL, any != 0);
+    if (any) blk_list[rb * ct + count + __popc(m & ((1u << lane) - 1u))] = (int32_t)t;
+    count += __popc(m);
+  }
+  if (lane == 0) blk_count[rb] = count;
+}
+
+__global__ void plane_zero_tiles_kernel(const uint32_t* __restrict__ a, int64_t nplanes, int64_t prows,
+                                        int64_t pcols, int64_t* __restrict__ zero_counts) {
+  const int64_t rt_n = prows >> 3, ct = pcols >> 7, wpr = pcols >> 5;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nplanes * rt_n * ct) return;
+  const int64_t p = idx / (rt_n * ct);
+  const int64_t rem = idx % (rt_n * ct);
+  const int64_t rt = rem / ct, t = rem % ct;
+  const uint32_t* base = a + p * prows * wpr;
+  uint32_t any = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(base + (rt * 8 + i) * wpr + t * 4));
+    any |= q.x | q.y | q.z | q.w;
+  }
+  if (!any) atomicAdd(reinterpret_cast<unsigned long long*>(zero_counts + p), 1ull);
+}
+
+__global__ void status_reset_kernel(int64_t* s, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) s[i] = 0x7f7f7f7f7f7f7f7fLL;
+}
+
+__global__ void popcount_kernel(const uint32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __popc(in[i]);
+}
+
+__global__ void reduce_planes_kernel(const int64_t* __restrict__ accs, int64_t nplanes, int64_t n,
+                                     int32_t* __restrict__ out, int32_t* overflow) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // exact int64 shift-sum (wraps only beyond 2^63, far outside any valid input)
+  long long total = 0;
+  for (int64_t p = 0; p < nplanes; ++p) total += (long long)((unsigned long long)accs[p * n + i] << p);
+  if (total > 2147483647LL || total < -2147483648LL) {
+    if (overflow) atomicExch(overflow, 1);
+  }
+  out[i] = (int32_t)total;
+}
+
+}  // namespace qg
+
+// ======================================================================= ABI
+using namespace qg;
+
+static inline int launch_status() {
+  return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA;
+}
+static inline bool bad_pad(int pad) { return pad != 8 && pad != 128; }
+static inline int64_t pad_up(int64_t n, int64_t m) { return (n + m - 1) / m * m; }
+
+extern "C" int qg_status_reset(int64_t* status, int64_t n, void* stream) {
+  if (!status || n < 0) return QG_ERR_ARG;
+  if (n == 0) return QG_OK;
+  status_reset_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(status, n);
+  return launch_status();
+}
+
+extern "C" int qg_quantize_pack(const void* src, int src_kind, int64_t rows, int64_t cols, int64_t ld,
+                                double alpha_min, double scale, int bits, int orientation, int pad_to,
+                                uint32_t* planes, uint8_t* codes, int64_t* row_sums, int64_t* col_sums,
+                                int64_t* status, void* stream) {
+  if (rows < 0 || cols < 0 || ld < cols || (rows * cols > 0 && !src) || !planes) return QG_ERR_ARG;
+  if (bits < 1 || bits > 8) return QG_ERR_BITS;
+  if (orientation != QG_COLUMN_WISE && orientation != QG_ROW_WISE) return QG_ERR_ARG;
+  if (bad_pad(pad_to)) return QG_ERR_ARG;
+  const int64_t prows = orientation == QG_COLUMN_WISE ? pad_up(rows, pad_to) : pad_up(rows, 128);
+  const int64_t pcols = orientation == QG_COLUMN_WISE ? pad_up(cols, 128) : pad_up(cols, pad_to);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  switch (src_kind) {
+    case QG_SRC_F32:
+      rc = dispatch_quantize_pack<float>((const float*)src, rows, cols, ld, alpha_min, scale, bits, orientation,
+                                         prows, pcols, planes, codes, row_sums, col_sums, status, 0, st);
+      break;
+    case QG_SRC_F64:
+      rc = dispatch_quantize_pack<double>((const double*)src, rows, cols, ld, alpha_min, scale, bits, orientation,
+                                          prows, pcols, planes, codes, row_sums, col_sums, status, 0, st);
+      break;
+    case QG_SRC_U8:
+      rc = dispatch_quantize_pack<uint8_t>((const uint8_t*)src, rows, cols, ld, alpha_min, scale, bits,
+                                           orientation, prows, pcols, planes, codes, row_sums, col_sums, status, 0,
+                                           st);
+      break;
+    default:
+      return QG_ERR_ARG;
+  }
+  return rc != QG_OK ? rc : launch_status();
+}
+
+extern "C" int qg_pack_planes(const uint8_t* planes01, int64_t nplanes, int64_t rows, int64_t cols,
+                              int orientation, int pad_to, uint32_t* words, int64_t* status, void* stream) {
+  if (nplanes < 0 || rows < 0 || cols < 0 || !words || (nplanes * rows * cols > 0 && !planes01)) return QG_ERR_ARG;
+  if (orientation != QG_COLUMN_WISE && orientation != QG_ROW_WISE) return QG_ERR_ARG;
+  if (bad_pad(pad_to)) return QG_ERR_ARG;
+  const int64_t prows = orientation == QG_COLUMN_WISE ? pad_up(rows, pad_to) : pad_up(rows, 128);
+  const int64_t pcols = orientation == QG_COLUMN_WISE ? pad_up(cols, 128) : pad_up(cols, pad_to);
+  const int64_t wpp = prows * pcols / 32;
+  for (int64_t p = 0; p < nplanes; ++p) {
+    int rc = launch_quantize_pack<uint8_t, 1>(planes01 + p * rows * cols, rows, cols, cols, 0.0, 1.0, orientation,
+                                              prows, pcols, words + p * wpp, nullptr, nullptr, nullptr, status,
+                                              p * rows * cols, (cudaStream_t)stream);
+    if (rc != QG_OK) return rc;
+  }
+  return launch_status();
+}
+
+extern "C" int qg_unpack(const uint32_t* words, int64_t nplanes, int64_t rows, int64_t cols, int64_t padded_rows,
+                         int64_t padded_cols, int orientation, uint8_t* out_planes, int32_t* out_codes,
+                         void* stream) {
+  if (nplanes < 1 || rows < 0 || cols < 0 || !words) return QG_ERR_ARG;
+  if (padded_rows < rows || padded_cols < cols) return QG_ERR_SHAPE;
+  const int64_t n = rows * cols;
+  if (n == 0) return QG_OK;
+  unpack_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      words, nplanes, rows, cols, padded_rows, padded_cols, orientation, out_planes, out_codes);
+  return launch_status();
+}
+
+extern "C" int qg_repack(const uint32_t* src, int64_t nplanes, int64_t src_pr, int64_t src_pc, int src_orientation,
+                         uint32_t* dst, int64_t dst_pr, int64_t dst_pc, void* stream) {
+  if (!src || !dst || nplanes < 1) return QG_ERR_ARG;
+  if (src_pr % 8 || src_pc % 8 || dst_pr % 8 || dst_pc % 8) return QG_ERR_SHAPE;
+  const int64_t rg = (std::max(src_pr, dst_pr) + 31) / 32, cg = (std::max(src_pc, dst_pc) + 31) / 32;
+  const int64_t warps = rg * cg * nplanes;
+  if (warps == 0) return QG_OK;
+  repack_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      src, nplanes, src_pr, src_pc, src_orientation, dst, dst_pr, dst_pc);
+  return launch_status();
+}
+
+extern "C" int qg_tile_scan(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,
+                            uint8_t* zero_flags, int64_t* degrees, int64_t* zero_count, int32_t* blk_list,
+                            int32_t* blk_count, void* stream) {
+  if (!a_words || padded_rows % 8 || padded_cols % 128 || rows > padded_rows) return QG_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rt = padded_rows / 8;
+  if (rt > 0 && (zero_flags || degrees || zero_count))
+    tile_scan_kernel<<<(unsigned)((rt * 32 + 255) / 256), 256, 0, st>>>(a_words, rows, padded_rows, padded_cols,
+                                                                         zero_flags, degrees, zero_count);
+  if (blk_list && blk_count) {
+    const int64_t nrb = (padded_rows + 127) / 128;
+    if (nrb > 0)
+      block_list_kernel<<<(unsigned)((nrb * 32 + 127) / 128), 128, 0, st>>>(a_words, padded_rows, padded_cols,
+                                                                             blk_list, blk_count);
+  }
+  return launch_status();
+}
+
+extern "C" int qg_plane_zero_tiles(const uint32_t* words, int64_t nplanes, int64_t padded_rows,
+                                   int64_t padded_cols, int64_t* zero_counts, void* stream) {
+  if (!words || !zero_counts || padded_rows % 8 || padded_cols % 128) return QG_ERR_ARG;
+  const int64_t n = nplanes * (padded_rows / 8) * (padded_cols / 128);
+  if (n == 0) return QG_OK;
+  plane_zero_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      words, nplanes, padded_rows, padded_cols, zero_counts);
+  return launch_status();
+}
+
+extern "C" int qg_popcount32(const uint32_t* in, int64_t n, int32_t* out, void* stream) {
+  if (n < 0 || (n && (!in || !out))) return QG_ERR_ARG;
+  if (n == 0) return QG_OK;
+  popcount_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(in, n, out);
+  return launch_status();
+}
+
+extern "C" int qg_reduce_planes(const int64_t* accs, int64_t nplanes, int64_t n, int32_t* out, int32_t* overflow,
+                                void* stream) {
+  if (nplanes < 1 || nplanes > 62 || n < 0 || (n && (!accs || !out))) return QG_ERR_ARG;
+  if (n == 0) return QG_OK;
+  reduce_planes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(accs, nplanes, n, out,
+                                                                                      overflow);
+  return launch_status();
+}
+
+namespace qg {
+// One thread per edge: set bit (src, dst) in column-wise words (zero-initialised).
+__global__ void edges_to_bits_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ dst, int64_t n_edges,
+                                     int64_t rows, uint32_t* __restrict__ words, int64_t wpr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_edges) return;
+  const int64_t r = src[i], c = dst[i];
+  if (r < 0 || r >= rows || c < 0) return;
+  atomicOr(words + r * wpr + (c >> 5), 1u << (c & 31));
+}
+}  // namespace qg
+
+extern "C" int qg_edges_to_bits(const int64_t* src, const int64_t* dst, int64_t n_edges, int64_t rows,
+                                uint32_t* words, int64_t padded_rows, int64_t padded_cols, void* stream) {
+  if (!words || n_edges < 0 || (n_edges && (!src || !dst)) || padded_cols % 128 || rows > padded_rows)
+    return QG_ERR_ARG;
+  if (n_edges == 0) return QG_OK;
+  qg::edges_to_bits_kernel<<<(unsigned)((n_edges + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      src, dst, n_edges, rows, words, padded_cols / 32);
+  return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA;
+}

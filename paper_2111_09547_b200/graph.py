@@ -1,0 +1,284 @@
+"""Block-diagonal subgraph batches and their single-transfer compound buffer.
+
+Mirror of the batch side of graph.py (graph.py:265-440).  Graph IO and the
+BFS partitioner (graph.py:85-262) are host preprocessing outside the
+reference's timed region and out of this package's scope: partitions are
+supplied as ``PartitionAssignment`` (the METIS-import path, graph.py:232-256).
+
+Batch construction runs on the GPU: kept intra-part edges are written
+straight into packed adjacency words (``qg_edges_to_bits``; no dense
+total x total matrix), features go through the fused bit_qnt kernel.
+``unpack_batch`` moves a whole QGTB compound buffer with ONE host-to-device
+copy and carves device views out of it.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .bitpack import (COLUMN_WISE, ROW_WISE, BitPlaneStack, PackedBitMatrix, _HEADER as _STACK_HEADER,
+                      deserialize, pad8, pad128, serialize)
+from .errors import FormatError
+from .quantize import QuantParams, quantize_pack_device
+
+BUFFER_MAGIC = b"QGTB"
+_BUFFER_HEADER = struct.Struct("<4sHIIBddBQQ")
+
+
+@dataclass(eq=False)
+class Graph:
+    """Directed edge set over ``num_nodes`` nodes, duplicates collapsed (graph.py:48-82)."""
+
+    num_nodes: int
+    edges: np.ndarray
+    features: np.ndarray | None = None
+
+    def __post_init__(self):
+        e = np.asarray(self.edges, dtype=np.int64).reshape(-1, 2)
+        if e.size:
+            if e.min() < 0 or e.max() >= self.num_nodes:
+                raise ValueError("edge endpoint out of range")
+            e = np.unique(e, axis=0)
+        self.edges = e
+        if self.features is not None:
+            self.features = np.asarray(self.features, dtype=np.float64)
+            if self.features.shape[0] != self.num_nodes:
+                raise ValueError("feature row count must equal num_nodes")
+        self._dev_edges = None
+
+    @property
+    def num_edges(self) -> int:
+        return len(self.edges)
+
+    def device_edges(self) -> torch.Tensor:
+        if self._dev_edges is None:
+            self._dev_edges = N.to_device(self.edges)
+        return self._dev_edges
+
+
+@dataclass(eq=False)
+class PartitionAssignment:
+    """Node -> part map (graph.py:159-175); members served from a cached CSR."""
+
+    num_parts: int
+    part_of: np.ndarray
+    edge_cut: int | None = None
+
+    def __post_init__(self):
+        self.part_of = np.asarray(self.part_of, dtype=np.int64)
+        if self.part_of.size and (self.part_of.min() < 0 or self.part_of.max() >= self.num_parts):
+            raise ValueError("part index out of range")
+        self._csr = None
+
+    def members(self, part: int) -> np.ndarray:
+        if self._csr is None:
+            order = np.argsort(self.part_of, kind="stable")
+            starts = np.searchsorted(self.part_of[order], np.arange(self.num_parts + 1))
+            self._csr = (order, starts)
+        order, starts = self._csr
+        return order[starts[part]:starts[part + 1]]
+
+
+class SubgraphBatch:
+    """Block-diagonal binarized adjacency + quantized features (graph.py:265-305).
+
+    ``node_ids`` / ``boundaries`` are host metadata; adjacency and features are
+    device-resident.  ``degrees()`` comes from the cached tile scan.
+    """
+
+    def __init__(self, node_ids, adjacency: PackedBitMatrix, features: BitPlaneStack | None, boundaries,
+                 x_params: QuantParams | None = None, feat_row_sums: torch.Tensor | None = None):
+        self.node_ids = np.asarray(node_ids, dtype=np.int64)
+        self.boundaries = np.asarray(boundaries, dtype=np.int64)
+        self.adjacency = adjacency
+        self.features = features
+        self.x_params = x_params
+        self._feat_row_sums = feat_row_sums
+        total = len(self.node_ids)
+        if self.boundaries[0] != 0 or self.boundaries[-1] != total:
+            raise ValueError("boundaries must start at 0 and end at total nodes")
+        if adjacency.logical_rows != total or adjacency.logical_cols != total:
+            raise ValueError("adjacency must be square over the batch nodes")
+
+    @property
+    def total_nodes(self) -> int:
+        return len(self.node_ids)
+
+    @property
+    def num_subgraphs(self) -> int:
+        return len(self.boundaries) - 1
+
+    def degrees(self) -> np.ndarray:
+        """Out-degree per batch row from the packed adjacency, int64 (graph.py:292-295)."""
+        from .bitgemm import _schedule
+        return _schedule(self.adjacency).degrees.cpu().numpy()
+
+    def __eq__(self, other):
+        return (isinstance(other, SubgraphBatch) and np.array_equal(self.node_ids, other.node_ids)
+                and np.array_equal(self.boundaries, other.boundaries) and self.adjacency == other.adjacency
+                and self.features == other.features and self.x_params == other.x_params)
+
+    __hash__ = None
+
+
+def _local_edges(g: Graph, assign: PartitionAssignment, groups, node_ids: np.ndarray):
+    """Kept (intra-part) edges in batch-local indices, on the device (graph.py:328-338)."""
+    dev = N.device()
+    e = g.device_edges()
+    if e.numel() == 0:
+        z = torch.zeros(0, dtype=torch.int64, device=dev)
+        return z, z
+    local = torch.full((g.num_nodes,), -1, dtype=torch.int64, device=dev)
+    local[N.to_device(node_ids)] = torch.arange(len(node_ids), device=dev)
+    block_of = torch.full((g.num_nodes,), -1, dtype=torch.int64, device=dev)
+    for b, gr in enumerate(groups):
+        block_of[N.to_device(gr)] = b
+    s, d = e[:, 0], e[:, 1]
+    keep = (block_of[s] >= 0) & (block_of[s] == block_of[d])
+    return local[s[keep]], local[d[keep]]
+
+
+def build_batch(g: Graph, assign: PartitionAssignment, part_ids, x_quant: QuantParams | None = None, *,
+                add_self_loops: bool = True) -> SubgraphBatch:
+    """Induced block-diagonal batch for ``part_ids`` (graph.py:308-357), built on the GPU."""
+    part_ids = list(part_ids)
+    if len(part_ids) != len(set(part_ids)):
+        raise ValueError("part_ids must be distinct")
+    groups = [assign.members(p) for p in part_ids]
+    node_ids = np.concatenate(groups) if groups else np.zeros(0, dtype=np.int64)
+    total = len(node_ids)
+    if total == 0:
+        raise ValueError("empty batch")
+    boundaries = np.cumsum([0] + [len(gr) for gr in groups])
+    src, dst = _local_edges(g, assign, groups, node_ids)
+    if add_self_loops:
+        diag = torch.arange(total, device=src.device, dtype=torch.int64)
+        src, dst = torch.cat([src, diag]), torch.cat([dst, diag])
+    pr, pc = pad8(total), pad128(total)
+    words = torch.zeros(pr * pc // 32, dtype=torch.int32, device=src.device)
+    N.call("qg_edges_to_bits", N.ptr(src.contiguous()), N.ptr(dst.contiguous()), src.numel(), total,
+           N.ptr(words), pr, pc, N.stream())
+    adjacency = PackedBitMatrix(COLUMN_WISE, total, total, pr, pc, words)
+    features, row_sums = None, None
+    if g.features is not None:
+        if x_quant is None:
+            raise ValueError("x_quant is required to quantize node features")
+        r = quantize_pack_device(g.features[node_ids], x_quant, N.ROW_WISE_ID, 8, row_sums=True)
+        features = BitPlaneStack._wrap(ROW_WISE, r["rows"], r["cols"], r["pr"], r["pc"], r["planes"])
+        row_sums = r["row_sums"]
+    return SubgraphBatch(node_ids=node_ids, adjacency=adjacency, features=features, boundaries=boundaries,
+                         x_params=x_quant, feat_row_sums=row_sums)
+
+
+@dataclass(eq=False)
+class CompoundBuffer:
+    """One contiguous byte image of a batch (graph.py:360-371)."""
+
+    data: bytes
+
+    @property
+    def nbytes(self) -> int:
+        return len(self.data)
+
+    def __eq__(self, other):
+        return isinstance(other, CompoundBuffer) and self.data == other.data
+
+
+def pack_batch(b: SubgraphBatch) -> CompoundBuffer:
+    """Serialize a batch into one transfer object, byte-identical to graph.py:374-397."""
+    adj_stack = BitPlaneStack._wrap(COLUMN_WISE, *b.adjacency.dims(), b.adjacency.dwords.reshape(1, -1))
+    adj_bytes = serialize(adj_stack)
+    feat_bytes = serialize(b.features) if b.features is not None else b""
+    ns, total = b.num_subgraphs, b.total_nodes
+    fixed = _BUFFER_HEADER.size + 4 * (ns + 1) + 4 * total
+    adj_off = fixed
+    feat_off = adj_off + len(adj_bytes) if feat_bytes else 0
+    if b.x_params is not None:
+        amin, amax, bits = b.x_params.alpha_min, b.x_params.alpha_max, b.x_params.bits
+    else:
+        amin, amax, bits = 0.0, 0.0, 0
+    fbits = b.features.bits if b.features is not None else 0
+    header = _BUFFER_HEADER.pack(BUFFER_MAGIC, 1, ns, total, fbits, amin, amax, bits, adj_off, feat_off)
+    body = (header + b.boundaries.astype("<u4").tobytes() + b.node_ids.astype("<u4").tobytes()
+            + adj_bytes + feat_bytes)
+    return CompoundBuffer(data=body)
+
+
+def _parse_stack_header(data, off, end):
+    if end - off < _STACK_HEADER.size:
+        raise FormatError("payload shorter than header")
+    return _STACK_HEADER.unpack_from(data, off)
+
+
+def unpack_batch(buf, *, pinned: bool = False) -> SubgraphBatch:
+    """Inverse of pack_batch (graph.py:400-431): ONE host-to-device copy of the buffer.
+
+    The header is validated on the host; adjacency and feature words become
+    device views into the transferred buffer (re-aligned to 16 B on device
+    when the section offset is not, since the GEMM kernels use 128-bit loads).
+    """
+    data = buf.data if isinstance(buf, CompoundBuffer) else bytes(buf)
+    if len(data) < _BUFFER_HEADER.size:
+        raise FormatError("compound buffer shorter than header")
+    magic, version, ns, total, fbits, amin, amax, bits, adj_off, feat_off = _BUFFER_HEADER.unpack_from(data)
+    if magic != BUFFER_MAGIC:
+        raise FormatError(f"bad compound-buffer magic {magic!r}")
+    if version != 1:
+        raise FormatError(f"unsupported compound-buffer version {version}")
+    off = _BUFFER_HEADER.size
+    need = off + 4 * (ns + 1) + 4 * total
+    if len(data) < need or adj_off != need:
+        raise FormatError("corrupt compound-buffer header")
+    boundaries = np.frombuffer(data, dtype="<u4", count=ns + 1, offset=off).astype(np.int64)
+    node_ids = np.frombuffer(data, dtype="<u4", count=total, offset=off + 4 * (ns + 1)).astype(np.int64)
+    adj_end = feat_off if feat_off else len(data)
+    sections = [(adj_off, adj_end)] + ([(feat_off, len(data))] if feat_off else [])
+    metas = []
+    for (s0, s1) in sections:
+        magic2, ver2, orient, sbits, lr, lc, pr, pc = _parse_stack_header(data, s0, s1)
+        if magic2 != b"QGTC":
+            raise FormatError(f"bad magic {magic2!r}")
+        if ver2 != 1:
+            raise FormatError(f"unsupported version {ver2}")
+        if orient not in (0, 1):
+            raise FormatError(f"bad orientation byte {orient}")
+        if not 1 <= sbits <= 64:
+            raise FormatError(f"bad plane count {sbits}")
+        if s1 - s0 != _STACK_HEADER.size + sbits * (pr * pc // 32) * 4:
+            raise FormatError(f"payload length {s1 - s0} != expected "
+                              f"{_STACK_HEADER.size + sbits * (pr * pc // 32) * 4}")
+        metas.append((orient, sbits, lr, lc, pr, pc))
+    if metas[0][1] != 1:
+        raise FormatError("adjacency section must be a 1-bit stack")
+    if feat_off and metas[1][1] != fbits:
+        raise FormatError("feature bit count disagrees with header")
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+    if pinned:
+        host = host.pin_memory()
+    dev_buf = host.to(N.device(), non_blocking=pinned)          # the single H2D transfer
+    stacks = []
+    for (s0, _), (orient, sbits, lr, lc, pr, pc) in zip(sections, metas):
+        w0 = s0 + _STACK_HEADER.size
+        nbytes = sbits * (pr * pc // 32) * 4
+        view = dev_buf[w0:w0 + nbytes]
+        if w0 % 16:
+            view = view.clone()
+        words = view.view(torch.int32).reshape(sbits, -1)
+        stacks.append(BitPlaneStack._wrap(COLUMN_WISE if orient == 0 else ROW_WISE, lr, lc, pr, pc, words))
+    params = QuantParams(amin, amax, bits) if fbits else None
+    return SubgraphBatch(node_ids=node_ids, adjacency=stacks[0].planes[0],
+                         features=stacks[1] if feat_off else None, boundaries=boundaries, x_params=params)
+
+
+def float32_dense_bytes(b: SubgraphBatch) -> int:
+    """Size of the naive float32 dense encoding of the same batch (graph.py:434-440)."""
+    n = b.total_nodes
+    size = 4 * n * n
+    if b.features is not None:
+        size += 4 * n * b.features.logical_cols
+    return size
