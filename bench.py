@@ -1,0 +1,428 @@
+"""QGTC B200 benchmark (driver contract).
+
+Metric (BASELINE.json): QGNN inference ms/epoch per bitwidth, plus bit-GEMM
+effective TOPS vs the tensor-pipe peak.  Workload at N=1: configs[1] -- a
+3-layer GIN (hidden 64) over a synthetic BlogCatalog-shaped graph (10k nodes,
+334k undirected edges, 16 planted parts in one batch), bit sweep 1..8; the
+headline is the 4-bit point (the reference CLI default, cli.py:112-113).
+
+A step = one epoch = the reference's timed region (cli.py:215-222): every
+batch through model_forward.  Ours replays it as ONE CUDA graph (tile scan +
+fused bit-GEMMs).  `value` is device-resident ms/epoch (L2 flushed between
+steps, events around each step); `e2e` is the same epoch through the public
+runtime with pinned host QGT2 images -> H2D -> graph -> fp64 logits D2H.
+
+`--impl reference` times the reference algorithm's CPU port (oracle/) on all
+host cores (process pool over the independent subgraph parts) on the same
+config.  N>1 (torchrun): weak scaling -- every rank runs its own epoch
+replica (different seed), value = total time / epochs of all ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+INT8_PEAK_FILE = os.path.join(ROOT, "profiles", "int8_peak.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--config", default="C2")
+    p.add_argument("--bits", type=int, default=4)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-sample-s", type=float, default=12.0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """NVML sampler of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index=0, period=0.002):
+        self.samples, self.reasons, self.period = [], set(), period
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def int8_peak_tops():
+    if os.path.exists(INT8_PEAK_FILE):
+        with open(INT8_PEAK_FILE) as fh:
+            d = json.load(fh)
+        return float(d["int8_tops"]), d.get("source", INT8_PEAK_FILE)
+    bf16 = json.load(open(MEASURED))["bf16_tflops"] if os.path.exists(MEASURED) else 1590.0
+    return 2.0 * bf16, "2 x measured bf16 (MEASURED_PEAKS.json)"
+
+
+# --------------------------------------------------------------- workload
+def build_workload(cfg_name, bits, seed):
+    from paper_2111_09547_b200 import synth
+    cfg = synth.with_bits(synth.CONFIGS[cfg_name], bits)
+    batches, feats, _ = synth.planted_batches(cfg, seed=seed)
+    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=seed)
+    return cfg, batches, feats, model
+
+
+def time_device_epochs(runner, steps, warmup, world):
+    import torch
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    st = runner.stream
+    with torch.cuda.stream(st):
+        for _ in range(warmup):
+            flush.zero_()
+            runner.run()
+    torch.cuda.synchronize()
+    barrier(world)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    sampler = ClockSampler(torch.cuda.current_device())
+    with sampler:
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            for s, e in ev:
+                flush.zero_()
+                s.record(st)
+                runner.run()
+                e.record(st)
+        torch.cuda.synchronize()
+    barrier(world)
+    total_ms = sum(s.elapsed_time(e) for s, e in ev)
+    return total_ms, sampler.summary()
+
+
+def time_e2e(host_runner, steps, warmup, world):
+    import torch
+    st = host_runner.stream
+    for _ in range(warmup):
+        host_runner.run_host()
+        st.synchronize()
+    barrier(world)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0 = time.perf_counter()
+    for s, e in ev:
+        s.record(st)
+        out = host_runner.run_host()
+        e.record(st)
+        st.synchronize()            # the caller reads the logits every step
+        _ = float(out[0, 0])
+    wall = (time.perf_counter() - t0) * 1e3
+    barrier(world)
+    return sum(s.elapsed_time(e) for s, e in ev), wall
+
+
+def kernel_roofline(model, batches, reps=20):
+    """Average duration of the bit-GEMM launches of one epoch (events on the launch stream)."""
+    import torch
+    from paper_2111_09547_b200 import bitgemm, engine
+    rec = []
+    bitgemm.PROFILE_HOOK = rec
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            for b in batches:
+                engine.model_forward_device(b, model)
+        torch.cuda.synchronize()
+        rec.clear()
+        # park the GPU so the host enqueues every launch first: events then bracket
+        # back-to-back kernels, not host gaps
+        torch.cuda._sleep(int(3e8))
+        for _ in range(reps):
+            for b in batches:
+                engine.model_forward_device(b, model)
+        torch.cuda.synchronize()
+    bitgemm.PROFILE_HOOK = None
+    dur = sum(s.elapsed_time(e) for s, e, _ in rec) / reps        # ms per epoch in bit-GEMMs
+    ops = sum(o for _, _, o in rec) / reps
+    launches = len(rec) / reps
+    return dur, ops, launches
+
+
+# ------------------------------------------------------------- CPU oracle
+def _oracle_part_inputs(batch, feats, parts):
+    """Host operands of the first `parts` subgraphs (block-diagonal => independent)."""
+    from oracle import qgtc_oracle as O
+    hi = int(batch.boundaries[parts])
+    a = batch.adjacency
+    dense = O.unpack_words(a.words, O.COL, a.logical_rows, a.logical_cols, a.padded_rows, a.padded_cols)
+    sub = np.ascontiguousarray(dense[:hi, :hi])
+    aw, pr, pc = O.pack_words(sub, O.COL, 8)
+    return aw, (hi, hi, pr, pc), np.asarray(feats[:hi], dtype=np.float64)
+
+
+def _oracle_forward(args):
+    aw, dims, feats, x, layers = args
+    sys.path.insert(0, ROOT)
+    from oracle import qgtc_oracle as O
+    codes = O.quantize_codes(feats, x.alpha_min, x.alpha_max, x.bits)
+    return O.model_forward(aw, dims, codes, x, layers)
+
+
+def _part_slices(batch, feats):
+    from oracle import qgtc_oracle as O
+    a = batch.adjacency
+    dense = O.unpack_words(a.words, O.COL, a.logical_rows, a.logical_cols, a.padded_rows, a.padded_cols)
+    out = []
+    for p in range(batch.num_subgraphs):
+        lo, hi = int(batch.boundaries[p]), int(batch.boundaries[p + 1])
+        aw, pr, pc = O.pack_words(np.ascontiguousarray(dense[lo:hi, lo:hi]), O.COL, 8)
+        out.append((aw, (hi - lo, hi - lo, pr, pc), np.asarray(feats[lo:hi], dtype=np.float64)))
+    return out
+
+
+def cpu_baseline(batches, feats, model, x_params, logits_dev, budget_s):
+    """Single-thread oracle on the first parts of batch 0; extrapolated to the epoch."""
+    b0 = batches[0]
+    parts = 1
+    t_used, out = None, None
+    while True:
+        args = _oracle_part_inputs(b0, feats[0], parts) + (x_params, model.layers)
+        t0 = time.perf_counter()
+        out = _oracle_forward(args)
+        t_used = time.perf_counter() - t0
+        if t_used * 2 > budget_s or parts * 2 > b0.num_subgraphs:
+            break
+        parts *= 2
+    hi = int(b0.boundaries[parts])
+    exact = bool(np.array_equal(out, logits_dev[0][:hi].cpu().numpy()))
+    total_parts = sum(b.num_subgraphs for b in batches)
+    ms_epoch = t_used * 1e3 * total_parts / parts
+    return {"value": ms_epoch, "unit": "ms/epoch", "cores": 1, "kind": "port",
+            "sample": f"oracle/qgtc_oracle.model_forward on {parts}/{total_parts} subgraph parts "
+                      f"({hi} nodes, {t_used:.1f} s), x{total_parts / parts:g} extrapolated",
+            "parity_on_sample": "bit-exact" if exact else "MISMATCH"}
+
+
+# ----------------------------------------------------------- reference arm
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cfg, batches, feats, model = build_workload(args.config, args.bits, seed=0)
+    x = batches[0].x_params
+    jobs = []
+    for b, f in zip(batches, feats):
+        for sl in _part_slices(b, f):
+            jobs.append(sl + (x, model.layers))
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    # bounded: cap the timed loop so the whole run stays within a few minutes
+    with ctx.Pool(min(cores, len(jobs))) as pool:
+        t0 = time.perf_counter()
+        pool.map(_oracle_forward, jobs, chunksize=1)
+        one = time.perf_counter() - t0
+        budget = 150.0
+        steps = max(1, min(steps, int(budget / max(one, 1e-3))))
+        warm = min(warm, 1)
+        for _ in range(warm):
+            pool.map(_oracle_forward, jobs, chunksize=1)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            pool.map(_oracle_forward, jobs, chunksize=1)
+            times.append(time.perf_counter() - t0)
+    ms = float(np.mean(times)) * 1e3
+    line = {
+        "metric": "QGNN inference ms/epoch (GIN 3x64, 4-bit); bit-GEMM effective TOPS",
+        "value": ms, "unit": "ms/epoch", "impl": "reference", "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": f"u{args.bits}", "data": "synthetic",
+        "config": {"workload": cfg.name, "bits": args.bits, "nodes": cfg.num_nodes,
+                   "edges_undirected": cfg.num_edges, "parts": cfg.num_parts},
+        "cpu_baseline": {"value": ms, "unit": "ms/epoch", "cores": min(cores, len(jobs)), "kind": "port",
+                         "sample": f"full epoch: {len(jobs)} independent subgraph parts over a "
+                                   f"{min(cores, len(jobs))}-process pool (oracle/qgtc_oracle.py)"},
+        "e2e": {"value": ms, "unit": "ms/epoch", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours
+def ours(args, world, rank):
+    import torch
+    from paper_2111_09547_b200 import _native as N
+    from paper_2111_09547_b200.runtime import EpochRunner, HostEpochRunner
+
+    N.lib()
+    cfg, batches, feats, model = build_workload(args.config, args.bits, seed=rank)
+    runner = EpochRunner(model, batches).capture()
+    total_ms, clocks = time_device_epochs(runner, args.steps, args.warmup, world)
+    total_ms = max_over_ranks(world, total_ms)
+    ms_epoch = total_ms / (args.steps * world)
+    launches = runner.kernel_launches_per_epoch() * args.steps
+
+    # end to end through the public runtime: pinned H2D -> graph -> D2H every step
+    host = HostEpochRunner(model, batches)
+    e2e_ms, e2e_wall = time_e2e(host, args.steps, min(args.warmup, 5), world)
+    e2e_ms = max_over_ranks(world, e2e_ms) / (args.steps * world)
+
+    # parity of the e2e path against the device path
+    with torch.cuda.stream(runner.stream):
+        dev_logits = torch.cat([o for o in runner.run()])
+    torch.cuda.synchronize()
+    dev_logits = dev_logits.cpu()
+    host_out = host.run_host()
+    host.stream.synchronize()
+    e2e_parity = bool(torch.equal(dev_logits, host_out))
+
+    # roofline of the dominant kernel (bit-GEMM) -- algorithmic int8-MAC work per launch
+    gemm_ms, gemm_ops, gemm_launches = kernel_roofline(model, batches)
+    peak, peak_src = int8_peak_tops()
+    achieved = gemm_ops / (gemm_ms * 1e-3) / 1e12
+    traffic = None
+    if os.path.exists(PROFILE_SUMMARY):
+        try:
+            traffic = json.load(open(PROFILE_SUMMARY)).get("bitgemm_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    eff_tops = 2.0 * sum(
+        b.total_nodes * b.total_nodes * (ly.out_dim if ly.order == "update-then-aggregate" else ly.in_dim)
+        for b in batches for ly in model.layers) / (ms_epoch * 1e-3) / 1e12
+
+    sweep = {}
+    if not args.no_sweep:
+        for bits in range(1, 9):
+            if bits == args.bits:
+                sweep[str(bits)] = round(ms_epoch, 5)
+                continue
+            _, bb, _, mm = build_workload(args.config, bits, seed=rank)
+            rr = EpochRunner(mm, bb).capture()
+            k = max(20, args.steps // 4)
+            t, _ = time_device_epochs(rr, k, 5, world)
+            sweep[str(bits)] = round(max_over_ranks(world, t) / (k * world), 5)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(batches, feats, model, batches[0].x_params, runner.run(), args.cpu_sample_s)
+
+    if rank != 0:
+        return
+    line = {
+        "metric": "QGNN inference ms/epoch (GIN 3x64, 4-bit); bit-GEMM effective TOPS",
+        "value": round(ms_epoch, 5), "unit": "ms/epoch", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_epoch, 5), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": f"u{args.bits} codes / s32 acc / fp64 epilogue",
+        "data": "synthetic planted-partition graph, U[0,1) features, random-init weights",
+        "config": {"workload": cfg.name, "model": "batched-gin 3 layers hidden 64", "bits": args.bits,
+                   "nodes": cfg.num_nodes, "edges_undirected": cfg.num_edges, "parts": cfg.num_parts,
+                   "batches": len(batches), "in_dim": cfg.in_dim, "classes": cfg.classes,
+                   "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}"},
+        "sweep_ms_per_epoch_by_bits": sweep,
+        "effective_tops": round(eff_tops, 3),
+        "roofline": {"bound": "tensor", "kernel": "tc_bitgemm_kernel (tcgen05.mma kind::i8)",
+                     "achieved": round(achieved, 3), "peak": peak, "unit": "TOPS",
+                     "frac": round(achieved / peak, 5), "traffic": traffic, "peak_source": peak_src,
+                     "work": "2 x 1024 x N_padded int8-MACs per non-zero 8x128 left tile (one u8 MAC "
+                             "retires all bit-plane pairs); durations from CUDA events per launch",
+                     "launches_per_epoch": gemm_launches, "kernel_ms_per_epoch": round(gemm_ms, 5),
+                     "kernel_share_of_step": round(gemm_ms / ms_epoch, 3)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_ms, 5), "unit": "ms/epoch", "h2d_bytes_per_step": host.h2d_bytes,
+                "d2h_bytes_per_step": host.d2h_bytes, "wall_ms_per_step": round(e2e_wall / args.steps, 5),
+                "parity_vs_device_path": "bit-exact" if e2e_parity else "MISMATCH",
+                "path": "pinned QGT2 images -> 1 H2D -> epoch CUDA graph -> fp64 logits -> 1 D2H"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, _ = dist_setup()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+    else:
+        ours(args, world, rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -121,7 +121,7 @@ int qg_repack(const uint32_t* src, int64_t nplanes, int64_t src_pr, int64_t src_
  *   zero_flags: optional u8 [pr/8][pc/128] (1 = all-zero tile)
  *   degrees:    optional int64 [rows]
  *   zero_count: optional int64 [1], ACCUMULATED (caller zeroes)
- *   blk_list / blk_count: optional per-128-row-block lists of non-zero
+ *   blk_list / blk_count: optional (requires zero_flags) per-128-row-block lists of non-zero
  *     128-bit K tiles (the zero-tile-jumping schedule of the GEMM kernels):
  *     blk_list[rb * (pc/128) + i], i < blk_count[rb].
  */
@@ -151,6 +151,8 @@ typedef struct {
   const double* bn_denom;      /* sqrt(var + eps), host-computed                  */
   const double* bn_gamma;
   const double* bn_beta;
+  const double* bn_inv_denom;  /* RN(1 / bn_denom), host-computed (fast exact division) */
+  double q_inv_scale;          /* RN(1 / q_scale), host-computed                       */
   int32_t out_kind;            /* QG_OUT_REAL / QG_OUT_PLANES                     */
   int32_t q_bits;              /* requant grid (quantize.py:93-105)               */
   double q_amin, q_scale;
@@ -187,6 +189,8 @@ typedef struct {
   const qg_epilogue* epi;      /* EPILOGUE mode                                   */
   int32_t* overflow;           /* optional device flag, set to 1 on int32 overflow */
   int32_t* scratch_i32;        /* [m][n] scratch for the POPC epilogue path       */
+  int64_t* phase_ns;           /* optional profiling hook: per CTA 6 %globaltimer stamps
+                                  (entry, setup done, MMAs done, epilogue computed, stored, exit) */
   int32_t cross_bit;           /* PER_PLANE: 1 = one plane per CTA (cross-bit reuse),
                                   0 = planes stacked along N so each L tile is
                                   expanded once for all planes (cross-tile reuse) */
@@ -215,6 +219,12 @@ int qg_reduce_planes(const int64_t* accs, int64_t nplanes, int64_t n, int32_t* o
  * pack_colwise of build_batch (graph.py:334-342) without a dense matrix. */
 int qg_edges_to_bits(const int64_t* src, const int64_t* dst, int64_t n_edges, int64_t rows,
                      uint32_t* words, int64_t padded_rows, int64_t padded_cols, void* stream);
+
+/* Test hook: out[i] = a[i] / b[i] through the epilogue's division routine
+ * (Markstein reciprocal sequence + IEEE fallback) and ref[i] through IEEE
+ * __ddiv_rn, so tests can prove the fast path is correctly rounded. */
+int qg_test_div(const double* a, const double* b, const double* inv_b, int64_t n, double* out, double* ref,
+                void* stream);
 
 /* popcount32 (bitgemm.py:58-60) on the device. */
 int qg_popcount32(const uint32_t* in, int64_t n, int32_t* out, void* stream);

@@ -31,7 +31,7 @@ STATUS_CLEAR = 0x7F7F7F7F7F7F7F7F
 # every compute entry point declared in include/qgtc_b200.h
 EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes", "qg_unpack", "qg_repack",
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
-           "qg_popcount32", "qg_edges_to_bits")
+           "qg_popcount32", "qg_edges_to_bits", "qg_test_div")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -44,8 +44,8 @@ class Epilogue(ctypes.Structure):
         ("use_const", ctypes.c_int32),
         ("k_acc", _f64), ("k_row", _f64), ("k_col", _f64), ("k_const", _f64),
         ("row_sums", _vp), ("col_sums", _vp), ("bias", _vp),
-        ("bn_mean", _vp), ("bn_denom", _vp), ("bn_gamma", _vp), ("bn_beta", _vp),
-        ("out_kind", ctypes.c_int32), ("q_bits", ctypes.c_int32),
+        ("bn_mean", _vp), ("bn_denom", _vp), ("bn_gamma", _vp), ("bn_beta", _vp), ("bn_inv_denom", _vp),
+        ("q_inv_scale", _f64), ("out_kind", ctypes.c_int32), ("q_bits", ctypes.c_int32),
         ("q_amin", _f64), ("q_scale", _f64),
         ("q_orientation", ctypes.c_int32), ("pad_", ctypes.c_int32),
         ("q_prows", _i64), ("q_pcols", _i64),
@@ -64,7 +64,7 @@ class GemmArgs(ctypes.Structure):
         ("blk_list", _vp), ("blk_count", _vp),
         ("mode", ctypes.c_int32), ("algo", ctypes.c_int32),
         ("out_i32", _vp), ("epi", ctypes.POINTER(Epilogue)), ("overflow", _vp), ("scratch_i32", _vp),
-        ("cross_bit", ctypes.c_int32), ("pad2", ctypes.c_int32),
+        ("phase_ns", _vp), ("cross_bit", ctypes.c_int32), ("pad2", ctypes.c_int32),
     ]
 
 
@@ -93,6 +93,7 @@ def lib() -> ctypes.CDLL:
             "qg_reduce_planes": ([_vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
             "qg_popcount32": ([_vp, _i64, _vp, _vp], ctypes.c_int),
             "qg_edges_to_bits": ([_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp], ctypes.c_int),
+            "qg_test_div": ([_vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)

@@ -216,8 +216,10 @@ def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, b
         e.bias = b.data_ptr()
     if bn is not None:
         vecs = [_dev_vec(v, torch.float64) for v in bn]
+        if len(vecs) == 4:   # RN(1/denom): IEEE division on the host side of the contract
+            vecs.append(1.0 / vecs[1])
         plan.keep.extend(vecs)
-        e.bn_mean, e.bn_denom, e.bn_gamma, e.bn_beta = (v.data_ptr() for v in vecs)
+        e.bn_mean, e.bn_denom, e.bn_gamma, e.bn_beta, e.bn_inv_denom = (v.data_ptr() for v in vecs)
     e.act = N.ACT[kind]
     if out_params is None:
         plan.out_real = torch.empty((rows, cols), dtype=torch.float64, device=dev)
@@ -228,6 +230,7 @@ def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, b
     planes = torch.zeros((q.bits, pr * pc // 32), dtype=torch.int32, device=dev)
     plan.out_stack = BitPlaneStack._wrap(out_orientation, rows, cols, pr, pc, planes)
     e.out_kind, e.q_bits, e.q_amin, e.q_scale = N.OUT_PLANES, q.bits, q.alpha_min, q.scale
+    e.q_inv_scale = 1.0 / q.scale
     e.q_orientation, e.q_prows, e.q_pcols, e.q_planes = orient_id(out_orientation), pr, pc, planes.data_ptr()
     if want_row_sums:
         plan.row_sums = torch.zeros(rows, dtype=torch.int64, device=dev)
@@ -323,6 +326,18 @@ def _plane_zero_tiles(stack: BitPlaneStack) -> list[int]:
 
 
 # --------------------------------------------------------------- the GEMM
+PROFILE_HOOK = None   # bench.py: list receiving (start_event, end_event, algorithmic_ops) per launch
+PHASE_HOOK = None     # tools/: list receiving (grid_ctas, int64 [ctas, 6] %globaltimer stamps) per launch
+
+
+def _launch_work(mp, kp, np_, rbits, mode, schedule):
+    """Algorithmic int8-MAC ops of one launch: 2 x 1024 x N_padded per non-zero 8x128 left tile."""
+    tiles = (mp // TILE_ROWS) * (kp // TILE_K_BITS)
+    if schedule is not None:
+        tiles -= schedule.zeros
+    return 2.0 * 1024 * np_ * tiles * (rbits if mode == N.GEMM_PER_PLANE else 1)
+
+
 def gemm_device(lhs_dwords, lbits, m, mp, k, kp, rhs_dwords, rbits, n, np_, *, mode, schedule=None,
                 out=None, epi_struct=None, algo="auto", cross_bit=False, overflow=None, scratch=None):
     """Launch qg_bitgemm on device tensors (no syncs)."""
@@ -341,6 +356,18 @@ def gemm_device(lhs_dwords, lbits, m, mp, k, kp, rhs_dwords, rbits, n, np_, *, m
         args.overflow = overflow.data_ptr()
     if scratch is not None:
         args.scratch_i32 = scratch.data_ptr()
+    if PHASE_HOOK is not None:
+        ctas = max(1, (mp + 127) // 128) * 64
+        stamps = torch.zeros((ctas, 70), dtype=torch.int64, device=lhs_dwords.device)
+        args.phase_ns = stamps.data_ptr()
+        PHASE_HOOK.append(stamps)
+    if PROFILE_HOOK is not None:
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        N.check(N.lib().qg_bitgemm(args, N.stream()), "qg_bitgemm")
+        e_ev.record()
+        PROFILE_HOOK.append((s_ev, e_ev, _launch_work(mp, kp, np_, rbits, mode, schedule)))
+        return
     N.check(N.lib().qg_bitgemm(args, N.stream()), "qg_bitgemm")
 
 

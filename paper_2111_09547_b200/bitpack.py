@@ -209,6 +209,8 @@ def _pack_device(t: torch.Tensor, orientation: str, pad_to: int):
         t = t.to(torch.uint8)
     t = t.contiguous()
     words = torch.empty((bits, pr * pc // 32), dtype=torch.int32, device=t.device)
+    if words.numel() == 0:
+        return BitPlaneStack._wrap(orientation, rows, cols, pr, pc, words)
     status = N.new_status()
     N.call("qg_pack_planes", N.ptr(t), bits, rows, cols, orient_id(orientation), pad_to, N.ptr(words),
            N.ptr(status), N.stream())
@@ -250,6 +252,9 @@ def unpack(p: PackedBitMatrix) -> np.ndarray:
 def _unpack_device(dwords2d, orientation, rows, cols, pr, pc, codes=False):
     bits = dwords2d.shape[0]
     dev = dwords2d.device
+    if rows * cols == 0:
+        return torch.zeros((rows, cols) if codes else (bits, rows, cols),
+                           dtype=torch.int32 if codes else torch.uint8, device=dev)
     if codes:
         out = torch.empty((rows, cols), dtype=torch.int32, device=dev)
         N.call("qg_unpack", N.ptr(dwords2d), bits, rows, cols, pr, pc, orient_id(orientation), None,

@@ -27,6 +27,52 @@ __device__ __forceinline__ uint32_t quantize_code(double x, double amin, double 
   return (uint32_t)v;
 }
 
+// Correctly rounded a / b from y = RN(1/b) (host-computed): q0 = a*y, one
+// Newton correction makes q1 faithful, then Markstein's theorem makes
+// q2 = RN(q1 + (a - b*q1)*y) the correctly rounded quotient, with the
+// remainders exact through fma.  Outside a safe exponent range (zero,
+// subnormal, huge, inf/nan) it falls back to the IEEE division, so the result
+// is always bit-identical to __ddiv_rn(a, b) (checked by qg_test_div tests).
+// IEEE fallback kept out of line so the (rare) slow path does not bloat every call site.
+static __device__ __noinline__ double div_rn_ieee(double a, double b) { return __ddiv_rn(a, b); }
+// tanh evaluated at fp32 precision (bitgemm.py:206-207); out of line (rarely used, large)
+static __device__ __noinline__ double tanh_f32(double x) { return (double)(float)tanh(x); }
+
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+  // +-0 / finite b: IEEE gives a zero signed sign(a)^sign(b) == a * y exactly (ReLU
+  // outputs on an alpha_min = 0 grid hit this for half the elements)
+  if (a == 0.0 && fabs(y) < 0x1p+1000) return __dmul_rn(a, y);
+  const double aa = fabs(a), bb = fabs(b);
+  double q = __dmul_rn(a, y);
+  const double qq = fabs(q);
+  if (!(aa < 0x1p+900 && aa > 0x1p-900 && bb < 0x1p+900 && bb > 0x1p-900 && qq < 0x1p+900 && qq > 0x1p-900))
+    return div_rn_ieee(a, b);
+  double r = __fma_rn(-q, b, a);
+  q = __fma_rn(r, y, q);
+  r = __fma_rn(-q, b, a);
+  return __fma_rn(r, y, q);
+}
+
+// Eq.2 requantization with the fast correctly rounded division.
+__device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, double scale, double inv_scale,
+                                                       uint32_t maxv) {
+  double v = floor(div_rn(__dsub_rn(x, amin), scale, inv_scale));
+  if (!(v > 0.0)) return 0u;
+  if (v >= (double)maxv) return maxv;
+  return (uint32_t)v;
+}
+
+// 8x8 bit-matrix transpose of a u64 (byte i = row i): afterwards byte j holds
+// bit j of every input byte (Hacker's Delight 7-3).  Used to turn 8 codes into
+// 8 plane bytes in a handful of ops.
+__device__ __forceinline__ uint64_t transpose8x8(uint64_t x) {
+  uint64_t t;
+  t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;  x = x ^ t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull; x = x ^ t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull; x = x ^ t ^ (t << 28);
+  return x;
+}
+
 // 4 packed bits -> 4 bytes of 0/1 (bit i -> byte i).
 __device__ __forceinline__ uint32_t expand_nibble(uint32_t nib) {
   return (nib * 0x00204081u) & 0x01010101u;
@@ -42,80 +88,97 @@ __device__ __forceinline__ double epi_real(const qg_epilogue& e, int64_t acc, in
   if (e.use_const) real = __dadd_rn(real, e.k_const);
   if (e.bias) real = __dadd_rn(real, e.bias[c]);
   if (e.bn_mean) {
-    real = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(real, e.bn_mean[c]), e.bn_denom[c]), e.bn_gamma[c]),
-                     e.bn_beta[c]);
+    real = __dadd_rn(__dmul_rn(div_rn(__dsub_rn(real, e.bn_mean[c]), e.bn_denom[c], e.bn_inv_denom[c]),
+                               e.bn_gamma[c]), e.bn_beta[c]);
   }
   if (e.act == QG_ACT_RELU) {
     real = (real < 0.0) ? 0.0 : real;
   } else if (e.act == QG_ACT_TANH) {
-    real = (double)(float)tanh(real);     // bitgemm.py:206-207 evaluates tanh at fp32 precision
+    real = tanh_f32(real);
   }
   return real;
 }
 
 // Warp-collective epilogue over a 32-row x 32-column chunk.  Lane l owns row
-// r0 + l and holds v[j] = acc(row, c0 + j).  All 32 lanes must call it.
-// rows/cols are the logical output dims; r0 is a multiple of 32.
-template <typename AccT>
-__device__ __forceinline__ void epi_chunk32(const qg_epilogue& e, int64_t r0, int64_t c0, const AccT* v,
+// r0 + l; `get8(sub, v)` delivers acc(row, c0 + 8*sub + jj) for jj < 8 (TMEM
+// slices in the GEMM, global loads in the stand-alone kernel).  All 32 lanes
+// must call it; r0 and c0 are multiples of 32; rows/cols are logical dims.
+template <typename Get8>
+__device__ __forceinline__ void epi_chunk32(const qg_epilogue& e, int64_t r0, int64_t c0, Get8 get8,
                                             int64_t rows, int64_t cols) {
   const int lane = threadIdx.x & 31;
   const int64_t r = r0 + lane;
   const bool rvalid = r < rows;
   if (e.out_kind == QG_OUT_REAL) {
-    if (rvalid) {
-      double* dst = e.out_real + r * cols;
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        int64_t c = c0 + j;
-        if (c < cols) dst[c] = epi_real(e, (int64_t)v[j], r, c);
+    for (int sub = 0; sub < 4; ++sub) {
+      uint32_t v[8];
+      get8(sub, v);
+      if (rvalid) {
+        double* dst = e.out_real + r * cols;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int64_t c = c0 + sub * 8 + jj;
+          if (c < cols) dst[c] = epi_real(e, (int64_t)(int32_t)v[jj], r, c);
+        }
       }
     }
     return;
   }
-  // requantize -> codes (0 outside the logical matrix so padding stays zero)
+  // requantize -> codes (0 outside the logical matrix so padding stays zero) -> bit planes
   const uint32_t maxv = (1u << e.q_bits) - 1u;
-  uint32_t code[32];
-  int64_t rsum = 0;
+  const bool colwise = e.q_orientation == QG_COLUMN_WISE;
+  uint32_t w[8];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    int64_t c = c0 + j;
-    uint32_t q = 0;
-    if (rvalid && c < cols) {
-      double real = epi_real(e, (int64_t)v[j], r, c);
-      if (!isfinite(real)) status_min(e.status, r * cols + c);
-      q = quantize_code(real, e.q_amin, e.q_scale, maxv);
-      rsum += q;
+  for (int p = 0; p < 8; ++p) w[p] = 0;
+  int64_t rsum = 0;
+  for (int sub = 0; sub < 4; ++sub) {
+    uint32_t v[8];
+    get8(sub, v);
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = sub * 8 + jj;
+      const int64_t c = c0 + j;
+      uint32_t q = 0;
+      if (rvalid && c < cols) {
+        const double real = epi_real(e, (int64_t)(int32_t)v[jj], r, c);
+        if (!isfinite(real)) status_min(e.status, r * cols + c);
+        q = quantize_code_fast(real, e.q_amin, e.q_scale, e.q_inv_scale, maxv);
+        rsum += q;
+      }
+      if (colwise) {
+        // this lane's row: bit j of word (r, c0/32)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) w[p] |= ((q >> p) & 1u) << j;
+      } else {
+        // column c0+j over the warp's 32 rows: lane j keeps the ballot
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          if (p < e.q_bits) {
+            const uint32_t b = __ballot_sync(QG_FULL, (q >> p) & 1u);
+            if (lane == j) w[p] = b;
+          }
+        }
+      }
     }
-    code[j] = q;
   }
   if (e.q_row_sums && rvalid && rsum) atomicAdd(reinterpret_cast<unsigned long long*>(e.q_row_sums + r),
                                                 (unsigned long long)rsum);
-  if (e.q_orientation == QG_COLUMN_WISE) {
-    // word (r, c0/32) per plane: this lane's row, 32 consecutive columns
+  if (colwise) {
     const int64_t wpr = e.q_pcols >> 5;
     const int64_t wpp = e.q_prows * wpr;
     if (r < e.q_prows && (c0 >> 5) < wpr) {
-      for (int p = 0; p < e.q_bits; ++p) {
-        uint32_t w = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) w |= ((code[j] >> p) & 1u) << j;
-        e.q_planes[p * wpp + r * wpr + (c0 >> 5)] = w;
-      }
+      for (int p = 0; p < 8; ++p)
+        if (p < e.q_bits) e.q_planes[p * wpp + r * wpr + (c0 >> 5)] = w[p];
     }
   } else {
-    // word (c, r0/32) per plane: 32 consecutive rows (the warp's lanes) of one column
     const int64_t wpc = e.q_prows >> 5;   // words per column
     const int64_t wpp = e.q_pcols * wpc;
-    for (int p = 0; p < e.q_bits; ++p) {
-      uint32_t mine = 0;
+    const int64_t c = c0 + lane;
+    if (c < e.q_pcols && (r0 >> 5) < wpc) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        uint32_t b = __ballot_sync(QG_FULL, (code[j] >> p) & 1u);
-        if (lane == j) mine = b;
-      }
-      int64_t c = c0 + lane;
-      if (c < e.q_pcols && (r0 >> 5) < wpc) e.q_planes[p * wpp + c * wpc + (r0 >> 5)] = mine;
+      for (int p = 0; p < 8; ++p)
+        if (p < e.q_bits) e.q_planes[p * wpp + c * wpc + (r0 >> 5)] = w[p];
     }
   }
 }

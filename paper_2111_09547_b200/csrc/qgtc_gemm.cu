@@ -34,12 +34,25 @@ struct GemmParams {
   int32_t n_tiles;
   int32_t mode;
   int64_t vstride;                 // PER_PLANE: virtual column stride of one R plane
+  int64_t n_ext;                   // computed (virtual) column extent, <= n_tiles*bn
+  int32_t raw_stages;              // cp.async ring depth for the packed plane words (2..4)
+  int32_t log2bn;                  // bn is a power of two (32..256)
   const int32_t* blk_list;
   const int32_t* blk_count;
   int32_t* out_i32;
   int32_t* overflow;
+  int64_t* phase_ns;
   qg_epilogue epi;
 };
+
+constexpr int kStampStride = 6 + 4 * 16;   // 6 phase stamps + 4 per main-loop iteration (first 16)
+__device__ __forceinline__ void phase_stamp(const GemmParams& P, int k) {
+  if (P.phase_ns && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    P.phase_ns[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kStampStride + k] = (int64_t)t;
+  }
+}
 
 __device__ __forceinline__ uint4 ldg128(const uint32_t* p) {
   uint4 r;
@@ -69,44 +82,61 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
-// Expand one 128-bit K slice of `nb` stacked planes (w[p] = 4 words) to 128
-// code bytes and store them as the 8 K-cores of one UMMA row.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int n = valid ? 16 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kThreads = 256;
+
+// Expand one unit = (operand row, K-core c): 16 code bytes from `nb` plane
+// words (raw[p*stride + row*4 + (c>>1)]).  Codes: sum_p bit_p << p; ZERO_ONE:
+// a single plane's 0/1 bytes.
 template <bool ZERO_ONE>
-__device__ __forceinline__ void expand_store_row(const uint4* w, int nb, uint32_t row_base) {
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint32_t o[4];
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int sh = 4 * ((c & 1) * 4 + jj);
-      uint32_t acc = 0;
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        if (p < nb) {
-          const uint32_t word = (c >> 1) == 0 ? w[p].x : (c >> 1) == 1 ? w[p].y : (c >> 1) == 2 ? w[p].z : w[p].w;
-          const uint32_t e = expand_nibble((word >> sh) & 0xFu);
-          acc |= ZERO_ONE ? e : (e << p);
-        }
-      }
-      o[jj] = acc;
-    }
-    sts128(row_base + c * 128, o[0], o[1], o[2], o[3]);
+__device__ __forceinline__ void expand_unit(const uint32_t* raw, int pstride, int row, int c, int nb, uint32_t dst) {
+  const int sh0 = (c & 1) * 16;
+  const uint32_t* src = raw + row * 4 + (c >> 1);
+  uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+#pragma unroll 1
+  for (int p = 0; p < nb; ++p) {
+    const uint32_t w = src[p * pstride] >> sh0;
+    const int sh = ZERO_ONE ? 0 : p;
+    o0 |= expand_nibble(w & 0xFu) << sh;
+    o1 |= expand_nibble((w >> 4) & 0xFu) << sh;
+    o2 |= expand_nibble((w >> 8) & 0xFu) << sh;
+    o3 |= expand_nibble((w >> 12) & 0xFu) << sh;
   }
+  sts128(dst, o0, o1, o2, o3);
 }
 
+// smem address of (operand row r, K-core c) in the UMMA K-major interleaved layout
+__device__ __forceinline__ uint32_t umma_off(int r, int c) { return (uint32_t)((r >> 3) * 1024 + c * 128 + (r & 7) * 16); }
+
 template <bool PER_PLANE, int TMEM_COLS>
-__global__ void __launch_bounds__(128) tc_bitgemm_kernel(const __grid_constant__ GemmParams P) {
+__global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_constant__ GemmParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_base_s;
+  phase_stamp(P, 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bn = P.bn;
   const int64_t rb = blockIdx.x;
   const int nt = (int)blockIdx.y;
-  uint8_t* sA = smem;                       // 2 x 16 KB
-  uint8_t* sB = smem + 2 * 16384;           // 2 x bn*128 B
-  const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+  const int lb = P.lbits;
+  const int rbits = PER_PLANE ? 1 : P.rbits;
+  // dynamic smem: sA[2][16K] | sB[2][bn*128] | rawA[NR][lb*2K] | rawB[NR][rbits*bn*16] | sCol[7][bn]
+  const uint32_t sA0 = smem_u32(smem);
   const uint32_t bstage = (uint32_t)bn * 128u;
+  const uint32_t sB0 = sA0 + 2 * 16384u;
+  uint32_t* rawA = reinterpret_cast<uint32_t*>(smem + 2 * 16384 + 2 * bstage);
+  const int rawA_stage = lb * 128 * 4;            // words
+  const int NR = P.raw_stages;
+  uint32_t* rawB = rawA + NR * rawA_stage;
+  const int rawB_stage = rbits * bn * 4;          // words
+  double* sCol = reinterpret_cast<double*>(rawB + NR * rawB_stage);   // [7][bn] per-column epilogue constants
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -118,61 +148,131 @@ __global__ void __launch_bounds__(128) tc_bitgemm_kernel(const __grid_constant__
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
+
+  const int nk = P.blk_count ? P.blk_count[rb] : P.k_tiles;
+  const int32_t* klist = P.blk_list ? P.blk_list + rb * (int64_t)P.k_tiles : nullptr;
+
+  // cp.async issue for K tile `kt` into raw stage `rs`: 16 B per (plane, row)
+  auto issue = [&](int kt, int rs) {
+    const int na = lb * 128, nbb = rbits * bn;
+    for (int u = tid; u < na + nbb; u += kThreads) {
+      if (u < na) {
+        const int p = u >> 7, r = u & 127;
+        const int64_t row = rb * 128 + r;
+        const bool ok = row < P.m_padded;
+        const uint32_t* src = P.lhs + p * P.lwpp + (ok ? row : 0) * P.lwpr + kt * 4;
+        cp_async16(smem_u32(rawA + rs * rawA_stage + (p * 128 + r) * 4), src, ok);
+      } else {
+        const int v = u - na, p = v >> P.log2bn, j = v & (bn - 1);
+        const int64_t vc = (int64_t)nt * bn + j;
+        int64_t col = vc, pl = p;
+        if (PER_PLANE) { pl = vc / P.vstride; col = vc % P.vstride; }
+        const bool ok = pl < P.rbits && col < P.n_padded && vc < P.n_ext;
+        const uint32_t* src = P.rhs + (ok ? pl * P.rwpp + col * P.rwpr : 0) + kt * 4;
+        cp_async16(smem_u32(rawB + rs * rawB_stage + (p * bn + j) * 4), src, ok);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // prologue: prefetch the first NR-1 K tiles (empty groups keep the group count uniform)
+  for (int s0 = 0; s0 < NR - 1; ++s0) {
+    if (s0 < nk) issue(klist ? klist[s0] : s0, s0);
+    else cp_async_commit();
+  }
+  if (P.mode == QG_GEMM_EPILOGUE) {
+    // per-column epilogue constants of this CTA's columns (same fp64 products as the
+    // reference's broadcast terms, computed once instead of per element)
+    const qg_epilogue& E0 = P.epi;
+    for (int i = tid; i < bn; i += kThreads) {
+      const int64_t c = (int64_t)nt * bn + i;
+      const bool ok = c < P.n;
+      sCol[0 * bn + i] = (ok && E0.use_col) ? __dmul_rn(E0.k_col, (double)E0.col_sums[c]) : 0.0;
+      sCol[1 * bn + i] = (ok && E0.bias) ? E0.bias[c] : 0.0;
+      if (E0.bn_mean) {
+        sCol[2 * bn + i] = ok ? E0.bn_mean[c] : 0.0;
+        sCol[3 * bn + i] = ok ? E0.bn_denom[c] : 1.0;
+        sCol[4 * bn + i] = ok ? E0.bn_inv_denom[c] : 1.0;
+        sCol[5 * bn + i] = ok ? E0.bn_gamma[c] : 0.0;
+        sCol[6 * bn + i] = ok ? E0.bn_beta[c] : 0.0;
+      }
+    }
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_s;
-
-  const int nk = P.blk_count ? P.blk_count[rb] : P.k_tiles;
-  const int32_t* klist = P.blk_list ? P.blk_list + rb * (int64_t)P.k_tiles : nullptr;
-  const int64_t row = rb * 128 + tid;
-  const int lb = P.lbits;
-  const int rb_bits = PER_PLANE ? 1 : P.rbits;
   const uint32_t idesc = idesc_u8(bn);
-  // per-thread R columns: tid, tid+128 (bn <= 256).  PER_PLANE: virtual column
-  // v -> (plane v / vstride, column v % vstride) so one CTA can cover several planes.
-  const uint32_t* rcol[2] = {nullptr, nullptr};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int t = tid + 128 * h;
-    if (t >= bn) continue;
-    const int64_t vc = (int64_t)nt * bn + t;
-    int64_t col = vc, pl = 0;
-    if (PER_PLANE) { pl = vc / P.vstride; col = vc % P.vstride; }
-    if (pl < P.rbits && col < P.n_padded) rcol[h] = P.rhs + pl * P.rwpp + col * P.rwpr;
-  }
-  const bool has_c0 = tid < bn, has_c1 = tid + 128 < bn;
+  phase_stamp(P, 1);
 
   for (int it = 0; it < nk; ++it) {
     const int st = it & 1;
-    const int kt = klist ? klist[it] : it;
-    uint4 wa[8], wb0[8], wb1[8];
+    const int pf = it + NR - 1;                        // prefetch distance NR-1
+    if (pf < nk) issue(klist ? klist[pf] : pf, pf % NR);
+    else cp_async_commit();
+    if (NR == 4) cp_async_wait<3>();
+    else if (NR == 3) cp_async_wait<2>();
+    else cp_async_wait<1>();
+    __syncthreads();                                   // raw stage it%NR visible to every thread
+    if (it < 16) phase_stamp(P, 6 + 4 * it);
+    if (it >= 2) mbar_wait(smem_u32(&mbar[st]), ((it - 2) >> 1) & 1);
+    if (it < 16) phase_stamp(P, 7 + 4 * it);
+    long long tx0 = clock64();
+    const uint32_t* ra = rawA + (it % NR) * rawA_stage;
+    const uint32_t* rbw = rawB + (it % NR) * rawB_stage;
+    // A: thread -> row r = tid&127, K-cores h, h+2, h+4, h+6 (h = tid>>7): one 128-bit
+    // shared load per plane feeds four independent expansion chains.
+    {
+      const int r = tid & 127, h = tid >> 7;
+      uint32_t o[4][4];
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      wa[p] = make_uint4(0, 0, 0, 0);
-      wb0[p] = make_uint4(0, 0, 0, 0);
-      wb1[p] = make_uint4(0, 0, 0, 0);
-      if (p < lb && row < P.m_padded) wa[p] = ldg128(P.lhs + p * P.lwpp + row * P.lwpr + kt * 4);
-      if (p < rb_bits) {
-        if (rcol[0]) wb0[p] = ldg128(rcol[0] + p * P.rwpp + kt * 4);
-        if (rcol[1]) wb1[p] = ldg128(rcol[1] + p * P.rwpp + kt * 4);
+      for (int i = 0; i < 4; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0;
+#pragma unroll 1
+      for (int p = 0; p < lb; ++p) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(ra + (p * 128 + r) * 4);
+        const uint32_t wv[4] = {w4.x >> (16 * h), w4.y >> (16 * h), w4.z >> (16 * h), w4.w >> (16 * h)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          o[i][0] |= expand_nibble(wv[i] & 0xFu) << p;
+          o[i][1] |= expand_nibble((wv[i] >> 4) & 0xFu) << p;
+          o[i][2] |= expand_nibble((wv[i] >> 8) & 0xFu) << p;
+          o[i][3] |= expand_nibble((wv[i] >> 12) & 0xFu) << p;
+        }
+      }
+      const uint32_t abase = sA0 + st * 16384u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sts128(abase + umma_off(r, h + 2 * i), o[i][0], o[i][1], o[i][2], o[i][3]);
+    }
+    // B: thread -> column j = tid & (bn-1), K-cores c0, c0+cs, ... (bn/32 of them)
+    {
+      const int j = tid & (bn - 1), c0 = tid >> P.log2bn, cs = kThreads >> P.log2bn;
+      const uint32_t bbase = sB0 + st * bstage;
+#pragma unroll 1
+      for (int c = c0; c < 8; c += cs) {
+        const int wi = c >> 1, sh = (c & 1) * 16;
+        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+#pragma unroll 1
+        for (int p = 0; p < rbits; ++p) {
+          const uint32_t w = rbw[(p * bn + j) * 4 + wi] >> sh;
+          const int shp = PER_PLANE ? 0 : p;
+          o0 |= expand_nibble(w & 0xFu) << shp;
+          o1 |= expand_nibble((w >> 4) & 0xFu) << shp;
+          o2 |= expand_nibble((w >> 8) & 0xFu) << shp;
+          o3 |= expand_nibble((w >> 12) & 0xFu) << shp;
+        }
+        sts128(bbase + umma_off(j, c), o0, o1, o2, o3);
       }
     }
-    if (it >= 2) mbar_wait(smem_u32(&mbar[st]), ((it - 2) >> 1) & 1);
-    // A row tid -> group tid/8, row-in-core tid%8
-    const uint32_t a_row = sA0 + st * 16384u + (uint32_t)((tid >> 3) * 1024 + (tid & 7) * 16);
-    expand_store_row<false>(wa, lb, a_row);
-    if (has_c0) {
-      const uint32_t b_row = sB0 + st * bstage + (uint32_t)((tid >> 3) * 1024 + (tid & 7) * 16);
-      if (PER_PLANE) expand_store_row<true>(wb0, 1, b_row); else expand_store_row<false>(wb0, rb_bits, b_row);
-    }
-    if (has_c1) {
-      const int t1 = tid + 128;
-      const uint32_t b_row = sB0 + st * bstage + (uint32_t)((t1 >> 3) * 1024 + (t1 & 7) * 16);
-      if (PER_PLANE) expand_store_row<true>(wb1, 1, b_row); else expand_store_row<false>(wb1, rb_bits, b_row);
-    }
+    long long tx1 = clock64();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    long long tx2 = clock64();
     __syncthreads();
+    if (it < 16) phase_stamp(P, 8 + 4 * it);
+    if (P.phase_ns && it == 1 && (tid & 31) == 0) {
+      // per-warp cycle split of iteration 1: expansion / fence
+      int64_t* dbg = P.phase_ns + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kStampStride + 54;
+      dbg[warp] = (int64_t)(tx1 - tx0) * 100000 + (int64_t)(tx2 - tx1);
+    }
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
@@ -187,56 +287,163 @@ __global__ void __launch_bounds__(128) tc_bitgemm_kernel(const __grid_constant__
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(&mbar[st])) : "memory");
     }
+    if (it < 16) phase_stamp(P, 9 + 4 * it);
   }
   if (nk > 0) {
     mbar_wait(smem_u32(&mbar[(nk - 1) & 1]), ((nk - 1) >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
+  phase_stamp(P, 2);
 
-  // ---------------- epilogue: TMEM -> registers (lane = row) ----------------
-  const int64_t r0 = rb * 128 + warp * 32;
+  // ---- epilogue: 8-column TMEM slices spread over all 8 warps ----
+  // warp w owns TMEM lanes 32*(w%4).. (rows) and slices s = w/4, w/4 + 2, ...
+  const int quad = warp & 3, half = warp >> 2;
+  const int64_t r0 = rb * 128 + quad * 32;
   const int64_t myrow = r0 + lane;
-  for (int c0 = 0; c0 < bn; c0 += 32) {
-    uint32_t v[32];
-    if (nk > 0) {
-      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
-            "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-            "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = 0;
-    }
-    const int64_t cbase = (int64_t)nt * bn + c0;
-    if (P.mode == QG_GEMM_EPILOGUE) {
-      const int32_t* sv = reinterpret_cast<const int32_t*>(v);
-      epi_chunk32<int32_t>(P.epi, r0, cbase, sv, P.m, P.n);
-    } else if (myrow < P.m) {
-      if (PER_PLANE) {
-#pragma unroll 4
-        for (int j = 0; j < 32; ++j) {
-          const int64_t vc = cbase + j;
-          const int64_t pl = vc / P.vstride, col = vc % P.vstride;
-          if (pl < P.rbits && col < P.n) P.out_i32[(pl * P.m + myrow) * P.n + col] = (int32_t)v[j];
-        }
+  const int64_t col_lo = (int64_t)nt * bn;
+  const int64_t rem_cols = P.n_ext - col_lo;
+  const int ncols_cta = rem_cols <= 0 ? 0 : (rem_cols < bn ? (int)rem_cols : bn);
+  const int nslices = (ncols_cta + 7) >> 3;
+  const qg_epilogue& E = P.epi;
+  const bool fused = P.mode == QG_GEMM_EPILOGUE;
+  const bool packed = fused && E.out_kind == QG_OUT_PLANES;
+  const bool colwise = packed && E.q_orientation == QG_COLUMN_WISE;
+  // colwise words of the CTA tile are OR-accumulated in smem (reusing the sA stages)
+  uint32_t* sWords = reinterpret_cast<uint32_t*>(smem);     // [128 rows][bn/32 words][8 planes]
+  __shared__ unsigned long long sRowSum[128];
+  const int wpc_cta = (bn + 31) >> 5;
+  if (packed) {
+    for (int i = tid; i < 128 * wpc_cta * 8; i += kThreads) sWords[i] = 0;
+    if (tid < 128) sRowSum[tid] = 0ull;
+  }
+  __syncthreads();
+  const bool rvalid = myrow < P.m;
+  const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
+  // row term k_row * row_sums[r] is identical for every column (hoisted)
+  const double rterm = (fused && E.use_row && rvalid) ? __dmul_rn(E.k_row, (double)E.row_sums[myrow]) : 0.0;
+  unsigned long long rsum = 0;
+  const int wpc_rows = packed ? (int)(E.q_prows >> 5) : 0;
+  for (int sl = half; sl < nslices; sl += 2) {
+    const int64_t cb = col_lo + sl * 8;
+    uint64_t codes8 = 0;                 // byte jj = requantized code of column cb+jj (colwise packing)
+#pragma unroll 1
+    for (int g = 0; g < 2; ++g) {        // two groups of 4 columns: small code, 4 independent chains
+      uint32_t v[4];
+      if (nk > 0) {
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sl * 8 + g * 4);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       } else {
-        int32_t* dst = P.out_i32 + myrow * P.n;
+        v[0] = v[1] = v[2] = v[3] = 0;
+      }
+      const int64_t c4 = cb + g * 4;
+      if (!fused) {
+        if (rvalid) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (cbase + j < P.n) dst[cbase + j] = (int32_t)v[j];
+          for (int jj = 0; jj < 4; ++jj) {
+            const int64_t vc = c4 + jj;
+            if (PER_PLANE) {
+              const int64_t pl = vc / P.vstride, col = vc % P.vstride;
+              if (pl < P.rbits && col < P.n) P.out_i32[(pl * P.m + myrow) * P.n + col] = (int32_t)v[jj];
+            } else if (vc < P.n) {
+              P.out_i32[myrow * P.n + vc] = (int32_t)v[jj];
+            }
+          }
+        }
+        continue;
+      }
+      double real[4];
+      const int cl4 = sl * 8 + g * 4;             // CTA-local column of element 0
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int cl = cl4 + jj;
+        double x = __dmul_rn(E.k_acc, (double)(int32_t)v[jj]);
+        if (E.use_row) x = __dadd_rn(x, rterm);
+        if (E.use_col) x = __dadd_rn(x, sCol[cl]);
+        if (E.use_const) x = __dadd_rn(x, E.k_const);
+        if (E.bias) x = __dadd_rn(x, sCol[bn + cl]);
+        if (E.bn_mean)
+          x = __dadd_rn(__dmul_rn(div_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl], sCol[4 * bn + cl]),
+                                  sCol[5 * bn + cl]), sCol[6 * bn + cl]);
+        if (E.act == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
+        else if (E.act == QG_ACT_TANH) x = tanh_f32(x);
+        real[jj] = x;
+      }
+      if (!packed) {
+        if (rvalid) {
+          double* dst = E.out_real + myrow * P.n;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (c4 + jj < P.n) dst[c4 + jj] = real[jj];
+        }
+        continue;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int64_t c = c4 + jj;
+        uint32_t q = 0;
+        if (rvalid && c < P.n) {
+          if (!isfinite(real[jj])) status_min(E.status, myrow * P.n + c);
+          q = quantize_code_fast(real[jj], E.q_amin, E.q_scale, E.q_inv_scale, maxv);
+          rsum += q;
+        }
+        codes8 |= (uint64_t)q << (8 * (g * 4 + jj));
+      }
+    }
+    if (packed && !colwise) {
+      // row-wise words: column cb+jj over the warp's 32 rows; lane jj keeps the ballot
+      // of column jj, then 8 lanes store one word per plane
+      const uint64_t planes8 = transpose8x8(codes8);   // byte p, bit jj = bit p of code jj
+      const int64_t c = cb + lane;
+      const bool in = lane < 8 && c < E.q_pcols && (r0 >> 5) < wpc_rows;
+      uint32_t* dst = E.q_planes + (in ? c * wpc_rows + (r0 >> 5) : 0);
+      const int64_t pstride = E.q_pcols * wpc_rows;
+#pragma unroll 1
+      for (int p = 0; p < E.q_bits; ++p) {
+        const uint32_t byte = (uint32_t)(planes8 >> (8 * p)) & 0xFFu;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const uint32_t b = __ballot_sync(QG_FULL, (byte >> jj) & 1u);
+          mine = (lane == jj) ? b : mine;
+        }
+        if (in) dst[p * pstride] = mine;
+      }
+    }
+    if (colwise) {
+      // byte p of the transpose = plane p's 8 bits of this slice
+      const uint64_t planes8 = transpose8x8(codes8);
+      const int lr = quad * 32 + lane;
+      const int wi = (sl * 8) >> 5, sh = (sl * 8) & 31;
+#pragma unroll 1
+      for (int p = 0; p < E.q_bits; ++p) {
+        const uint32_t b = (uint32_t)(planes8 >> (8 * p)) & 0xFFu;
+        if (b) atomicOr(&sWords[(lr * wpc_cta + wi) * 8 + p], b << sh);
       }
     }
   }
+  phase_stamp(P, 3);
+  if (packed) {
+    if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], rsum);
+    __syncthreads();
+    if (colwise) {
+      const int64_t wpr = E.q_pcols >> 5, wpp = E.q_prows * wpr;
+      const int64_t w0 = col_lo >> 5;
+      for (int i = tid; i < 128 * wpc_cta * 8; i += kThreads) {
+        const int p = i & 7, wi = (i >> 3) % wpc_cta, lr = (i >> 3) / wpc_cta;
+        const int64_t row = rb * 128 + lr;
+        if (p < E.q_bits && row < E.q_prows && w0 + wi < wpr) E.q_planes[p * wpp + row * wpr + w0 + wi] = sWords[i];
+      }
+    }
+    if (E.q_row_sums && tid < 128 && rb * 128 + tid < P.m && sRowSum[tid])
+      atomicAdd(reinterpret_cast<unsigned long long*>(E.q_row_sums + rb * 128 + tid), sRowSum[tid]);
+  }
+  phase_stamp(P, 4);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  phase_stamp(P, 5);
 }
 
 // ----------------------------------------------------------- POPC (exact)
@@ -286,10 +493,14 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const int32_t* __restrict
   if (item >= rgroups * cchunks) return;
   const int64_t r0 = (item / cchunks) * 32, c0 = (item % cchunks) * 32;
   const int64_t r = r0 + lane;
-  int32_t v[32];
+  auto get8 = [&](int sub, uint32_t (&v)[8]) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = (r < rows && c0 + j < cols) ? acc[r * cols + c0 + j] : 0;
-  epi_chunk32<int32_t>(E, r0, c0, v, rows, cols);
+    for (int j = 0; j < 8; ++j) {
+      const int64_t c = c0 + sub * 8 + j;
+      v[j] = (r < rows && c < cols) ? (uint32_t)acc[r * cols + c] : 0u;
+    }
+  };
+  epi_chunk32(E, r0, c0, get8, rows, cols);
 }
 
 }  // namespace qg
@@ -338,14 +549,19 @@ static void set_smem_attr(size_t bytes) {
 }
 
 template <bool PER_PLANE>
-static int launch_tc(const GemmParams& P, dim3 grid, cudaStream_t st) {
-  const size_t smem = 2 * 16384 + 2 * (size_t)P.bn * 128;
+static int launch_tc(GemmParams P, dim3 grid, cudaStream_t st) {
+  const int rbits = PER_PLANE ? 1 : P.rbits;
+  const size_t fixed = 2 * 16384 + 2 * (size_t)P.bn * 128 + 7 * (size_t)P.bn * 8;
+  const size_t stage = (size_t)P.lbits * 128 * 16 + (size_t)rbits * P.bn * 16;
+  const size_t budget = 227 * 1024 - 4096;           // keep room for static smem
+  P.raw_stages = (int32_t)std::max<size_t>(2, std::min<size_t>(4, (budget - fixed) / stage));
+  const size_t smem = fixed + (size_t)P.raw_stages * stage;
   const int cols = P.bn <= 32 ? 32 : P.bn <= 64 ? 64 : P.bn <= 128 ? 128 : 256;
   switch (cols) {
-    case 32: set_smem_attr<PER_PLANE, 32>(smem); tc_bitgemm_kernel<PER_PLANE, 32><<<grid, 128, smem, st>>>(P); break;
-    case 64: set_smem_attr<PER_PLANE, 64>(smem); tc_bitgemm_kernel<PER_PLANE, 64><<<grid, 128, smem, st>>>(P); break;
-    case 128: set_smem_attr<PER_PLANE, 128>(smem); tc_bitgemm_kernel<PER_PLANE, 128><<<grid, 128, smem, st>>>(P); break;
-    default: set_smem_attr<PER_PLANE, 256>(smem); tc_bitgemm_kernel<PER_PLANE, 256><<<grid, 128, smem, st>>>(P); break;
+    case 32: set_smem_attr<PER_PLANE, 32>(smem); tc_bitgemm_kernel<PER_PLANE, 32><<<grid, kThreads, smem, st>>>(P); break;
+    case 64: set_smem_attr<PER_PLANE, 64>(smem); tc_bitgemm_kernel<PER_PLANE, 64><<<grid, kThreads, smem, st>>>(P); break;
+    case 128: set_smem_attr<PER_PLANE, 128>(smem); tc_bitgemm_kernel<PER_PLANE, 128><<<grid, kThreads, smem, st>>>(P); break;
+    default: set_smem_attr<PER_PLANE, 256>(smem); tc_bitgemm_kernel<PER_PLANE, 256><<<grid, kThreads, smem, st>>>(P); break;
   }
   return launch_status_g();
 }
@@ -373,7 +589,7 @@ extern "C" int qg_bitgemm(const qg_gemm_args* a, void* stream) {
   P.k_tiles = (int32_t)(a->k_padded / 128);
   P.mode = a->mode;
   P.blk_list = a->blk_list; P.blk_count = a->blk_count;
-  P.out_i32 = a->out_i32; P.overflow = a->overflow;
+  P.out_i32 = a->out_i32; P.overflow = a->overflow; P.phase_ns = a->phase_ns;
   if (a->epi) P.epi = *a->epi;
 
   // the s32 tensor accumulator is exact iff the largest possible sum fits
@@ -386,28 +602,35 @@ extern "C" int qg_bitgemm(const qg_gemm_args* a, void* stream) {
 
   if (algo == QG_ALGO_TCGEN05) {
     const int64_t row_blocks = (a->m_padded + 127) / 128;
+    // column extent actually computed: logical columns (padding columns of R are zero)
+    int64_t vtotal;
     if (a->mode == QG_GEMM_PER_PLANE) {
-      const int64_t n32 = (a->n_padded + 31) / 32 * 32;
-      int64_t vtotal;
+      const int64_t n32 = (a->n + 31) / 32 * 32;
       if (a->cross_bit || n32 > 256) {
-        // one plane per tile: stride rounded to a whole number of tiles
-        P.bn = (int32_t)std::min<int64_t>(256, n32);
-        P.vstride = (a->n_padded + P.bn - 1) / P.bn * P.bn;
-        vtotal = P.vstride * a->rbits;
+        P.vstride = std::max<int64_t>(32, n32);                    // one plane per tile group
+        P.vstride = (P.vstride + 255) / 256 * 256 > 256 ? (P.vstride + 255) / 256 * 256 : P.vstride;
       } else {
-        // planes stacked along N: each L tile is expanded once for several planes
-        P.vstride = a->n_padded;
-        vtotal = P.vstride * a->rbits;
-        P.bn = (int32_t)std::min<int64_t>(256, (vtotal + 31) / 32 * 32);
+        P.vstride = a->n;                                          // planes stacked along N
       }
-      P.n_tiles = (int32_t)((vtotal + P.bn - 1) / P.bn);
-      dim3 grid((unsigned)row_blocks, (unsigned)P.n_tiles);
-      return launch_tc<true>(P, grid, st);
+      vtotal = P.vstride * a->rbits;
+    } else {
+      P.vstride = a->n_padded;
+      vtotal = a->n;
     }
-    const int64_t nround = (a->n_padded + 31) / 32 * 32;
-    P.bn = (int32_t)std::min<int64_t>(256, nround);
-    P.n_tiles = (int32_t)((a->n_padded + P.bn - 1) / P.bn);
+    P.n_ext = vtotal;
+    const int64_t ext32 = std::max<int64_t>(32, (vtotal + 31) / 32 * 32);
+    // largest power-of-two N tile (32..256) that still gives >= one full wave of CTAs
+    int bn = 32;
+    while (bn < 256 && bn < ext32) bn *= 2;
+    while (bn > 32 && row_blocks * ((ext32 + bn - 1) / bn) < 148) bn /= 2;
+    if (a->mode == QG_GEMM_PER_PLANE && a->cross_bit)
+      while (bn > 32 && bn > P.vstride) bn /= 2;
+    P.bn = bn;
+    P.log2bn = 5;
+    while ((1 << P.log2bn) < bn) ++P.log2bn;
+    P.n_tiles = (int32_t)((ext32 + bn - 1) / bn);
     dim3 grid((unsigned)row_blocks, (unsigned)P.n_tiles);
+    if (a->mode == QG_GEMM_PER_PLANE) return launch_tc<true>(P, grid, st);
     return launch_tc<false>(P, grid, st);
   }
   // POPC path
@@ -425,4 +648,22 @@ extern "C" int qg_bitgemm(const qg_gemm_args* a, void* stream) {
   return epilogue_launch(dst, a->m, a->n, *a->epi, st);
 }
 
-extern "C" int qg_version(void) { return 13; }
+namespace qg {
+__global__ void test_div_kernel(const double* a, const double* b, const double* y, int64_t n, double* out,
+                                double* ref) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = div_rn(a[i], b[i], y[i]);
+  ref[i] = __ddiv_rn(a[i], b[i]);
+}
+}  // namespace qg
+
+extern "C" int qg_test_div(const double* a, const double* b, const double* inv_b, int64_t n, double* out,
+                           double* ref, void* stream) {
+  if (n < 0 || (n && (!a || !b || !inv_b || !out || !ref))) return QG_ERR_ARG;
+  if (n == 0) return QG_OK;
+  qg::test_div_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(a, b, inv_b, n, out, ref);
+  return launch_status_g();
+}
+
+extern "C" int qg_version(void) { return 14; }

@@ -284,27 +284,26 @@ __global__ void __launch_bounds__(256) tile_scan_kernel(const uint32_t* __restri
 }
 
 // Zero-tile-jumping schedule: per 128-row block, the ordered list of K tiles
-// with at least one set bit.  One warp per row block, ballot + popc prefix.
-__global__ void block_list_kernel(const uint32_t* __restrict__ a, int64_t prows, int64_t pcols,
+// with at least one set bit, derived from the 8x128 flags (16 flags per
+// 128x128 block).  One warp per row block; lanes read consecutive flags.
+__global__ void block_list_kernel(const uint8_t* __restrict__ flags, int64_t prows, int64_t pcols,
                                   int32_t* __restrict__ blk_list, int32_t* __restrict__ blk_count) {
   const int lane = threadIdx.x & 31;
   const int64_t rb = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nrb = (prows + 127) >> 7;
   if (rb >= nrb) return;
-  const int64_t ct = pcols >> 7, wpr = pcols >> 5;
-  const int64_t r_lo = rb * 128, r_hi = (prows < r_lo + 128 ? prows : r_lo + 128);
+  const int64_t ct = pcols >> 7, rt = prows >> 3;
+  const int64_t t_lo = rb * 16, t_hi = (rt < t_lo + 16 ? rt : t_lo + 16);
   int32_t count = 0;
-  for (int64_t t0 = 0; t0 < ct; t0 += 32) {
-    const int64_t t = t0 + lane;
-    uint32_t any = 0;
-    if (t < ct) {
-      for (int64_t r = r_lo; r < r_hi && !any; ++r) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a + r * wpr + t * 4));
-        any = q.x | q.y | q.z | q.w;
-      }
+  for (int64_t k0 = 0; k0 < ct; k0 += 32) {
+    const int64_t k = k0 + lane;
+    bool nz = false;
+    if (k < ct) {
+#pragma unroll 4
+      for (int64_t t = t_lo; t < t_hi; ++t) nz |= flags[t * ct + k] == 0;
     }
-    const uint32_t m = __ballot_sync(QG_FULL, any != 0);
-    if (any) blk_list[rb * ct + count + __popc(m & ((1u << lane) - 1u))] = (int32_t)t;
+    const uint32_t m = __ballot_sync(QG_FULL, nz);
+    if (nz) blk_list[rb * ct + count + __popc(m & ((1u << lane) - 1u))] = (int32_t)k;
     count += __popc(m);
   }
   if (lane == 0) blk_count[rb] = count;
@@ -452,9 +451,10 @@ extern "C" int qg_tile_scan(const uint32_t* a_words, int64_t rows, int64_t padde
     tile_scan_kernel<<<(unsigned)((rt * 32 + 255) / 256), 256, 0, st>>>(a_words, rows, padded_rows, padded_cols,
                                                                          zero_flags, degrees, zero_count);
   if (blk_list && blk_count) {
+    if (!zero_flags) return QG_ERR_ARG;   // the schedule is derived from the 8x128 flags
     const int64_t nrb = (padded_rows + 127) / 128;
     if (nrb > 0)
-      block_list_kernel<<<(unsigned)((nrb * 32 + 127) / 128), 128, 0, st>>>(a_words, padded_rows, padded_cols,
+      block_list_kernel<<<(unsigned)((nrb * 32 + 127) / 128), 128, 0, st>>>(zero_flags, padded_rows, padded_cols,
                                                                              blk_list, blk_count);
   }
   return launch_status();

@@ -282,3 +282,81 @@ def float32_dense_bytes(b: SubgraphBatch) -> int:
     if b.features is not None:
         size += 4 * n * b.features.logical_cols
     return size
+
+
+# ---------------------------------------------------------------- QGT2 wire
+# Bandwidth/alignment-optimised compound format for the device fast path
+# (SURVEY.md section 8(f) rank 1).  Same content as QGTB, but every section
+# starts on a 256-byte boundary so device views are 128-bit loadable.
+#   header (64 B): magic "QGT2", u16 version, u16 flags, u32 num_subgraphs,
+#   u32 total_nodes, u8 feature_bits, u8 x_bits, u16 reserved, f64 amin,
+#   f64 amax, u32 adj_pr, u32 adj_pc, u32 feat_pr, u32 feat_pc, u32 in_dim
+#   then sections: boundaries u32[ns+1], node_ids u32[total], adjacency
+#   words, feature plane words.
+V2_MAGIC = b"QGT2"
+_V2_HEADER = struct.Struct("<4sHHIIBBHddIIIII")
+_V2_ALIGN = 256
+
+
+def _v2_layout(ns: int, total: int, adj_words: int, feat_words: int):
+    def up(x):
+        return -(-x // _V2_ALIGN) * _V2_ALIGN
+    o_b = up(_V2_HEADER.size)
+    o_ids = up(o_b + 4 * (ns + 1))
+    o_adj = up(o_ids + 4 * total)
+    o_feat = up(o_adj + 4 * adj_words)
+    end = up(o_feat + 4 * feat_words)
+    return o_b, o_ids, o_adj, o_feat, end
+
+
+def pack_batch_v2(b: SubgraphBatch) -> bytes:
+    """QGT2 image of a batch (row-wise feature planes, column-wise adjacency)."""
+    a, f = b.adjacency, b.features
+    fw = 0 if f is None else int(f.dwords.numel())
+    ns, total = b.num_subgraphs, b.total_nodes
+    o_b, o_ids, o_adj, o_feat, end = _v2_layout(ns, total, int(a.dwords.numel()), fw)
+    out = bytearray(end)
+    xp = b.x_params
+    _V2_HEADER.pack_into(out, 0, V2_MAGIC, 1, 0, ns, total, 0 if f is None else f.bits,
+                         0 if xp is None else xp.bits, 0, 0.0 if xp is None else xp.alpha_min,
+                         0.0 if xp is None else xp.alpha_max, a.padded_rows, a.padded_cols,
+                         0 if f is None else f.padded_rows, 0 if f is None else f.padded_cols,
+                         0 if f is None else f.logical_cols)
+    out[o_b:o_b + 4 * (ns + 1)] = b.boundaries.astype("<u4").tobytes()
+    out[o_ids:o_ids + 4 * total] = b.node_ids.astype("<u4").tobytes()
+    out[o_adj:o_adj + 4 * a.dwords.numel()] = a.dwords.cpu().numpy().astype("<i4").tobytes()
+    if f is not None:
+        out[o_feat:o_feat + 4 * fw] = f.dwords.cpu().numpy().astype("<i4").tobytes()
+    return bytes(out)
+
+
+def batch_from_v2(header_bytes: bytes, dev_buf: torch.Tensor, base: int = 0) -> SubgraphBatch:
+    """Device views of a QGT2 image already resident at ``dev_buf[base:]``.
+
+    Only the header / id sections are read on the host (from ``header_bytes``);
+    the adjacency and feature words are zero-copy views into the device buffer.
+    """
+    (magic, version, _flags, ns, total, fbits, xbits, _r, amin, amax, apr, apc, fpr, fpc,
+     in_dim) = _V2_HEADER.unpack_from(header_bytes)
+    if magic != V2_MAGIC:
+        raise FormatError(f"bad compound-buffer magic {magic!r}")
+    if version != 1:
+        raise FormatError(f"unsupported compound-buffer version {version}")
+    fw = fbits * fpr * fpc // 32
+    o_b, o_ids, o_adj, o_feat, end = _v2_layout(ns, total, apr * apc // 32, fw)
+    if len(header_bytes) < o_adj:
+        raise FormatError("compound buffer shorter than its id sections")
+    boundaries = np.frombuffer(header_bytes, dtype="<u4", count=ns + 1, offset=o_b).astype(np.int64)
+    node_ids = np.frombuffer(header_bytes, dtype="<u4", count=total, offset=o_ids).astype(np.int64)
+    if (base + o_adj) % 16:
+        raise FormatError("QGT2 image must start 16-byte aligned")
+    adj_w = dev_buf[base + o_adj: base + o_adj + 4 * (apr * apc // 32)].view(torch.int32)
+    adj = PackedBitMatrix(COLUMN_WISE, total, total, apr, apc, adj_w)
+    feats = None
+    params = None
+    if fbits:
+        fwords = dev_buf[base + o_feat: base + o_feat + 4 * fw].view(torch.int32).reshape(fbits, -1)
+        feats = BitPlaneStack._wrap(ROW_WISE, total, in_dim, fpr, fpc, fwords)
+        params = QuantParams(amin, amax, xbits)
+    return SubgraphBatch(node_ids=node_ids, adjacency=adj, features=feats, boundaries=boundaries,
+                         x_params=params)

@@ -1,0 +1,124 @@
+"""Kernel-level GPU checks beyond the golden fixtures: size-independent
+properties at larger shapes (two independent device algorithms agree, exact
+integer identities), the epilogue's fast division, and edge cases."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2111_09547_b200 as bg
+from oracle import qgtc_oracle as O
+from paper_2111_09547_b200 import _native as N
+from paper_2111_09547_b200 import bitgemm, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _div_check(a: np.ndarray, b: np.ndarray):
+    y = 1.0 / b                                   # RN(1/b), IEEE on the host
+    ta, tb, ty = (torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (a, b, y))
+    out, ref = torch.empty_like(ta), torch.empty_like(ta)
+    N.call("qg_test_div", N.ptr(ta), N.ptr(tb), N.ptr(ty), ta.numel(), N.ptr(out), N.ptr(ref), N.stream())
+    out, ref = out.cpu().numpy(), ref.cpu().numpy()
+    np.testing.assert_array_equal(ref, a / b)     # device IEEE == numpy IEEE
+    same = (out.view(np.int64) == ref.view(np.int64)) | (np.isnan(out) & np.isnan(ref))
+    assert same.all(), (a[~same][:5], b[~same][:5], out[~same][:5], ref[~same][:5])
+
+
+def test_fast_division_is_correctly_rounded():
+    rng = np.random.default_rng(0)
+    n = 2_000_000
+    # wide exponent range incl. the fallback regions
+    a = rng.standard_normal(n) * np.exp2(rng.integers(-1060, 1020, n).astype(np.float64))
+    b = np.abs(rng.standard_normal(n)) * np.exp2(rng.integers(-1060, 1020, n).astype(np.float64)) + 1e-300
+    _div_check(a, b)
+    # epilogue-like: quotients straddling integers (the floor() boundary) and grid scales
+    b = rng.uniform(1e-6, 10.0, n)
+    k = rng.integers(-10 ** 6, 10 ** 6, n).astype(np.float64)
+    a = k * b
+    a = np.where(rng.uniform(size=n) < 0.5, np.nextafter(a, np.inf), np.nextafter(a, -np.inf))
+    _div_check(a, b)
+    scales = np.array([(hi - lo) / (1 << bits) for lo, hi in [(-0.5, 0.5), (0.0, 1.0), (-3.1, 7.7)]
+                       for bits in range(1, 9)])
+    b = rng.choice(scales, n)
+    a = rng.uniform(-50, 50, n)
+    _div_check(a, b)
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1.7e308, 1.0, 3.0])
+    aa, bb = np.meshgrid(specials, np.array([1.0, 3.0, 0.1, 7e-310, 1e300]))
+    _div_check(aa.ravel(), bb.ravel())
+
+
+@pytest.mark.parametrize("bits", [1, 3, 8])
+def test_tcgen05_matches_popc_at_scale(bits):
+    # A 2048 x 4096 block-diagonal (zero-tile jumping active) x X (4096 x 200, `bits` planes)
+    a = synth.bernoulli_adjacency(2048, 4096, 0.3, seed=bits, blocks=4)
+    x, codes = synth.random_codes_stack(4096, 200, bits, bg.ROW_WISE, seed=bits)
+    xs = bg.BitPlaneStack._wrap(bg.ROW_WISE, 4096, 200, x.padded_rows, x.padded_cols, x.dwords)
+    tc = bitgemm.bmm_planes_device(a, xs, algo="tcgen05")
+    pc = bitgemm.bmm_planes_device(a, xs, algo="popc")
+    assert torch.equal(tc, pc)
+    # reduced accumulator == A @ codes (exact in fp64 at these magnitudes)
+    dense = torch.from_numpy(bg.unpack(a).astype(np.float64)).cuda()
+    want = (dense @ codes.to(torch.float64)).to(torch.int64)
+    red = torch.zeros_like(want)
+    for p in range(bits):
+        red += tc[p].to(torch.int64) << p
+    assert torch.equal(red, want)
+
+
+def test_reduced_gemm_matches_dense_product():
+    for (m, k, n, s, t) in [(1000, 300, 129, 8, 8), (257, 1000, 64, 3, 5), (130, 128, 300, 2, 1)]:
+        x, xc = synth.random_codes_stack(m, k, s, bg.COLUMN_WISE, seed=m)
+        w, wc = synth.random_codes_stack(k, n, t, bg.ROW_WISE, seed=n)
+        acc = bg.gemm_sbit_by_tbit(x, w, "int32")
+        want = (xc.double() @ wc.double()).cpu().numpy().astype(np.int64)
+        np.testing.assert_array_equal(acc, want)
+
+
+def test_per_plane_cross_bit_and_cross_tile_agree():
+    rng = np.random.default_rng(5)
+    dense = (rng.uniform(0, 1, (300, 700)) < 0.1).astype(np.uint8)
+    a = bg.pack_colwise(dense)
+    xp = (rng.uniform(0, 1, (6, 700, 45)) < 0.5).astype(np.uint8)
+    xs = bg.pack_planes(xp, bg.ROW_WISE)
+    base = bg.bmm_1bit_by_nbit(a, xs, reuse=bg.CROSS_TILE)
+    for jump in (True, False):
+        outs = bg.bmm_1bit_by_nbit(a, xs, jump=jump, reuse=bg.CROSS_BIT)
+        for p in range(6):
+            np.testing.assert_array_equal(outs[p], base[p])
+            np.testing.assert_array_equal(outs[p], dense.astype(np.int64) @ xp[p].astype(np.int64))
+
+
+def test_repack_roundtrip_large():
+    rng = np.random.default_rng(6)
+    planes = (rng.uniform(0, 1, (5, 1000, 333)) < 0.5).astype(np.uint8)
+    st = bg.pack_planes(planes, bg.ROW_WISE)
+    col = bg.repack(st, bg.COLUMN_WISE)
+    np.testing.assert_array_equal(bg.to_planes(col), planes)
+    back = bg.repack(col, bg.ROW_WISE)
+    assert back == st
+    w, _, _ = O.pack_stack(planes, O.COL, 8)
+    np.testing.assert_array_equal(np.stack([p.words for p in col.planes]), w)
+
+
+def test_quantize_pack_large_matches_oracle():
+    rng = np.random.default_rng(7)
+    m = rng.uniform(-1, 2, (5000, 300))
+    for bits in (1, 4, 8):
+        p = bg.QuantParams(-0.5, 1.5, bits)
+        for orient in (bg.ROW_WISE, bg.COLUMN_WISE):
+            st = bg.pack_planes(bg.bit_decompose(bg.quantize_matrix(m, p)), orient)
+            w, _, _ = O.pack_stack(O.planes_of(O.quantize_codes(m, -0.5, 1.5, bits), bits),
+                                   O.COL if orient == bg.COLUMN_WISE else O.ROW, 8)
+            np.testing.assert_array_equal(np.stack([q.words for q in st.planes]), w)
+
+
+def test_empty_and_degenerate_shapes():
+    a = bg.pack_colwise(np.zeros((0, 5), np.uint8))
+    assert a.padded_rows == 0 and len(a.words) == 0
+    x = bg.pack_planes(np.ones((2, 5, 3), np.uint8), bg.ROW_WISE)
+    outs = bg.bmm_1bit_by_nbit(a, x)
+    assert all(o.shape == (0, 3) for o in outs)
+    one = bg.pack_colwise(np.ones((1, 1), np.uint8))
+    y = bg.pack_planes(np.ones((8, 1, 1), np.uint8), bg.ROW_WISE)
+    assert [int(o[0, 0]) for o in bg.bmm_1bit_by_nbit(one, y)] == [1] * 8
