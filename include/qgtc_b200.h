@@ -163,6 +163,13 @@ typedef struct {
   uint32_t* q_planes;          /* q_bits x words; caller zero-fills               */
   int64_t* q_row_sums;         /* optional [rows], ACCUMULATED (caller zeroes)    */
   int64_t* status;             /* optional: first non-finite requant input index  */
+  uint8_t* q_codes;            /* optional u8 code cache of the requantized output, the
+                                  K-major operand layout of the next bit-GEMM:
+                                  row-major [rows][ld] (next lhs) or col-major
+                                  [cols][ld] (next rhs); padding must be zero      */
+  int64_t q_codes_ld;
+  int32_t q_codes_colmajor;
+  int32_t q_skip_planes;       /* 1: write only the code cache (planes built lazily) */
 } qg_epilogue;
 
 /*
@@ -189,6 +196,11 @@ typedef struct {
   const qg_epilogue* epi;      /* EPILOGUE mode                                   */
   int32_t* overflow;           /* optional device flag, set to 1 on int32 overflow */
   int32_t* scratch_i32;        /* [m][n] scratch for the POPC epilogue path       */
+  const uint8_t* lhs_codes;    /* optional: L as u8 codes [>= m][lhs_ld] (K contiguous,
+                                  zero beyond k); used instead of the planes (TCGEN05) */
+  int64_t lhs_ld;
+  const uint8_t* rhs_codes;    /* optional: R as u8 codes [>= n][rhs_ld] (K contiguous) */
+  int64_t rhs_ld;
   int64_t* phase_ns;           /* optional profiling hook: per CTA 6 %globaltimer stamps
                                   (entry, setup done, MMAs done, epilogue computed, stored, exit) */
   int32_t cross_bit;           /* PER_PLANE: 1 = one plane per CTA (cross-bit reuse),
@@ -213,6 +225,12 @@ int qg_bitgemm(const qg_gemm_args* args, void* stream);
  * overflow flag.  Replaces reduce_bitplanes (bitgemm.py:291-298). */
 int qg_reduce_planes(const int64_t* accs, int64_t nplanes, int64_t n, int32_t* out,
                      int32_t* overflow, void* stream);
+
+/* Packed planes -> u8 codes (sum_p bit_p << p) in a K-major operand layout:
+ * row-major [rows][ld] or col-major [cols][ld].  Padding entries are not written. */
+int qg_planes_to_codes(const uint32_t* words, int64_t nplanes, int64_t rows, int64_t cols,
+                       int64_t padded_rows, int64_t padded_cols, int orientation, uint8_t* codes,
+                       int64_t ld, int colmajor, void* stream);
 
 /* Set adjacency bits from an edge list into zero-initialised column-wise
  * words (row = src, col = dst).  Replaces the dense total x total build +

@@ -31,7 +31,7 @@ STATUS_CLEAR = 0x7F7F7F7F7F7F7F7F
 # every compute entry point declared in include/qgtc_b200.h
 EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes", "qg_unpack", "qg_repack",
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
-           "qg_popcount32", "qg_edges_to_bits", "qg_test_div")
+           "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -50,6 +50,8 @@ class Epilogue(ctypes.Structure):
         ("q_orientation", ctypes.c_int32), ("pad_", ctypes.c_int32),
         ("q_prows", _i64), ("q_pcols", _i64),
         ("out_real", _vp), ("q_planes", _vp), ("q_row_sums", _vp), ("status", _vp),
+        ("q_codes", _vp), ("q_codes_ld", _i64), ("q_codes_colmajor", ctypes.c_int32),
+        ("q_skip_planes", ctypes.c_int32),
     ]
 
 
@@ -64,6 +66,7 @@ class GemmArgs(ctypes.Structure):
         ("blk_list", _vp), ("blk_count", _vp),
         ("mode", ctypes.c_int32), ("algo", ctypes.c_int32),
         ("out_i32", _vp), ("epi", ctypes.POINTER(Epilogue)), ("overflow", _vp), ("scratch_i32", _vp),
+        ("lhs_codes", _vp), ("lhs_ld", _i64), ("rhs_codes", _vp), ("rhs_ld", _i64),
         ("phase_ns", _vp), ("cross_bit", ctypes.c_int32), ("pad2", ctypes.c_int32),
     ]
 
@@ -94,6 +97,7 @@ def lib() -> ctypes.CDLL:
             "qg_popcount32": ([_vp, _i64, _vp, _vp], ctypes.c_int),
             "qg_edges_to_bits": ([_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp], ctypes.c_int),
             "qg_test_div": ([_vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
+            "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)

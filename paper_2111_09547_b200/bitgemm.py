@@ -27,7 +27,8 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .bitpack import COLUMN_WISE, ROW_WISE, BitPlaneStack, PackedBitMatrix, orient_id, padded_dims
+from .bitpack import (COLUMN_WISE, ROW_WISE, BitPlaneStack, CodeBackedStack, PackedBitMatrix, orient_id, pad128,
+                      padded_dims)
 from .errors import ReductionOverflowError, ShapeError
 from .quantize import QuantParams
 
@@ -193,7 +194,7 @@ def _build_epilogue(epi: EpilogueSpec, rows: int, cols: int, *, out_orientation=
 
 
 def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, bias, bn, kind, out_params,
-                        rows, cols, out_orientation, out_pad_to, want_row_sums, dev) -> _EpiPlan:
+                        rows, cols, out_orientation, out_pad_to, want_row_sums, dev, code_cache=False) -> _EpiPlan:
     """Device epilogue state; fp64 coefficients grouped as _dequantize (bitgemm.py:166-178)."""
     plan = _EpiPlan()
     e = plan.struct
@@ -227,11 +228,22 @@ def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, b
         return plan
     q = out_params
     pr, pc = padded_dims(rows, cols, out_orientation, out_pad_to)
-    planes = torch.zeros((q.bits, pr * pc // 32), dtype=torch.int32, device=dev)
-    plan.out_stack = BitPlaneStack._wrap(out_orientation, rows, cols, pr, pc, planes)
     e.out_kind, e.q_bits, e.q_amin, e.q_scale = N.OUT_PLANES, q.bits, q.alpha_min, q.scale
     e.q_inv_scale = 1.0 / q.scale
-    e.q_orientation, e.q_prows, e.q_pcols, e.q_planes = orient_id(out_orientation), pr, pc, planes.data_ptr()
+    e.q_orientation, e.q_prows, e.q_pcols = orient_id(out_orientation), pr, pc
+    if code_cache:
+        # codes only, in the next GEMM's operand layout: a column-wise output feeds a left
+        # operand (row-major codes), a row-wise output a right operand (col-major codes)
+        colmajor = out_orientation == ROW_WISE
+        ld = pad128(rows if colmajor else cols)
+        codes = torch.zeros(((cols if colmajor else rows), ld), dtype=torch.uint8, device=dev)
+        plan.out_stack = CodeBackedStack(out_orientation, rows, cols, q.bits, codes, ld, colmajor, out_pad_to)
+        e.q_codes, e.q_codes_ld, e.q_codes_colmajor, e.q_skip_planes = codes.data_ptr(), ld, int(colmajor), 1
+        e.q_planes = 0
+    else:
+        planes = torch.zeros((q.bits, pr * pc // 32), dtype=torch.int32, device=dev)
+        plan.out_stack = BitPlaneStack._wrap(out_orientation, rows, cols, pr, pc, planes)
+        e.q_planes = planes.data_ptr()
     if want_row_sums:
         plan.row_sums = torch.zeros(rows, dtype=torch.int64, device=dev)
         e.q_row_sums = plan.row_sums.data_ptr()
@@ -283,7 +295,11 @@ class _Schedule:
         self.degrees = torch.empty(a.logical_rows, dtype=torch.int64, device=dev)
         self.zero_count = torch.zeros(1, dtype=torch.int64, device=dev)
         self.blk_list = torch.empty((nrb, max(self.ct, 1)), dtype=torch.int32, device=dev)
-        self.blk_count = torch.empty(nrb, dtype=torch.int32, device=dev)
+        self.blk_count = torch.zeros(nrb, dtype=torch.int32, device=dev)
+        self._zeros = None
+        if a.dwords.numel() == 0:
+            self.degrees.zero_()
+            return
         N.call("qg_tile_scan", N.ptr(a.dwords), a.logical_rows, pr, pc, N.ptr(self.flags), N.ptr(self.degrees),
                N.ptr(self.zero_count), N.ptr(self.blk_list), N.ptr(self.blk_count), N.stream())
         self._zeros = None
@@ -339,12 +355,19 @@ def _launch_work(mp, kp, np_, rbits, mode, schedule):
 
 
 def gemm_device(lhs_dwords, lbits, m, mp, k, kp, rhs_dwords, rbits, n, np_, *, mode, schedule=None,
-                out=None, epi_struct=None, algo="auto", cross_bit=False, overflow=None, scratch=None):
-    """Launch qg_bitgemm on device tensors (no syncs)."""
+                out=None, epi_struct=None, algo="auto", cross_bit=False, overflow=None, scratch=None,
+                lhs_codes=None, rhs_codes=None):
+    """Launch qg_bitgemm on device tensors (no syncs).  ``lhs_codes``/``rhs_codes``
+    are optional (u8 tensor, ld) code caches used instead of the plane words."""
     args = N.GemmArgs()
+    if lhs_codes is not None:
+        args.lhs_codes, args.lhs_ld = lhs_codes[0].data_ptr(), lhs_codes[1]
+    if rhs_codes is not None:
+        args.rhs_codes, args.rhs_ld = rhs_codes[0].data_ptr(), rhs_codes[1]
     args.lhs, args.lbits, args.m, args.m_padded, args.k, args.k_padded = \
-        lhs_dwords.data_ptr(), lbits, m, mp, k, kp
-    args.rhs, args.rbits, args.n, args.n_padded = rhs_dwords.data_ptr(), rbits, n, np_
+        (lhs_dwords.data_ptr() if lhs_dwords is not None else args.lhs_codes), lbits, m, mp, k, kp
+    args.rhs, args.rbits, args.n, args.n_padded = \
+        (rhs_dwords.data_ptr() if rhs_dwords is not None else args.rhs_codes), rbits, n, np_
     if schedule is not None:
         args.blk_list, args.blk_count = schedule.blk_list.data_ptr(), schedule.blk_count.data_ptr()
     args.mode, args.algo, args.cross_bit = mode, N.ALGO[algo], int(cross_bit)
@@ -358,7 +381,7 @@ def gemm_device(lhs_dwords, lbits, m, mp, k, kp, rhs_dwords, rbits, n, np_, *, m
         args.scratch_i32 = scratch.data_ptr()
     if PHASE_HOOK is not None:
         ctas = max(1, (mp + 127) // 128) * 64
-        stamps = torch.zeros((ctas, 70), dtype=torch.int64, device=lhs_dwords.device)
+        stamps = torch.zeros((ctas, 70), dtype=torch.int64, device=N.device())
         args.phase_ns = stamps.data_ptr()
         PHASE_HOOK.append(stamps)
     if PROFILE_HOOK is not None:

@@ -187,6 +187,56 @@ class BitPlaneStack:
         return f"BitPlaneStack({self.bits} x {self.orientation} {self.logical_rows}x{self.logical_cols})"
 
 
+class CodeBackedStack(BitPlaneStack):
+    """A stack whose source of truth is a u8 code cache in HBM (the fused GEMM
+    epilogues emit codes in the next GEMM's K-major operand layout).  The packed
+    plane words -- the reference's ``words`` -- are materialised on first access
+    by the bit_qnt kernel (a row-wise packing of M is the column-wise packing of
+    M^T, so either code layout serves either orientation)."""
+
+    def __init__(self, orientation, rows, cols, bits, codes: torch.Tensor, ld: int, colmajor: bool, pad_to=8):
+        pr, pc = padded_dims(rows, cols, orientation, pad_to)
+        self.bits = int(bits)
+        self._planes = None
+        self._meta = (orientation, int(rows), int(cols), int(pr), int(pc))
+        self.codes, self.codes_ld, self.codes_colmajor = codes, int(ld), bool(colmajor)
+        self._dwords = None
+
+    @property
+    def dwords(self) -> torch.Tensor:
+        if self._dwords is None:
+            o, rows, cols, pr, pc = self._meta
+            # codes viewed as a row-major matrix: M itself, or M^T for col-major codes
+            src_rows, src_cols = (cols, rows) if self.codes_colmajor else (rows, cols)
+            want_col = (o == COLUMN_WISE) != self.codes_colmajor
+            oid = N.COLUMN_WISE_ID if want_col else N.ROW_WISE_ID
+            words = torch.empty((self.bits, pr * pc // 32), dtype=torch.int32, device=self.codes.device)
+            if words.numel():
+                status = N.new_status()
+                N.call("qg_quantize_pack", N.ptr(self.codes), N.SRC_U8, src_rows, src_cols, self.codes_ld, 0.0, 1.0,
+                       self.bits, oid, 8, N.ptr(words), None, None, None, N.ptr(status), N.stream())
+            self._dwords = words
+        return self._dwords
+
+    @dwords.setter
+    def dwords(self, value):
+        self._dwords = value
+
+
+def stack_code_operand(stack: BitPlaneStack, colmajor: bool):
+    """(u8 codes, ld) of a stack in a K-major operand layout (row-major for a
+    left operand, col-major for a right one); reuses a code cache when present."""
+    if isinstance(stack, CodeBackedStack) and stack.codes_colmajor == colmajor:
+        return stack.codes, stack.codes_ld
+    rows, cols, pr, pc = stack.dims()
+    ld = pad128(rows if colmajor else cols)
+    codes = torch.zeros(((cols if colmajor else rows), ld), dtype=torch.uint8, device=stack.dwords.device)
+    if rows * cols:
+        N.call("qg_planes_to_codes", N.ptr(stack.dwords), stack.bits, rows, cols, pr, pc,
+               orient_id(stack.orientation), N.ptr(codes), ld, int(colmajor), N.stream())
+    return codes, ld
+
+
 # ------------------------------------------------------------------ packing
 def _binary_planes(planes) -> torch.Tensor:
     """(bits, rows, cols) input -> u8 device tensor; non-binary -> DataError."""

@@ -144,6 +144,7 @@ __device__ __forceinline__ void epi_chunk32(const qg_epilogue& e, int64_t r0, in
         if (!isfinite(real)) status_min(e.status, r * cols + c);
         q = quantize_code_fast(real, e.q_amin, e.q_scale, e.q_inv_scale, maxv);
         rsum += q;
+        if (e.q_codes) e.q_codes[e.q_codes_colmajor ? c * e.q_codes_ld + r : r * e.q_codes_ld + c] = (uint8_t)q;
       }
       if (colwise) {
         // this lane's row: bit j of word (r, c0/32)
@@ -163,6 +164,7 @@ __device__ __forceinline__ void epi_chunk32(const qg_epilogue& e, int64_t r0, in
   }
   if (e.q_row_sums && rvalid && rsum) atomicAdd(reinterpret_cast<unsigned long long*>(e.q_row_sums + r),
                                                 (unsigned long long)rsum);
+  if (e.q_skip_planes) return;
   if (colwise) {
     const int64_t wpr = e.q_pcols >> 5;
     const int64_t wpp = e.q_prows * wpr;

@@ -37,6 +37,9 @@ struct GemmParams {
   int64_t n_ext;                   // computed (virtual) column extent, <= n_tiles*bn
   int32_t raw_stages;              // cp.async ring depth for the packed plane words (2..4)
   int32_t log2bn;                  // bn is a power of two (32..256)
+  const uint8_t* lhs_codes; int64_t lhs_ld;   // optional u8 code operands (K-major, UMMA-ready)
+  const uint8_t* rhs_codes; int64_t rhs_ld;
+  int32_t pf_dist;                 // cp.async prefetch distance (raw_stages - 2, >= 1)
   const int32_t* blk_list;
   const int32_t* blk_count;
   int32_t* out_i32;
@@ -118,7 +121,8 @@ __device__ __forceinline__ uint32_t umma_off(int r, int c) { return (uint32_t)((
 template <bool PER_PLANE, int TMEM_COLS>
 __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_constant__ GemmParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(8) uint64_t mbar_x[2];     // expanded-stage reuse (MMA of it-2 done)
+  __shared__ __align__(8) uint64_t mbar_r[4];     // raw-stage reuse (MMA of it-NR done)
   __shared__ uint32_t tmem_base_s;
   phase_stamp(P, 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -127,16 +131,21 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
   const int nt = (int)blockIdx.y;
   const int lb = P.lbits;
   const int rbits = PER_PLANE ? 1 : P.rbits;
-  // dynamic smem: sA[2][16K] | sB[2][bn*128] | rawA[NR][lb*2K] | rawB[NR][rbits*bn*16] | sCol[7][bn]
-  const uint32_t sA0 = smem_u32(smem);
+  const bool a_codes = P.lhs_codes != nullptr, b_codes = P.rhs_codes != nullptr;
+  const bool expand = !a_codes || !b_codes;
+  const int NR = P.raw_stages, PD = P.pf_dist;
+  // dynamic smem: [sA 2x16K if A expanded][sB 2x bn*128 if B expanded][rawA NR][rawB NR][sCol 7*bn*8]
+  const uint32_t base = smem_u32(smem);
+  uint32_t off = 0;
+  const uint32_t sA0 = base + off;  if (!a_codes) off += 2 * 16384u;
   const uint32_t bstage = (uint32_t)bn * 128u;
-  const uint32_t sB0 = sA0 + 2 * 16384u;
-  uint32_t* rawA = reinterpret_cast<uint32_t*>(smem + 2 * 16384 + 2 * bstage);
-  const int rawA_stage = lb * 128 * 4;            // words
-  const int NR = P.raw_stages;
-  uint32_t* rawB = rawA + NR * rawA_stage;
-  const int rawB_stage = rbits * bn * 4;          // words
-  double* sCol = reinterpret_cast<double*>(rawB + NR * rawB_stage);   // [7][bn] per-column epilogue constants
+  const uint32_t sB0 = base + off;  if (!b_codes) off += 2 * bstage;
+  const uint32_t rawA_bytes = a_codes ? 16384u : (uint32_t)lb * 2048u;
+  const uint32_t rawB_bytes = b_codes ? bstage : (uint32_t)rbits * bn * 16u;
+  uint8_t* rawA = smem + off;  off += NR * rawA_bytes;
+  uint8_t* rawB = smem + off;  off += NR * rawB_bytes;
+  // [7][bn] per-column epilogue constants, beyond the 32 KB epilogue scratch at the base
+  double* sCol = reinterpret_cast<double*>(smem + (off > 32768u ? off : 32768u));
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -144,41 +153,57 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
+    for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar_x[i])));
+    for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar_r[i])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
 
   const int nk = P.blk_count ? P.blk_count[rb] : P.k_tiles;
   const int32_t* klist = P.blk_list ? P.blk_list + rb * (int64_t)P.k_tiles : nullptr;
 
-  // cp.async issue for K tile `kt` into raw stage `rs`: 16 B per (plane, row)
+  // cp.async of K tile `kt` into raw stage `rs`
   auto issue = [&](int kt, int rs) {
-    const int na = lb * 128, nbb = rbits * bn;
-    for (int u = tid; u < na + nbb; u += kThreads) {
-      if (u < na) {
+    uint8_t* ra = rawA + rs * rawA_bytes;
+    uint8_t* rbp = rawB + rs * rawB_bytes;
+    if (a_codes) {
+      // 128 rows x 8 16-byte K-cores, straight into the UMMA layout (8 lanes = one 128 B row)
+      for (int u = tid; u < 1024; u += kThreads) {
+        const int c = u & 7, r = u >> 3;
+        const int64_t row = rb * 128 + r;
+        const bool ok = row < P.m;
+        cp_async16(smem_u32(ra) + umma_off(r, c), P.lhs_codes + (ok ? row : 0) * P.lhs_ld + kt * 128 + c * 16, ok);
+      }
+    } else {
+      for (int u = tid; u < lb * 128; u += kThreads) {
         const int p = u >> 7, r = u & 127;
         const int64_t row = rb * 128 + r;
         const bool ok = row < P.m_padded;
-        const uint32_t* src = P.lhs + p * P.lwpp + (ok ? row : 0) * P.lwpr + kt * 4;
-        cp_async16(smem_u32(rawA + rs * rawA_stage + (p * 128 + r) * 4), src, ok);
-      } else {
-        const int v = u - na, p = v >> P.log2bn, j = v & (bn - 1);
+        cp_async16(smem_u32(ra) + (p * 128 + r) * 16, P.lhs + p * P.lwpp + (ok ? row : 0) * P.lwpr + kt * 4, ok);
+      }
+    }
+    if (b_codes) {
+      for (int u = tid; u < bn * 8; u += kThreads) {
+        const int c = u & 7, j = u >> 3;
+        const int64_t col = (int64_t)nt * bn + j;
+        const bool ok = col < P.n;
+        cp_async16(smem_u32(rbp) + umma_off(j, c), P.rhs_codes + (ok ? col : 0) * P.rhs_ld + kt * 128 + c * 16, ok);
+      }
+    } else {
+      for (int u = tid; u < rbits * bn; u += kThreads) {
+        const int p = u >> P.log2bn, j = u & (bn - 1);
         const int64_t vc = (int64_t)nt * bn + j;
         int64_t col = vc, pl = p;
         if (PER_PLANE) { pl = vc / P.vstride; col = vc % P.vstride; }
         const bool ok = pl < P.rbits && col < P.n_padded && vc < P.n_ext;
-        const uint32_t* src = P.rhs + (ok ? pl * P.rwpp + col * P.rwpr : 0) + kt * 4;
-        cp_async16(smem_u32(rawB + rs * rawB_stage + (p * bn + j) * 4), src, ok);
+        cp_async16(smem_u32(rbp) + (p * bn + j) * 16, P.rhs + (ok ? pl * P.rwpp + col * P.rwpr : 0) + kt * 4, ok);
       }
     }
-    cp_async_commit();
   };
 
-  // prologue: prefetch the first NR-1 K tiles (empty groups keep the group count uniform)
-  for (int s0 = 0; s0 < NR - 1; ++s0) {
-    if (s0 < nk) issue(klist ? klist[s0] : s0, s0);
-    else cp_async_commit();
+  // prologue: prefetch the first PD K tiles (empty groups keep the group count uniform)
+  for (int s0 = 0; s0 < PD; ++s0) {
+    if (s0 < nk) issue(klist ? klist[s0] : s0, s0 % NR);
+    cp_async_commit();
   }
   if (P.mode == QG_GEMM_EPILOGUE) {
     // per-column epilogue constants of this CTA's columns (same fp64 products as the
@@ -206,91 +231,93 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
   phase_stamp(P, 1);
 
   for (int it = 0; it < nk; ++it) {
-    const int st = it & 1;
-    const int pf = it + NR - 1;                        // prefetch distance NR-1
-    if (pf < nk) issue(klist ? klist[pf] : pf, pf % NR);
-    else cp_async_commit();
-    if (NR == 4) cp_async_wait<3>();
-    else if (NR == 3) cp_async_wait<2>();
-    else cp_async_wait<1>();
-    __syncthreads();                                   // raw stage it%NR visible to every thread
+    const int st = it & 1, rs = it % NR;
+    const int pf = it + PD;
+    if (pf < nk) {
+      if (pf >= NR) mbar_wait(smem_u32(&mbar_r[pf % NR]), ((pf - NR) / NR) & 1);   // stage free again
+      issue(klist ? klist[pf] : pf, pf % NR);
+    }
+    cp_async_commit();
+    if (PD >= 2) cp_async_wait<2>(); else cp_async_wait<1>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // cp.async data -> tensor-core reads
+    __syncthreads();                                   // raw stage rs visible to every thread
     if (it < 16) phase_stamp(P, 6 + 4 * it);
-    if (it >= 2) mbar_wait(smem_u32(&mbar[st]), ((it - 2) >> 1) & 1);
+    if (expand && it >= 2) mbar_wait(smem_u32(&mbar_x[st]), ((it - 2) >> 1) & 1);
     if (it < 16) phase_stamp(P, 7 + 4 * it);
-    long long tx0 = clock64();
-    const uint32_t* ra = rawA + (it % NR) * rawA_stage;
-    const uint32_t* rbw = rawB + (it % NR) * rawB_stage;
-    // A: thread -> row r = tid&127, K-cores h, h+2, h+4, h+6 (h = tid>>7): one 128-bit
-    // shared load per plane feeds four independent expansion chains.
-    {
-      const int r = tid & 127, h = tid >> 7;
-      uint32_t o[4][4];
+    if (expand) {
+      const uint32_t* ra = reinterpret_cast<const uint32_t*>(rawA + rs * rawA_bytes);
+      const uint32_t* rbw = reinterpret_cast<const uint32_t*>(rawB + rs * rawB_bytes);
+      if (!a_codes) {
+        // A: thread -> row r = tid&127, K-cores h, h+2, h+4, h+6 (h = tid>>7): one 128-bit
+        // shared load per plane feeds four independent expansion chains.
+        const int r = tid & 127, h = tid >> 7;
+        uint32_t o[4][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0;
+        for (int i = 0; i < 4; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0;
 #pragma unroll 1
-      for (int p = 0; p < lb; ++p) {
-        const uint4 w4 = *reinterpret_cast<const uint4*>(ra + (p * 128 + r) * 4);
-        const uint32_t wv[4] = {w4.x >> (16 * h), w4.y >> (16 * h), w4.z >> (16 * h), w4.w >> (16 * h)};
+        for (int p = 0; p < lb; ++p) {
+          const uint4 w4 = *reinterpret_cast<const uint4*>(ra + (p * 128 + r) * 4);
+          const uint32_t wv[4] = {w4.x >> (16 * h), w4.y >> (16 * h), w4.z >> (16 * h), w4.w >> (16 * h)};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          o[i][0] |= expand_nibble(wv[i] & 0xFu) << p;
-          o[i][1] |= expand_nibble((wv[i] >> 4) & 0xFu) << p;
-          o[i][2] |= expand_nibble((wv[i] >> 8) & 0xFu) << p;
-          o[i][3] |= expand_nibble((wv[i] >> 12) & 0xFu) << p;
+          for (int i = 0; i < 4; ++i) {
+            o[i][0] |= expand_nibble(wv[i] & 0xFu) << p;
+            o[i][1] |= expand_nibble((wv[i] >> 4) & 0xFu) << p;
+            o[i][2] |= expand_nibble((wv[i] >> 8) & 0xFu) << p;
+            o[i][3] |= expand_nibble((wv[i] >> 12) & 0xFu) << p;
+          }
+        }
+        const uint32_t abase = sA0 + st * 16384u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sts128(abase + umma_off(r, h + 2 * i), o[i][0], o[i][1], o[i][2], o[i][3]);
+      }
+      if (!b_codes) {
+        // B: thread -> column j = tid & (bn-1), K-cores c0, c0+cs, ... (bn/32 of them)
+        const int j = tid & (bn - 1), c0 = tid >> P.log2bn, cs = kThreads >> P.log2bn;
+        const uint32_t bbase = sB0 + st * bstage;
+#pragma unroll 1
+        for (int c = c0; c < 8; c += cs) {
+          const int wi = c >> 1, sh = (c & 1) * 16;
+          uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+#pragma unroll 1
+          for (int p = 0; p < rbits; ++p) {
+            const uint32_t w = rbw[(p * bn + j) * 4 + wi] >> sh;
+            const int shp = PER_PLANE ? 0 : p;
+            o0 |= expand_nibble(w & 0xFu) << shp;
+            o1 |= expand_nibble((w >> 4) & 0xFu) << shp;
+            o2 |= expand_nibble((w >> 8) & 0xFu) << shp;
+            o3 |= expand_nibble((w >> 12) & 0xFu) << shp;
+          }
+          sts128(bbase + umma_off(j, c), o0, o1, o2, o3);
         }
       }
-      const uint32_t abase = sA0 + st * 16384u;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) sts128(abase + umma_off(r, h + 2 * i), o[i][0], o[i][1], o[i][2], o[i][3]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
     }
-    // B: thread -> column j = tid & (bn-1), K-cores c0, c0+cs, ... (bn/32 of them)
-    {
-      const int j = tid & (bn - 1), c0 = tid >> P.log2bn, cs = kThreads >> P.log2bn;
-      const uint32_t bbase = sB0 + st * bstage;
-#pragma unroll 1
-      for (int c = c0; c < 8; c += cs) {
-        const int wi = c >> 1, sh = (c & 1) * 16;
-        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
-#pragma unroll 1
-        for (int p = 0; p < rbits; ++p) {
-          const uint32_t w = rbw[(p * bn + j) * 4 + wi] >> sh;
-          const int shp = PER_PLANE ? 0 : p;
-          o0 |= expand_nibble(w & 0xFu) << shp;
-          o1 |= expand_nibble((w >> 4) & 0xFu) << shp;
-          o2 |= expand_nibble((w >> 8) & 0xFu) << shp;
-          o3 |= expand_nibble((w >> 12) & 0xFu) << shp;
-        }
-        sts128(bbase + umma_off(j, c), o0, o1, o2, o3);
-      }
-    }
-    long long tx1 = clock64();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    long long tx2 = clock64();
-    __syncthreads();
     if (it < 16) phase_stamp(P, 8 + 4 * it);
-    if (P.phase_ns && it == 1 && (tid & 31) == 0) {
-      // per-warp cycle split of iteration 1: expansion / fence
-      int64_t* dbg = P.phase_ns + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kStampStride + 54;
-      dbg[warp] = (int64_t)(tx1 - tx0) * 100000 + (int64_t)(tx2 - tx1);
-    }
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t abase = a_codes ? smem_u32(rawA + rs * rawA_bytes) : sA0 + st * 16384u;
+      const uint32_t bbase = b_codes ? smem_u32(rawB + rs * rawB_bytes) : sB0 + st * bstage;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t da = umma_desc(sA0 + st * 16384u + kk * 256u);
-        const uint64_t db = umma_desc(sB0 + st * bstage + kk * 256u);
+        const uint64_t da = umma_desc(abase + kk * 256u);
+        const uint64_t db = umma_desc(bbase + kk * 256u);
         const uint32_t accum = (it > 0 || kk > 0) ? 1u : 0u;
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
                      ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(accum));
       }
+      if (expand)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&mbar_x[st])) : "memory");
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(&mbar[st])) : "memory");
+          smem_u32(&mbar_r[rs])) : "memory");
     }
     if (it < 16) phase_stamp(P, 9 + 4 * it);
   }
+  cp_async_wait<0>();
   if (nk > 0) {
-    mbar_wait(smem_u32(&mbar[(nk - 1) & 1]), ((nk - 1) >> 1) & 1);
+    mbar_wait(smem_u32(&mbar_r[(nk - 1) % NR]), ((nk - 1) / NR) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
   phase_stamp(P, 2);
@@ -391,7 +418,17 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
         codes8 |= (uint64_t)q << (8 * (g * 4 + jj));
       }
     }
-    if (packed && !colwise) {
+    if (packed && E.q_codes && rvalid) {
+      // u8 code cache in the next GEMM's K-major operand layout
+      if (E.q_codes_colmajor) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cb + jj < P.n) E.q_codes[(cb + jj) * E.q_codes_ld + myrow] = (uint8_t)(codes8 >> (8 * jj));
+      } else {
+        *reinterpret_cast<uint64_t*>(E.q_codes + myrow * E.q_codes_ld + cb) = codes8;
+      }
+    }
+    if (packed && !colwise && !E.q_skip_planes) {
       // row-wise words: column cb+jj over the warp's 32 rows; lane jj keeps the ballot
       // of column jj, then 8 lanes store one word per plane
       const uint64_t planes8 = transpose8x8(codes8);   // byte p, bit jj = bit p of code jj
@@ -411,7 +448,7 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
         if (in) dst[p * pstride] = mine;
       }
     }
-    if (colwise) {
+    if (colwise && !E.q_skip_planes) {
       // byte p of the transpose = plane p's 8 bits of this slice
       const uint64_t planes8 = transpose8x8(codes8);
       const int lr = quad * 32 + lane;
@@ -427,7 +464,7 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
   if (packed) {
     if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], rsum);
     __syncthreads();
-    if (colwise) {
+    if (colwise && !E.q_skip_planes) {
       const int64_t wpr = E.q_pcols >> 5, wpp = E.q_prows * wpr;
       const int64_t w0 = col_lo >> 5;
       for (int i = tid; i < 128 * wpc_cta * 8; i += kThreads) {
@@ -521,7 +558,9 @@ static int check_epilogue(const qg_epilogue* e) {
   if (e->use_row && !e->row_sums) return QG_ERR_ARG;
   if (e->use_col && !e->col_sums) return QG_ERR_ARG;
   if (e->out_kind == QG_OUT_REAL) return e->out_real ? QG_OK : QG_ERR_ARG;
-  if (e->out_kind != QG_OUT_PLANES || !e->q_planes) return QG_ERR_ARG;
+  if (e->out_kind != QG_OUT_PLANES) return QG_ERR_ARG;
+  if (!e->q_planes && !(e->q_skip_planes && e->q_codes)) return QG_ERR_ARG;
+  if (e->q_codes && e->q_codes_ld % 16) return QG_ERR_SHAPE;
   if (e->q_bits < 1 || e->q_bits > 8) return QG_ERR_BITS;
   if (e->q_prows % 8 || e->q_pcols % 8) return QG_ERR_SHAPE;
   if (e->q_orientation == QG_ROW_WISE && e->q_prows % 128) return QG_ERR_SHAPE;
@@ -551,11 +590,15 @@ static void set_smem_attr(size_t bytes) {
 template <bool PER_PLANE>
 static int launch_tc(GemmParams P, dim3 grid, cudaStream_t st) {
   const int rbits = PER_PLANE ? 1 : P.rbits;
-  const size_t fixed = 2 * 16384 + 2 * (size_t)P.bn * 128 + 7 * (size_t)P.bn * 8;
-  const size_t stage = (size_t)P.lbits * 128 * 16 + (size_t)rbits * P.bn * 16;
+  const bool ac = P.lhs_codes != nullptr, bc = P.rhs_codes != nullptr;
+  const size_t expanded = (ac ? 0 : 2 * 16384) + (bc ? 0 : 2 * (size_t)P.bn * 128);
+  const size_t colc = 7 * (size_t)P.bn * 8;
+  const size_t stage = (ac ? 16384 : (size_t)P.lbits * 2048) + (bc ? (size_t)P.bn * 128 : (size_t)rbits * P.bn * 16);
   const size_t budget = 227 * 1024 - 4096;           // keep room for static smem
-  P.raw_stages = (int32_t)std::max<size_t>(2, std::min<size_t>(4, (budget - fixed) / stage));
-  const size_t smem = fixed + (size_t)P.raw_stages * stage;
+  P.raw_stages = (int32_t)std::max<size_t>(2, std::min<size_t>(4, (budget - expanded - colc) / stage));
+  P.pf_dist = std::max(1, P.raw_stages - 2);
+  // layout: [expanded stages][raw ring] then sCol, never below the 32 KB epilogue scratch
+  const size_t smem = std::max<size_t>(expanded + (size_t)P.raw_stages * stage, 32768) + colc;
   const int cols = P.bn <= 32 ? 32 : P.bn <= 64 ? 64 : P.bn <= 128 ? 128 : 256;
   switch (cols) {
     case 32: set_smem_attr<PER_PLANE, 32>(smem); tc_bitgemm_kernel<PER_PLANE, 32><<<grid, kThreads, smem, st>>>(P); break;
@@ -590,6 +633,9 @@ extern "C" int qg_bitgemm(const qg_gemm_args* a, void* stream) {
   P.mode = a->mode;
   P.blk_list = a->blk_list; P.blk_count = a->blk_count;
   P.out_i32 = a->out_i32; P.overflow = a->overflow; P.phase_ns = a->phase_ns;
+  P.lhs_codes = a->lhs_codes; P.lhs_ld = a->lhs_ld; P.rhs_codes = a->rhs_codes; P.rhs_ld = a->rhs_ld;
+  if ((P.lhs_codes && (P.lhs_ld < a->k_padded || P.lhs_ld % 16)) || (P.rhs_codes && (P.rhs_ld < a->k_padded || P.rhs_ld % 16)))
+    return QG_ERR_SHAPE;
   if (a->epi) P.epi = *a->epi;
 
   // the s32 tensor accumulator is exact iff the largest possible sum fits
@@ -599,6 +645,7 @@ extern "C" int qg_bitgemm(const qg_gemm_args* a, void* stream) {
   int algo = a->algo;
   if (algo == QG_ALGO_AUTO) algo = maxsum < 2147483647.0 ? QG_ALGO_TCGEN05 : QG_ALGO_POPC;
   if (algo == QG_ALGO_TCGEN05 && maxsum >= 2147483647.0) return QG_ERR_UNSUPPORTED;
+  if (algo == QG_ALGO_POPC && (P.lhs_codes || P.rhs_codes)) return QG_ERR_UNSUPPORTED;   // POPC reads planes
 
   if (algo == QG_ALGO_TCGEN05) {
     const int64_t row_blocks = (a->m_padded + 127) / 128;
@@ -666,4 +713,35 @@ extern "C" int qg_test_div(const double* a, const double* b, const double* inv_b
   return launch_status_g();
 }
 
-extern "C" int qg_version(void) { return 14; }
+namespace qg {
+__global__ void planes_to_codes_kernel(const uint32_t* __restrict__ words, int64_t nplanes, int64_t rows, int64_t cols,
+                                       int64_t prows, int64_t pcols, int orientation, uint8_t* __restrict__ codes,
+                                       int64_t ld, int colmajor) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  // iterate in the OUTPUT's contiguous order so stores coalesce
+  int64_t r, c;
+  if (colmajor) { c = idx / rows; r = idx % rows; } else { r = idx / cols; c = idx % cols; }
+  const int64_t wpp = prows * pcols / 32;
+  int64_t off; int bit;
+  if (orientation == QG_COLUMN_WISE) { off = r * (pcols >> 5) + (c >> 5); bit = (int)(c & 31); }
+  else { off = c * (prows >> 5) + (r >> 5); bit = (int)(r & 31); }
+  uint32_t code = 0;
+  for (int64_t p = 0; p < nplanes; ++p) code |= ((__ldg(words + p * wpp + off) >> bit) & 1u) << p;
+  codes[colmajor ? c * ld + r : r * ld + c] = (uint8_t)code;
+}
+}  // namespace qg
+
+extern "C" int qg_planes_to_codes(const uint32_t* words, int64_t nplanes, int64_t rows, int64_t cols,
+                                  int64_t padded_rows, int64_t padded_cols, int orientation, uint8_t* codes,
+                                  int64_t ld, int colmajor, void* stream) {
+  if (!words || !codes || nplanes < 1 || nplanes > 8 || rows < 0 || cols < 0) return QG_ERR_ARG;
+  if (ld < (colmajor ? rows : cols)) return QG_ERR_SHAPE;
+  const int64_t n = rows * cols;
+  if (n == 0) return QG_OK;
+  qg::planes_to_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      words, nplanes, rows, cols, padded_rows, padded_cols, orientation, codes, ld, colmajor);
+  return launch_status_g();
+}
+
+extern "C" int qg_version(void) { return 15; }
