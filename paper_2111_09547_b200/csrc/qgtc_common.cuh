@@ -53,13 +53,17 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
   return __fma_rn(r, y, q);
 }
 
-// Eq.2 requantization with the fast correctly rounded division.
-__device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, double scale, double inv_scale,
+// Eq.2 requantization in the epilogue.  Measured on B200 (profiles/r01_microbench.txt)
+// the MUFU-based IEEE division beats the Markstein sequence, and F2I.F64 is ~4x slower
+// than DFMA, so floor+convert is a single round-down conversion after the range clamp.
+__device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, double scale, double /*inv*/,
                                                        uint32_t maxv) {
-  double v = floor(div_rn(__dsub_rn(x, amin), scale, inv_scale));
-  if (!(v > 0.0)) return 0u;
+  const double a = __dsub_rn(x, amin);
+  if (!(a > 0.0)) return 0u;                  // a <= 0 (or NaN): floor(a/scale) <= 0 -> 0, no division
+  const double v = __ddiv_rn(a, scale);
+  if (!(v >= 1.0)) return 0u;                 // 0 < v < 1
   if (v >= (double)maxv) return maxv;
-  return (uint32_t)v;
+  return (uint32_t)__double2int_rd(v);        // 1 <= v < maxv: floor
 }
 
 // 8x8 bit-matrix transpose of a u64 (byte i = row i): afterwards byte j holds
@@ -88,8 +92,8 @@ __device__ __forceinline__ double epi_real(const qg_epilogue& e, int64_t acc, in
   if (e.use_const) real = __dadd_rn(real, e.k_const);
   if (e.bias) real = __dadd_rn(real, e.bias[c]);
   if (e.bn_mean) {
-    real = __dadd_rn(__dmul_rn(div_rn(__dsub_rn(real, e.bn_mean[c]), e.bn_denom[c], e.bn_inv_denom[c]),
-                               e.bn_gamma[c]), e.bn_beta[c]);
+    real = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(real, e.bn_mean[c]), e.bn_denom[c]), e.bn_gamma[c]),
+                     e.bn_beta[c]);
   }
   if (e.act == QG_ACT_RELU) {
     real = (real < 0.0) ? 0.0 : real;

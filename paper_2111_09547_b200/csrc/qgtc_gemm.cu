@@ -52,7 +52,8 @@ constexpr int kStampStride = 6 + 4 * 16;   // 6 phase stamps + 4 per main-loop i
 __device__ __forceinline__ void phase_stamp(const GemmParams& P, int k) {
   if (P.phase_ns && threadIdx.x == 0) {
     uint64_t t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (k == 0 || k == 5) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));   // ns, comparable across SMs
+    else t = (uint64_t)clock64();                                             // SM cycles, fine-grained
     P.phase_ns[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kStampStride + k] = (int64_t)t;
   }
 }
@@ -391,8 +392,8 @@ __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_const
         if (E.use_const) x = __dadd_rn(x, E.k_const);
         if (E.bias) x = __dadd_rn(x, sCol[bn + cl]);
         if (E.bn_mean)
-          x = __dadd_rn(__dmul_rn(div_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl], sCol[4 * bn + cl]),
-                                  sCol[5 * bn + cl]), sCol[6 * bn + cl]);
+          x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl]), sCol[5 * bn + cl]),
+                        sCol[6 * bn + cl]);
         if (E.act == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
         else if (E.act == QG_ACT_TANH) x = tanh_f32(x);
         real[jj] = x;

@@ -26,18 +26,20 @@ for i, st in enumerate(rec):
     s = full[:, :6]
     t0 = s[:, 0].min()
     span = (s[:, 5].max() - t0) / 1e3
-    d = np.diff(s, axis=1) / 1e3
     start = (s[:, 0] - t0) / 1e3
-    print(f"launch {i}: ctas={len(s)} span={span:.1f}us start(max)={start.max():.1f}us  "
-          + "  ".join(f"{n}={d[:, k].mean():.1f}/{d[:, k].max():.1f}" for k, n in enumerate(names)))
+    cyc = np.diff(s[:, 1:5], axis=1)          # clock64 cycles between stamps 1..4
+    names = ["mainloop", "epi-compute", "store"]
+    print(f"launch {i}: ctas={len(s)} span={span:.1f}us start(max)={start.max():.1f}us  total(ns)="
+          f"{np.mean(s[:, 5] - s[:, 0]):.0f}  "
+          + "  ".join(f"{n}={cyc[:, k].mean():.0f}/{cyc[:, k].max():.0f}cyc" for k, n in enumerate(names)))
     # main-loop iteration timeline of the slowest CTA (sync'd, mma-wait done, expanded, issued)
     slow = full[np.argmax(full[:, 5] - full[:, 0])]
     its = slow[6:].reshape(16, 4)
     its = its[its[:, 0] > 0]
     if len(its):
         base = slow[1]
-        print("   slowest CTA iterations (us from setup): " + " | ".join(
-            f"{(r[0]-base)/1e3:.2f},{(r[1]-base)/1e3:.2f},{(r[2]-base)/1e3:.2f},{(r[3]-base)/1e3:.2f}" for r in its[:8]))
+        print("   slowest CTA iterations (cycles from setup: synced,mma-waited,expanded,issued): " + " | ".join(
+            f"{r[0]-base},{r[1]-base},{r[2]-base},{r[3]-base}" for r in its[:8]))
     dbg = slow[54:62]
     if dbg.any():
         print("   iteration-1 per-warp cycles (expand, fence):", [(int(x // 100000), int(x % 100000)) for x in dbg])
