@@ -244,6 +244,12 @@ int qg_edges_to_bits(const int64_t* src, const int64_t* dst, int64_t n_edges, in
 int qg_test_div(const double* a, const double* b, const double* inv_b, int64_t n, double* out, double* ref,
                 void* stream);
 
+/* Test hook: out[i] = the epilogue's requantization code of x[i] (filtered
+ * reciprocal path) and ref[i] = clamp(floor(__ddiv_rn(x - amin, scale))), so
+ * tests can prove the fast path bit-identical to quantize.py:102-104. */
+int qg_test_requant(const double* x, int64_t n, double alpha_min, double scale, double inv_scale, int bits,
+                    uint32_t* out, uint32_t* ref, void* stream);
+
 /* popcount32 (bitgemm.py:58-60) on the device. */
 int qg_popcount32(const uint32_t* in, int64_t n, int32_t* out, void* stream);
 

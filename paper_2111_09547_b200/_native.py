@@ -31,7 +31,8 @@ STATUS_CLEAR = 0x7F7F7F7F7F7F7F7F
 # every compute entry point declared in include/qgtc_b200.h
 EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes", "qg_unpack", "qg_repack",
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
-           "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes")
+           "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes",
+           "qg_test_requant")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -97,6 +98,7 @@ def lib() -> ctypes.CDLL:
             "qg_popcount32": ([_vp, _i64, _vp, _vp], ctypes.c_int),
             "qg_edges_to_bits": ([_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp], ctypes.c_int),
             "qg_test_div": ([_vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
+            "qg_test_requant": ([_vp, _i64, _f64, _f64, _f64, _i32, _vp, _vp, _vp], ctypes.c_int),
             "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():

@@ -53,17 +53,39 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
   return __fma_rn(r, y, q);
 }
 
-// Eq.2 requantization in the epilogue.  Measured on B200 (profiles/r01_microbench.txt)
-// the MUFU-based IEEE division beats the Markstein sequence, and F2I.F64 is ~4x slower
-// than DFMA, so floor+convert is a single round-down conversion after the range clamp.
-__device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, double scale, double /*inv*/,
+// Eq.2 requantization in the epilogue: code = clamp(floor(RN(a / scale)), 0, maxv),
+// a = RN(x - amin), bit-identical to the reference (quantize.py:102-104).
+// Only the floor of the correctly rounded quotient is needed, so the common case
+// avoids the division: q0 = a * RN(1/scale) has |q0 - a/scale| <= 2^-52 * 256 < 2^-43
+// for q0 < maxv + 1 <= 256, and RN(a/scale) is within 2^-45 of a/scale; if q0's
+// fractional part is farther than 2^-40 from an integer, every candidate quotient has
+// the same floor.  floor(q0) comes from a round-down add of 2^52 (no F2I, which
+// runs at ~1/4 of the DFMA rate on B200).  Near-integer cases take IEEE __ddiv_rn.
+__device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, double scale, double inv_scale,
                                                        uint32_t maxv) {
   const double a = __dsub_rn(x, amin);
-  if (!(a > 0.0)) return 0u;                  // a <= 0 (or NaN): floor(a/scale) <= 0 -> 0, no division
-  const double v = __ddiv_rn(a, scale);
-  if (!(v >= 1.0)) return 0u;                 // 0 < v < 1
+  if (!(a > 0.0)) return 0u;                  // a <= 0 (or NaN): floor(a/scale) <= 0 -> 0
+  const double q0 = __dmul_rn(a, inv_scale);
+  if (q0 >= (double)maxv + 1.0) return maxv;  // quotient >= maxv + 1 - 2^-43 > maxv
+  const double t = __dadd_rd(q0, 0x1p52);     // 2^52 + floor(q0)
+  const double fl = __dsub_rn(t, 0x1p52);     // exact
+  const double frac = __dsub_rn(q0, fl);      // exact (Sterbenz), in [0, 1)
+  uint32_t k;
+  if (frac > 0x1p-40 && frac < 1.0 - 0x1p-40) {
+    k = (uint32_t)__double2loint(t);
+  } else {
+    const double v = __ddiv_rn(a, scale);
+    k = v >= 1.0 ? (uint32_t)__double2int_rd(fmin(v, (double)maxv)) : 0u;
+  }
+  return k < maxv ? k : maxv;
+}
+
+// Reference formulation (tests): floor of the IEEE quotient, clamped.
+__device__ __forceinline__ uint32_t quantize_code_ref(double x, double amin, double scale, uint32_t maxv) {
+  const double v = floor(__ddiv_rn(__dsub_rn(x, amin), scale));
+  if (!(v > 0.0)) return 0u;
   if (v >= (double)maxv) return maxv;
-  return (uint32_t)__double2int_rd(v);        // 1 <= v < maxv: floor
+  return (uint32_t)v;
 }
 
 // 8x8 bit-matrix transpose of a u64 (byte i = row i): afterwards byte j holds

@@ -745,4 +745,24 @@ extern "C" int qg_planes_to_codes(const uint32_t* words, int64_t nplanes, int64_
   return launch_status_g();
 }
 
-extern "C" int qg_version(void) { return 15; }
+namespace qg {
+__global__ void test_requant_kernel(const double* x, int64_t n, double amin, double scale, double inv, int bits,
+                                    uint32_t* out, uint32_t* ref) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t maxv = (1u << bits) - 1u;
+  out[i] = quantize_code_fast(x[i], amin, scale, inv, maxv);
+  ref[i] = quantize_code_ref(x[i], amin, scale, maxv);
+}
+}  // namespace qg
+
+extern "C" int qg_test_requant(const double* x, int64_t n, double amin, double scale, double inv_scale, int bits,
+                               uint32_t* out, uint32_t* ref, void* stream) {
+  if (n < 0 || (n && (!x || !out || !ref)) || bits < 1 || bits > 8) return QG_ERR_ARG;
+  if (n == 0) return QG_OK;
+  qg::test_requant_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, n, amin, scale,
+                                                                                       inv_scale, bits, out, ref);
+  return launch_status_g();
+}
+
+extern "C" int qg_version(void) { return 16; }

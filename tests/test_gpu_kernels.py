@@ -48,6 +48,37 @@ def test_fast_division_is_correctly_rounded():
     _div_check(aa.ravel(), bb.ravel())
 
 
+def _requant_check(x, amin, amax, bits):
+    scale = (amax - amin) / (1 << bits)
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+    out = torch.empty(t.numel(), dtype=torch.int32, device="cuda")
+    ref = torch.empty_like(out)
+    N.call("qg_test_requant", N.ptr(t), t.numel(), amin, scale, 1.0 / scale, bits, N.ptr(out), N.ptr(ref),
+           N.stream())
+    out, ref = out.cpu().numpy(), ref.cpu().numpy()
+    np.testing.assert_array_equal(ref, O.quantize_codes(x, amin, amax, bits))   # device IEEE == numpy
+    np.testing.assert_array_equal(out, ref)
+
+
+def test_filtered_requant_is_bit_identical():
+    rng = np.random.default_rng(11)
+    n = 1_000_000
+    for (amin, amax) in [(-0.5, 0.5), (0.0, 1.0), (-3.1, 7.7), (-1e-3, 2e-3), (0.0, 37.0), (-123.4, 567.8)]:
+        for bits in (1, 2, 4, 7, 8):
+            scale = (amax - amin) / (1 << bits)
+            x = rng.uniform(amin - 0.3 * (amax - amin), amax + 0.3 * (amax - amin), n)
+            _requant_check(x, amin, amax, bits)
+            # adversarial: exactly on and one ulp around every code boundary
+            k = np.arange(-2, (1 << bits) + 3, dtype=np.float64)
+            b = amin + k * scale
+            edge = np.concatenate([b, np.nextafter(b, np.inf), np.nextafter(b, -np.inf),
+                                   np.nextafter(np.nextafter(b, np.inf), np.inf),
+                                   np.nextafter(np.nextafter(b, -np.inf), -np.inf)])
+            _requant_check(edge, amin, amax, bits)
+    specials = np.array([0.0, -0.0, np.nan, np.inf, -np.inf, 1e300, -1e300, 5e-324])
+    _requant_check(specials, -0.5, 0.5, 4)
+
+
 @pytest.mark.parametrize("bits", [1, 3, 8])
 def test_tcgen05_matches_popc_at_scale(bits):
     # A 2048 x 4096 block-diagonal (zero-tile jumping active) x X (4096 x 200, `bits` planes)
