@@ -227,10 +227,12 @@ int qg_reduce_planes(const int64_t* accs, int64_t nplanes, int64_t n, int32_t* o
                      int32_t* overflow, void* stream);
 
 /* Packed planes -> u8 codes (sum_p bit_p << p) in a K-major operand layout:
- * row-major [rows][ld] or col-major [cols][ld].  Padding entries are not written. */
+ * row-major [rows][ld] or col-major [cols][ld].  Padding entries are not written.
+ * row_sums (optional, row-major output of row-wise planes only): int64 [rows],
+ * ACCUMULATED -- the left operand's row code sums (engine.py:280). */
 int qg_planes_to_codes(const uint32_t* words, int64_t nplanes, int64_t rows, int64_t cols,
                        int64_t padded_rows, int64_t padded_cols, int orientation, uint8_t* codes,
-                       int64_t ld, int colmajor, void* stream);
+                       int64_t ld, int colmajor, int64_t* row_sums, void* stream);
 
 /* Set adjacency bits from an edge list into zero-initialised column-wise
  * words (row = src, col = dst).  Replaces the dense total x total build +

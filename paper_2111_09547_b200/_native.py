@@ -99,7 +99,8 @@ def lib() -> ctypes.CDLL:
             "qg_edges_to_bits": ([_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp], ctypes.c_int),
             "qg_test_div": ([_vp, _vp, _vp, _i64, _vp, _vp, _vp], ctypes.c_int),
             "qg_test_requant": ([_vp, _i64, _f64, _f64, _f64, _i32, _vp, _vp, _vp], ctypes.c_int),
-            "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp], ctypes.c_int),
+            "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp],
+                                   ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)
@@ -141,9 +142,83 @@ def call(name: str, *args) -> None:
     check(getattr(lib(), name)(*args), name)
 
 
+# ------------------------------------------------------------ allocation
+# Every per-forward device buffer is requested through ALLOC with a kind:
+#   "static"   -- zero-initialised once (code caches: padding must stay zero,
+#                  the valid region is fully rewritten by every forward)
+#   "volatile" -- must be zero at the start of every forward (atomic accumulators)
+#   "empty"    -- fully written by its producer
+#   "status"   -- first-bad-index cells, reset to STATUS_CLEAR every forward
+# The default allocator is plain torch; runtime.EpochRunner records the sequence
+# once and then serves it from persistent slabs, so a captured epoch has ONE
+# memset + ONE fill instead of a fill kernel per buffer.
+class TorchAlloc:
+    def take(self, shape, dtype, kind):
+        dev = device()
+        if kind == "status":
+            return torch.full(shape, STATUS_CLEAR, dtype=torch.int64, device=dev)
+        if kind == "empty":
+            return torch.empty(shape, dtype=dtype, device=dev)
+        return torch.zeros(shape, dtype=dtype, device=dev)
+
+
+ALLOC = TorchAlloc()
+
+
+def alloc(shape, dtype, kind="static") -> torch.Tensor:
+    shape = tuple(int(v) for v in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+    return ALLOC.take(shape, dtype, kind)
+
+
+class SlabPlan:
+    """Records the allocation sequence of one forward (torch-backed)."""
+
+    def __init__(self):
+        self.seq = []
+
+    def take(self, shape, dtype, kind):
+        self.seq.append((shape, dtype, kind))
+        return TorchAlloc().take(shape, dtype, kind)
+
+
+class SlabAlloc:
+    """Serves a recorded allocation sequence from persistent slabs."""
+
+    ALIGN = 256
+
+    def __init__(self, plan: SlabPlan):
+        self.seq = list(plan.seq)
+        sizes = {"static": 0, "volatile": 0, "status": 0}
+        self.offsets = []
+        for shape, dtype, kind in self.seq:
+            nbytes = max(1, int(np.prod(shape))) * torch.empty((), dtype=dtype).element_size()
+            k = "static" if kind == "empty" else kind
+            self.offsets.append((k, sizes[k]))
+            sizes[k] += -(-nbytes // self.ALIGN) * self.ALIGN
+        dev = device()
+        self.slabs = {k: torch.zeros(max(v, self.ALIGN), dtype=torch.uint8, device=dev) for k, v in sizes.items()}
+        self.slabs["status"].view(torch.int64).fill_(STATUS_CLEAR)
+        self.i = 0
+
+    def reset(self):
+        """Per-forward re-initialisation (inside the captured graph)."""
+        self.i = 0
+        self.slabs["volatile"].zero_()
+        self.slabs["status"].view(torch.int64).fill_(STATUS_CLEAR)
+
+    def take(self, shape, dtype, kind):
+        if self.i >= len(self.seq) or self.seq[self.i][0] != shape or self.seq[self.i][1] != dtype:
+            raise RuntimeError("allocation sequence diverged from the recorded forward")
+        k, off = self.offsets[self.i]
+        self.i += 1
+        n = int(np.prod(shape))
+        nbytes = max(1, n) * torch.empty((), dtype=dtype).element_size()
+        return self.slabs[k][off:off + nbytes].view(dtype)[:n].view(shape)
+
+
 # ------------------------------------------------------------ device helpers
 def new_status(n: int = 1) -> torch.Tensor:
-    return torch.full((n,), STATUS_CLEAR, dtype=torch.int64, device=device())
+    return alloc((n,), torch.int64, "status")
 
 
 def status_index(status: torch.Tensor) -> int | None:

@@ -223,7 +223,7 @@ def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, b
         e.bn_mean, e.bn_denom, e.bn_gamma, e.bn_beta, e.bn_inv_denom = (v.data_ptr() for v in vecs)
     e.act = N.ACT[kind]
     if out_params is None:
-        plan.out_real = torch.empty((rows, cols), dtype=torch.float64, device=dev)
+        plan.out_real = N.alloc((rows, cols), torch.float64, "empty")
         e.out_kind, e.out_real = N.OUT_REAL, plan.out_real.data_ptr()
         return plan
     q = out_params
@@ -236,16 +236,16 @@ def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, b
         # operand (row-major codes), a row-wise output a right operand (col-major codes)
         colmajor = out_orientation == ROW_WISE
         ld = pad128(rows if colmajor else cols)
-        codes = torch.zeros(((cols if colmajor else rows), ld), dtype=torch.uint8, device=dev)
+        codes = N.alloc(((cols if colmajor else rows), ld), torch.uint8, "static")
         plan.out_stack = CodeBackedStack(out_orientation, rows, cols, q.bits, codes, ld, colmajor, out_pad_to)
         e.q_codes, e.q_codes_ld, e.q_codes_colmajor, e.q_skip_planes = codes.data_ptr(), ld, int(colmajor), 1
         e.q_planes = 0
     else:
-        planes = torch.zeros((q.bits, pr * pc // 32), dtype=torch.int32, device=dev)
+        planes = N.alloc((q.bits, pr * pc // 32), torch.int32, "volatile")
         plan.out_stack = BitPlaneStack._wrap(out_orientation, rows, cols, pr, pc, planes)
         e.q_planes = planes.data_ptr()
     if want_row_sums:
-        plan.row_sums = torch.zeros(rows, dtype=torch.int64, device=dev)
+        plan.row_sums = N.alloc(rows, torch.int64, "volatile")
         e.q_row_sums = plan.row_sums.data_ptr()
     plan.status = N.new_status()
     e.status = plan.status.data_ptr()
@@ -291,11 +291,11 @@ class _Schedule:
         pr, pc = a.padded_rows, a.padded_cols
         self.rt, self.ct = pr // TILE_ROWS, pc // TILE_K_BITS
         nrb = -(-pr // 128)
-        self.flags = torch.empty((self.rt, self.ct), dtype=torch.uint8, device=dev)
-        self.degrees = torch.empty(a.logical_rows, dtype=torch.int64, device=dev)
-        self.zero_count = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.blk_list = torch.empty((nrb, max(self.ct, 1)), dtype=torch.int32, device=dev)
-        self.blk_count = torch.zeros(nrb, dtype=torch.int32, device=dev)
+        self.flags = N.alloc((self.rt, self.ct), torch.uint8, "empty")
+        self.degrees = N.alloc(a.logical_rows, torch.int64, "volatile")
+        self.zero_count = N.alloc(1, torch.int64, "volatile")
+        self.blk_list = N.alloc((nrb, max(self.ct, 1)), torch.int32, "empty")
+        self.blk_count = N.alloc(nrb, torch.int32, "volatile")
         self._zeros = None
         if a.dwords.numel() == 0:
             self.degrees.zero_()

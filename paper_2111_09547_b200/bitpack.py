@@ -223,17 +223,19 @@ class CodeBackedStack(BitPlaneStack):
         self._dwords = value
 
 
-def stack_code_operand(stack: BitPlaneStack, colmajor: bool):
+def stack_code_operand(stack: BitPlaneStack, colmajor: bool, row_sums=None):
     """(u8 codes, ld) of a stack in a K-major operand layout (row-major for a
-    left operand, col-major for a right one); reuses a code cache when present."""
+    left operand, col-major for a right one); reuses a code cache when present.
+    ``row_sums`` (int64, zeroed) receives the row code sums when the conversion
+    is a row-wise -> row-major transpose."""
     if isinstance(stack, CodeBackedStack) and stack.codes_colmajor == colmajor:
         return stack.codes, stack.codes_ld
     rows, cols, pr, pc = stack.dims()
     ld = pad128(rows if colmajor else cols)
-    codes = torch.zeros(((cols if colmajor else rows), ld), dtype=torch.uint8, device=stack.dwords.device)
+    codes = N.alloc(((cols if colmajor else rows), ld), torch.uint8, "static")
     if rows * cols:
         N.call("qg_planes_to_codes", N.ptr(stack.dwords), stack.bits, rows, cols, pr, pc,
-               orient_id(stack.orientation), N.ptr(codes), ld, int(colmajor), N.stream())
+               orient_id(stack.orientation), N.ptr(codes), ld, int(colmajor), N.ptr(row_sums), N.stream())
     return codes, ld
 
 

@@ -715,33 +715,102 @@ extern "C" int qg_test_div(const double* a, const double* b, const double* inv_b
 }
 
 namespace qg {
-__global__ void planes_to_codes_kernel(const uint32_t* __restrict__ words, int64_t nplanes, int64_t rows, int64_t cols,
-                                       int64_t prows, int64_t pcols, int orientation, uint8_t* __restrict__ codes,
-                                       int64_t ld, int colmajor) {
+// Direct case: the packed axis of the planes is the contiguous axis of the code
+// layout (row-wise planes -> col-major codes, column-wise planes -> row-major
+// codes).  Thread per word position: 32 codes = 32 contiguous bytes, built with
+// the nibble-expansion trick (bit i of plane p -> bit p of byte i).
+__global__ void planes_to_codes_direct_kernel(const uint32_t* __restrict__ words, int nplanes, int64_t lines,
+                                              int64_t line_len, int64_t wpl, int64_t wpp,
+                                              uint8_t* __restrict__ codes, int64_t ld) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= rows * cols) return;
-  // iterate in the OUTPUT's contiguous order so stores coalesce
-  int64_t r, c;
-  if (colmajor) { c = idx / rows; r = idx % rows; } else { r = idx / cols; c = idx % cols; }
-  const int64_t wpp = prows * pcols / 32;
-  int64_t off; int bit;
-  if (orientation == QG_COLUMN_WISE) { off = r * (pcols >> 5) + (c >> 5); bit = (int)(c & 31); }
-  else { off = c * (prows >> 5) + (r >> 5); bit = (int)(r & 31); }
-  uint32_t code = 0;
-  for (int64_t p = 0; p < nplanes; ++p) code |= ((__ldg(words + p * wpp + off) >> bit) & 1u) << p;
-  codes[colmajor ? c * ld + r : r * ld + c] = (uint8_t)code;
+  const int64_t nw = (line_len + 31) >> 5;
+  if (idx >= lines * nw) return;
+  const int64_t line = idx / nw, w = idx % nw;
+  uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int p = 0; p < nplanes; ++p) {
+    const uint32_t x = __ldg(words + p * wpp + line * wpl + w);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] |= expand_nibble((x >> (4 * q)) & 0xFu) << p;
+  }
+  uint8_t* dst = codes + line * ld + w * 32;
+  const int64_t rem = line_len - w * 32;
+  if (rem >= 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    reinterpret_cast<uint4*>(dst)[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<uint4*>(dst)[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  } else {
+    for (int i = 0; i < 32 && i < rem; ++i) dst[i] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+  }
+}
+
+// Transpose case: row-wise planes -> row-major codes (or column-wise -> col-major).
+// Block = 32 output lines x 256 positions: thread t owns position t, expands its
+// word of 32 lines into a shared tile, then the tile is written line-major with
+// coalesced stores.  Optional per-line sums (row sums of the codes).
+__global__ void __launch_bounds__(256) planes_to_codes_transpose_kernel(
+    const uint32_t* __restrict__ words, int nplanes, int64_t lines, int64_t positions, int64_t wpl, int64_t wpp,
+    uint8_t* __restrict__ codes, int64_t ld, int64_t* __restrict__ line_sums) {
+  __shared__ uint8_t tile[32][256 + 16];
+  const int t = threadIdx.x;
+  const int64_t v = blockIdx.y;                 // 32-line group
+  const int64_t pos = (int64_t)blockIdx.x * 256 + t;
+  uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (pos < positions) {
+    for (int p = 0; p < nplanes; ++p) {
+      const uint32_t x = __ldg(words + p * wpp + pos * wpl + v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] |= expand_nibble((x >> (4 * q)) & 0xFu) << p;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) tile[i][t] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+  __syncthreads();
+  // each warp writes 4 lines of 256 bytes
+  const int warp = t >> 5, lane = t & 31;
+  for (int i = warp; i < 32; i += 8) {
+    const int64_t line = v * 32 + i;
+    if (line >= lines) break;
+    uint32_t sum = 0;
+    for (int j = lane; j < 256; j += 32) {
+      const int64_t q = (int64_t)blockIdx.x * 256 + j;
+      if (q < positions) {
+        codes[line * ld + q] = tile[i][j];
+        sum += tile[i][j];
+      }
+    }
+    if (line_sums) {
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) sum += __shfl_xor_sync(QG_FULL, sum, o2);
+      if (lane == 0 && sum) atomicAdd(reinterpret_cast<unsigned long long*>(line_sums + line), (unsigned long long)sum);
+    }
+  }
 }
 }  // namespace qg
 
 extern "C" int qg_planes_to_codes(const uint32_t* words, int64_t nplanes, int64_t rows, int64_t cols,
                                   int64_t padded_rows, int64_t padded_cols, int orientation, uint8_t* codes,
-                                  int64_t ld, int colmajor, void* stream) {
+                                  int64_t ld, int colmajor, int64_t* row_sums, void* stream) {
   if (!words || !codes || nplanes < 1 || nplanes > 8 || rows < 0 || cols < 0) return QG_ERR_ARG;
   if (ld < (colmajor ? rows : cols)) return QG_ERR_SHAPE;
-  const int64_t n = rows * cols;
-  if (n == 0) return QG_OK;
-  qg::planes_to_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      words, nplanes, rows, cols, padded_rows, padded_cols, orientation, codes, ld, colmajor);
+  if (rows * cols == 0) return QG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t wpp = padded_rows * padded_cols / 32;
+  const bool rowwise = orientation == QG_ROW_WISE;
+  if (rowwise == (bool)colmajor) {
+    // packed axis == contiguous code axis
+    const int64_t lines = colmajor ? cols : rows, len = colmajor ? rows : cols;
+    const int64_t wpl = rowwise ? padded_rows / 32 : padded_cols / 32;
+    const int64_t n = lines * ((len + 31) / 32);
+    qg::planes_to_codes_direct_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        words, (int)nplanes, lines, len, wpl, wpp, codes, ld);
+    if (row_sums) return QG_ERR_UNSUPPORTED;   // row sums only on the transpose (left-operand) path
+  } else {
+    // row-wise planes -> row-major codes: lines = rows, positions = columns
+    const int64_t lines = colmajor ? cols : rows, positions = colmajor ? rows : cols;
+    const int64_t wpl = rowwise ? padded_rows / 32 : padded_cols / 32;
+    dim3 grid((unsigned)((positions + 255) / 256), (unsigned)((lines + 31) / 32));
+    qg::planes_to_codes_transpose_kernel<<<grid, 256, 0, st>>>(words, (int)nplanes, lines, positions, wpl, wpp,
+                                                               codes, ld, colmajor ? nullptr : row_sums);
+  }
   return launch_status_g();
 }
 

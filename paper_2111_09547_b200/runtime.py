@@ -49,11 +49,22 @@ class EpochRunner:
     def capture(self):
         _prepared(self.model)
         with torch.cuda.stream(self.stream):
-            self._forward_all(verify=True)          # eager warm-up: attributes, allocator, error checks
+            plan = N.SlabPlan()
+            N.ALLOC = plan
+            try:
+                self._forward_all(verify=True)      # eager warm-up: records the allocation sequence
+            finally:
+                N.ALLOC = N.TorchAlloc()
             torch.cuda.synchronize()
+            self.slabs = N.SlabAlloc(plan)
             self.graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.graph, stream=self.stream):
-                self.logits = self._forward_all(verify=False)
+            N.ALLOC = self.slabs
+            try:
+                with torch.cuda.graph(self.graph, stream=self.stream):
+                    self.slabs.reset()              # 1 memset + 1 fill per epoch
+                    self.logits = self._forward_all(verify=False)
+            finally:
+                N.ALLOC = N.TorchAlloc()
         self._checks = list(getattr(self.model, "_pending_checks", []))
         return self
 
@@ -63,8 +74,9 @@ class EpochRunner:
         return self.logits
 
     def kernel_launches_per_epoch(self) -> int:
-        """Native kernels per epoch: per batch 2 (tile scan) + per layer 2 fused GEMMs (+1 repack for GIN)."""
-        per_batch = 2 + 2 * len(self.model.layers) + (1 if self.model.kind == "batched-gin" else 0)
+        """Native kernels per epoch: per batch 2 (tile scan + schedule) + 1 entry code
+        conversion + 2 fused GEMMs per layer."""
+        per_batch = 2 + 1 + 2 * len(self.model.layers)
         return per_batch * len(self.batches)
 
 
