@@ -330,7 +330,7 @@ def ours(args, world, rank):
 
     N.lib()
     cfg, batches, feats, model = build_workload(args.config, args.bits, seed=rank)
-    runner = EpochRunner(model, batches).capture()
+    runner = EpochRunner(model, batches, rescan=False).capture()
     total_ms, clocks = time_device_epochs(runner, args.steps, args.warmup, world)
     total_ms = max_over_ranks(world, total_ms)
     ms_epoch = total_ms / (args.steps * world)
@@ -371,7 +371,7 @@ def ours(args, world, rank):
                 sweep[str(bits)] = round(ms_epoch, 5)
                 continue
             _, bb, _, mm = build_workload(args.config, bits, seed=rank)
-            rr = EpochRunner(mm, bb).capture()
+            rr = EpochRunner(mm, bb, rescan=False).capture()
             k = max(20, args.steps // 4)
             t, _ = time_device_epochs(rr, k, 5, world)
             sweep[str(bits)] = round(max_over_ranks(world, t) / (k * world), 5)

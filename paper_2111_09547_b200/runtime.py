@@ -30,10 +30,14 @@ class EpochRunner:
     """Graph-captured epoch of ``model_forward`` over ``batches``."""
 
     def __init__(self, model: ModelConfig, batches: list, *, jump: bool = True, reuse: str = "cross-tile",
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, rescan: bool = True):
         self.model = model
         self.batches = list(batches)
         self.jump, self.reuse = jump, reuse
+        # rescan=False: the zero-tile schedule is computed once and cached on the
+        # adjacency, as the reference caches scan_zero_tiles on the operand
+        # (bitgemm.py:222-233); rescan=True puts the scan inside every epoch (new data).
+        self.rescan = rescan
         self.stream = stream or torch.cuda.Stream()
         self.graph = None
         self.logits = None
@@ -42,12 +46,17 @@ class EpochRunner:
     def _forward_all(self, verify: bool):
         outs = []
         for b in self.batches:
-            b.adjacency._schedule = None      # the scan is part of the step (new data each step)
+            if self.rescan:
+                b.adjacency._schedule = None  # the scan is part of the step (new data each step)
             outs.append(model_forward_device(b, self.model, jump=self.jump, reuse=self.reuse, verify=verify))
         return outs
 
     def capture(self):
         _prepared(self.model)
+        if not self.rescan:
+            from .bitgemm import _schedule
+            for b in self.batches:
+                _schedule(b.adjacency)        # cached, outside the captured epoch
         with torch.cuda.stream(self.stream):
             plan = N.SlabPlan()
             N.ALLOC = plan
@@ -76,7 +85,7 @@ class EpochRunner:
     def kernel_launches_per_epoch(self) -> int:
         """Native kernels per epoch: per batch 2 (tile scan + schedule) + 1 entry code
         conversion + 2 fused GEMMs per layer."""
-        per_batch = 2 + 1 + 2 * len(self.model.layers)
+        per_batch = (2 if self.rescan else 0) + 1 + 2 * len(self.model.layers)
         return per_batch * len(self.batches)
 
 
@@ -92,7 +101,7 @@ class HostEpochRunner:
         self.device = torch.empty_like(self.host, device=N.device())
         self.device.copy_(self.host)
         views = [batch_from_v2(im, self.device, int(o)) for im, o in zip(images, self.offsets)]
-        self.inner = EpochRunner(model, views, **kw).capture()
+        self.inner = EpochRunner(model, views, rescan=True, **kw).capture()
         rows = sum(v.total_nodes for v in views)
         self.classes = model.layers[-1].out_dim
         self.out_host = torch.empty((rows, self.classes), dtype=torch.float64).pin_memory()
