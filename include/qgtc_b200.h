@@ -221,6 +221,68 @@ typedef struct {
  */
 int qg_bitgemm(const qg_gemm_args* args, void* stream);
 
+/* ---- tiled fast path (engine) ------------------------------------------------
+ * Operands in HBM in the UMMA K-major interleaved "tiled" layout: a left operand
+ * (M x K) is stored as K slabs of 128, each [pad128(M)/8][8 K-cores][8 rows][16 B]
+ * (a 128-row block of a slab is a contiguous 16 KB); a right operand (K x N) as K
+ * slabs of [npad/8][8][8][16 B].  The 1-bit adjacency is stored as the array of
+ * its non-zero 128x128 blocks expanded to 0/1 bytes (16 KB each), addressed by a
+ * per-128-row-block schedule.  One segment = one subgraph batch; a launch covers
+ * any number of segments (CTA -> segment, row block, N tile).                   */
+typedef struct {
+  const uint8_t* a;            /* left tiles: dense slabs, or adjacency blocks       */
+  const uint8_t* b;            /* right tiles (slab pitch b_npad * 128)              */
+  const int32_t* blk_count;    /* adjacency: non-zero K tiles per 128-row block      */
+  const int32_t* blk_base;     /* adjacency: first block index of each row block     */
+  const int32_t* blk_kt;       /* adjacency: K tile of each block                    */
+  const int64_t* row_sums;     /* epilogue lhs row sums (degrees / code row sums)    */
+  uint8_t* q_codes;            /* epilogue: tiled u8 code output                     */
+  int64_t* q_row_sums;         /* epilogue: int64 row sums of the codes, ACCUMULATED */
+  double* out_real;            /* fp64 logits [m][n]                                 */
+  int32_t* out_i32;            /* int32 accumulator [m][n] (QG_GEMM_I32)             */
+  int64_t* status;             /* first non-finite requant input index               */
+  int64_t m;                   /* logical rows                                       */
+  int64_t r128;                /* rows padded to 128 (left slab pitch / left output) */
+  int64_t cta_begin;           /* first CTA of this segment                          */
+  int32_t k_tiles;             /* dense left: K tiles                                */
+  int32_t pad_;
+} qg_tseg;
+
+typedef struct {
+  const qg_tseg* segs;         /* DEVICE array of segments (sorted by cta_begin)     */
+  int32_t nsegs;
+  int32_t a_blocks;            /* 1: left = adjacency blocks, 0: dense left slabs    */
+  int64_t total_ctas;
+  int64_t b_npad;              /* right operand padded N (multiple of bn)            */
+  int64_t n;                   /* logical output columns                             */
+  int32_t bn, n_tiles;         /* N tile (power of two 32..256) and tiles per row block */
+  int32_t mode;                /* QG_GEMM_I32 or QG_GEMM_EPILOGUE                    */
+  int32_t out_layout;          /* 0 row-major fp64/int32, 1 left-tiled codes, 2 right-tiled codes */
+  int64_t out_npad;            /* right-tiled output: padded N                       */
+  const qg_epilogue* epi;      /* shared epilogue scalars / per-column vectors       */
+} qg_tiled_args;
+
+/* Warp-specialised tiled bit-GEMM (cp.async.bulk producer, single-thread
+ * tcgen05.mma kind::i8 issuer, 8-warp fused epilogue).  Same arithmetic as
+ * qg_bitgemm's EPILOGUE / I32 modes; replaces the per-batch loop of
+ * engine.py:320-332 for a whole epoch layer stage. */
+int qg_tiled_gemm(const qg_tiled_args* args, void* stream);
+
+/* Gather the non-zero 128x128 blocks (blk_rb/blk_kt) of a column-wise 1-bit matrix
+ * into `packed` (2 KB each; skipped when a_words == NULL and `packed` is already
+ * filled, e.g. shipped by the QGT2 tile-sparse wire format), expand them to 16 KB
+ * UMMA byte blocks and accumulate row degrees (graph.py:292-295; degrees zeroed). */
+int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,
+                     const int32_t* blk_rb, const int32_t* blk_kt, int64_t nblocks, uint32_t* packed,
+                     uint8_t* bytes, int64_t* degrees, void* stream);
+
+/* Plain row-major u8 codes [rows][ld] <-> left (right = 0, pitch = pad128(rows)) or
+ * right (right = 1, pitch = npad) tiled layout. */
+int qg_codes_to_tiles(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ld, int right, int64_t pitch,
+                      uint8_t* tiles, void* stream);
+int qg_tiles_to_codes(const uint8_t* tiles, int64_t rows, int64_t cols, int right, int64_t pitch, uint8_t* codes,
+                      int64_t ld, void* stream);
+
 /* Shifted reduction sum_p acc[p] << p (int64 in) narrowed to int32 with an
  * overflow flag.  Replaces reduce_bitplanes (bitgemm.py:291-298). */
 int qg_reduce_planes(const int64_t* accs, int64_t nplanes, int64_t n, int32_t* out,

@@ -204,11 +204,13 @@ def _build_epilogue_raw(lhs_params, rhs_params, row_sums, col_sums, inner_dim, b
     if amb != 0.0:
         rs = _dev_vec(row_sums, torch.int64)
         plan.keep.append(rs)
-        e.use_row, e.k_row, e.row_sums = 1, sa * amb, rs.data_ptr()
+        e.use_row, e.k_row = 1, sa * amb
+        e.row_sums = rs.data_ptr() if rs is not None else None     # None: set per segment
     if ama != 0.0:
         cs = _dev_vec(col_sums, torch.int64)
         plan.keep.append(cs)
-        e.use_col, e.k_col, e.col_sums = 1, sb * ama, cs.data_ptr()
+        e.use_col, e.k_col = 1, sb * ama
+        e.col_sums = cs.data_ptr() if cs is not None else None
     if ama != 0.0 and amb != 0.0:
         e.use_const, e.k_const = 1, (float(inner_dim) * ama) * amb
     if bias is not None:

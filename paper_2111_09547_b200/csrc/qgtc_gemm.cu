@@ -58,44 +58,6 @@ __device__ __forceinline__ void phase_stamp(const GemmParams& P, int k) {
   }
 }
 
-__device__ __forceinline__ uint4 ldg128(const uint32_t* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d));
-}
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-  // K-major, SWIZZLE_NONE canonical layout: core matrix = 8 rows x 16 B;
-  // LBO = 128 B (next core along K), SBO = 1024 B (next 8-row group).
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)(128 >> 4) << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;
-}
-__device__ __forceinline__ uint32_t idesc_u8(int n) {
-  return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);  // S32 acc, u8 x u8, K-major
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-  }
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  const int n = valid ? 16 : 0;   // src-size 0 -> zero fill
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-constexpr int kThreads = 256;
-
 // Expand one unit = (operand row, K-core c): 16 code bytes from `nb` plane
 // words (raw[p*stride + row*4 + (c>>1)]).  Codes: sum_p bit_p << p; ZERO_ONE:
 // a single plane's 0/1 bytes.
@@ -116,8 +78,6 @@ __device__ __forceinline__ void expand_unit(const uint32_t* raw, int pstride, in
   sts128(dst, o0, o1, o2, o3);
 }
 
-// smem address of (operand row r, K-core c) in the UMMA K-major interleaved layout
-__device__ __forceinline__ uint32_t umma_off(int r, int c) { return (uint32_t)((r >> 3) * 1024 + c * 128 + (r & 7) * 16); }
 
 template <bool PER_PLANE, int TMEM_COLS>
 __global__ void __launch_bounds__(kThreads) tc_bitgemm_kernel(const __grid_constant__ GemmParams P) {
@@ -834,4 +794,4 @@ extern "C" int qg_test_requant(const double* x, int64_t n, double amin, double s
   return launch_status_g();
 }
 
-extern "C" int qg_version(void) { return 16; }
+extern "C" int qg_version(void) { return 20; }

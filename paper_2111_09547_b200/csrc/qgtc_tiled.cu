@@ -1,0 +1,372 @@
+// Tiled, warp-specialised bit-GEMM for sm_100a (the engine's fast path).
+//
+// Operands live in HBM in the UMMA K-major interleaved layout (qgtc_common.cuh
+// left/right_tile_off): the 1-bit adjacency as 16 KB byte blocks (only the
+// non-zero 128x128 blocks, expanded once per batch), activations and weights as
+// u8 code caches written by the previous epilogue.  Per K tile a stage is
+// therefore exactly two contiguous bulk copies (TMA engine, UBLKCP) completing on
+// one mbarrier:
+//   warp 0 lane 0  producer   wait empty[s] -> expect_tx -> 2x cp.async.bulk
+//   warp 1 lane 0  MMA        wait full[s]  -> 4x tcgen05.mma kind::i8 -> commit empty[s]
+//   all 8 warps    epilogue   wait done     -> tcgen05.ld -> fp64 dequant/bias/BN/act
+//                                              -> requant -> tiled u8 codes + row sums
+//                                              (or fp64 logits / int32)
+// No per-tile __syncthreads.  One launch may cover many batches ("segments"):
+// CTA -> (segment, 128-row block, N tile), so an epoch layer stage over all
+// subgraph batches is a single grid.
+#include <algorithm>
+#include "qgtc_common.cuh"
+
+namespace qg {
+
+struct TiledParams {
+  const qg_tseg* segs;
+  int32_t nsegs;
+  int32_t a_blocks;         // 1: left operand = adjacency blocks (schedule), 0: dense left slabs
+  int64_t b_npad;           // right operand padded N (slab pitch = b_npad * 128)
+  int64_t n;                // logical output columns
+  int32_t bn, log2bn, n_tiles, stages;
+  int32_t mode;             // QG_GEMM_I32 / QG_GEMM_EPILOGUE
+  int32_t out_layout;       // 0 fp64/int32 row-major, 1 left-tiled codes, 2 right-tiled codes
+  int64_t out_npad;         // right-tiled output: padded N of the output (slab pitch)
+  qg_epilogue epi;          // shared scalars + per-column vectors (per-row pointers come from segs)
+};
+
+constexpr int kTThreads = 256;
+
+template <int TMEM_COLS>
+__global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ unsigned long long sRowSum[128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bn = P.bn, S = P.stages;
+
+  // ---- segment lookup (uniform): last segment with cta_begin <= blockIdx.x
+  int lo = 0, hi = P.nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.segs[mid].cta_begin <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const qg_tseg& G = P.segs[lo];
+  const int64_t local = (int64_t)blockIdx.x - G.cta_begin;
+  const int64_t rb = local / P.n_tiles;
+  const int nt = (int)(local % P.n_tiles);
+  const int64_t n0 = (int64_t)nt * bn;
+
+  const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u;
+  uint8_t* stage0 = smem;
+  const uint32_t stage_bytes = a_bytes + b_bytes;
+  double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);   // [7][bn] per-column constants
+
+  int nk, kbase = 0;
+  if (P.a_blocks) { nk = G.blk_count[rb]; kbase = G.blk_base[rb]; }
+  else nk = G.k_tiles;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  const bool fused = P.mode == QG_GEMM_EPILOGUE;
+  const qg_epilogue& E = P.epi;
+  if (fused) {
+    for (int i = tid; i < bn; i += kTThreads) {
+      const int64_t c = n0 + i;
+      const bool ok = c < P.n;
+      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
+      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
+      if (E.bn_mean) {
+        sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
+        sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
+        sCol[5 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
+        sCol[6 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+      }
+    }
+  }
+  if (tid < 128) sRowSum[tid] = 0ull;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer: two bulk copies per K tile ----------------
+    const uint8_t* bbase = G.b + (n0 >> 3) * 1024;
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % S;
+      if (it >= S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
+      int kt;
+      const uint8_t* asrc;
+      if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
+      else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
+      uint8_t* dst = stage0 + (size_t)s * stage_bytes;
+      mbar_expect_tx(&full[s], a_bytes + b_bytes);
+      bulk_g2s(dst, asrc, a_bytes, &full[s]);
+      bulk_g2s(dst + a_bytes, bbase + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = idesc_u8(bn);
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % S;
+      mbar_wait(smem_u32(&full[s]), (it / S) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_i8(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+      umma_commit(&empty[s]);
+    }
+    if (nk > 0) umma_commit(&done);
+  }
+  __syncwarp();
+  if (nk > 0) {
+    mbar_wait(smem_u32(&done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+
+  // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
+  const int quad = warp & 3, half = warp >> 2;
+  const int64_t r0 = rb * 128 + quad * 32;
+  const int64_t myrow = r0 + lane;
+  const bool rvalid = myrow < G.m;
+  const int64_t rem_cols = P.n - n0;
+  const int ncols_cta = rem_cols <= 0 ? 0 : (rem_cols < bn ? (int)rem_cols : bn);
+  const int nslices = (ncols_cta + 7) >> 3;
+  const bool packed = fused && E.out_kind == QG_OUT_PLANES;
+  const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
+  const double rterm = (fused && E.use_row && rvalid) ? __dmul_rn(E.k_row, (double)G.row_sums[myrow]) : 0.0;
+  unsigned long long rsum = 0;
+  for (int sl = half; sl < nslices; sl += 2) {
+    const int64_t cb = n0 + sl * 8;
+    uint64_t codes8 = 0;
+#pragma unroll 1
+    for (int g = 0; g < 2; ++g) {
+      uint32_t v[4];
+      if (nk > 0) {
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sl * 8 + g * 4);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+        v[0] = v[1] = v[2] = v[3] = 0;
+      }
+      const int64_t c4 = cb + g * 4;
+      if (!fused) {
+        if (rvalid) {
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (c4 + jj < P.n) G.out_i32[myrow * P.n + c4 + jj] = (int32_t)v[jj];
+        }
+        continue;
+      }
+      double real[4];
+      const int cl4 = sl * 8 + g * 4;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int cl = cl4 + jj;
+        double x = __dmul_rn(E.k_acc, (double)(int32_t)v[jj]);
+        if (E.use_row) x = __dadd_rn(x, rterm);
+        if (E.use_col) x = __dadd_rn(x, sCol[cl]);
+        if (E.use_const) x = __dadd_rn(x, E.k_const);
+        if (E.bias) x = __dadd_rn(x, sCol[bn + cl]);
+        if (E.bn_mean)
+          x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl]), sCol[5 * bn + cl]),
+                        sCol[6 * bn + cl]);
+        if (E.act == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
+        else if (E.act == QG_ACT_TANH) x = tanh_f32(x);
+        real[jj] = x;
+      }
+      if (!packed) {
+        if (rvalid) {
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (c4 + jj < P.n) G.out_real[myrow * P.n + c4 + jj] = real[jj];
+        }
+        continue;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int64_t c = c4 + jj;
+        uint32_t q = 0;
+        if (rvalid && c < P.n) {
+          if (!isfinite(real[jj]) && G.status) status_min(G.status, myrow * P.n + c);
+          q = quantize_code_fast(real[jj], E.q_amin, E.q_scale, E.q_inv_scale, maxv);
+          rsum += q;
+        }
+        codes8 |= (uint64_t)q << (8 * (g * 4 + jj));
+      }
+    }
+    if (packed && rvalid) {
+      if (P.out_layout == 1) {
+        // next LEFT operand: 8 consecutive K bytes of this row = one 8-byte store
+        *reinterpret_cast<uint64_t*>(G.q_codes + left_tile_off(myrow, cb, G.r128)) = codes8;
+      } else {
+        // next RIGHT operand (K = this row index): lanes of a warp write consecutive bytes
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cb + jj < P.n) G.q_codes[right_tile_off(myrow, cb + jj, P.out_npad)] = (uint8_t)(codes8 >> (8 * jj));
+      }
+    }
+  }
+  if (packed && G.q_row_sums) {
+    if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], rsum);
+    __syncthreads();
+    if (tid < 128 && rb * 128 + tid < G.m && sRowSum[tid])
+      atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[tid]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+// ------------------------------------------------ adjacency block preparation
+// Gather the non-zero 128x128 blocks of a column-wise packed 1-bit matrix into a
+// compact array of packed blocks (128 rows x 4 words = 2 KB each), following the
+// schedule (blk_base / blk_kt).  One warp per block.
+__global__ void block_gather_kernel(const uint32_t* __restrict__ a, int64_t prows, int64_t pcols,
+                                    const int32_t* __restrict__ blk_rb, const int32_t* __restrict__ blk_kt,
+                                    int64_t nblocks, uint32_t* __restrict__ packed) {
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= nblocks) return;
+  const int64_t rb = blk_rb[b], kt = blk_kt[b], wpr = pcols >> 5;
+  for (int r = lane; r < 128; r += 32) {
+    const int64_t row = rb * 128 + r;
+    uint4 q = make_uint4(0, 0, 0, 0);
+    if (row < prows) q = __ldg(reinterpret_cast<const uint4*>(a + row * wpr + kt * 4));
+    reinterpret_cast<uint4*>(packed)[b * 128 + r] = q;
+  }
+}
+
+// Expand packed blocks to UMMA-layout byte blocks (16 KB each) and accumulate the
+// row degrees (popcount) -- graph.py:292-295.  Block = 256 threads per packed block:
+// thread -> (row r = t & 127, K-core pair), 4 K-cores of 16 bytes each.
+__global__ void __launch_bounds__(256) block_expand_kernel(const uint32_t* __restrict__ packed, int64_t nblocks,
+                                                           const int32_t* __restrict__ blk_rb,
+                                                           uint8_t* __restrict__ bytes, int64_t* __restrict__ degrees,
+                                                           int64_t rows) {
+  const int64_t b = blockIdx.x;
+  if (b >= nblocks) return;
+  const int t = threadIdx.x, r = t & 127, h = t >> 7;
+  const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(packed) + b * 128 + r);
+  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+  uint8_t* blk = bytes + b * 16384;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = h + 2 * i;                   // K-core: bits 16c..16c+15 = word c>>1, half c&1
+    const uint32_t x = w[c >> 1] >> ((c & 1) * 16);
+    const uint4 o = make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu),
+                               expand_nibble((x >> 8) & 0xFu), expand_nibble((x >> 12) & 0xFu));
+    *reinterpret_cast<uint4*>(blk + umma_off(r, c)) = o;
+  }
+  if (degrees && h == 0) {
+    const int64_t row = (int64_t)blk_rb[b] * 128 + r;
+    const int d = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+    if (row < rows && d) atomicAdd(reinterpret_cast<unsigned long long*>(degrees + row), (unsigned long long)d);
+  }
+}
+
+// Plain code matrix (row-major [rows][ld]) -> left- or right-tiled layout.
+__global__ void codes_to_tiles_kernel(const uint8_t* __restrict__ codes, int64_t rows, int64_t cols, int64_t ld,
+                                      int right, int64_t pitch, uint8_t* __restrict__ tiles) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i / cols, c = i % cols;
+  // left: rows = M, cols = K (pitch = r128); right: rows = K, cols = N (pitch = npad)
+  const int64_t off = right ? right_tile_off(r, c, pitch) : left_tile_off(r, c, pitch);
+  tiles[off] = codes[r * ld + c];
+}
+
+// Tiled codes -> plain row-major codes (materialising plane views of code caches).
+__global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t rows, int64_t cols, int right,
+                                      int64_t pitch, uint8_t* __restrict__ codes, int64_t ld) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i / cols, c = i % cols;
+  const int64_t off = right ? right_tile_off(r, c, pitch) : left_tile_off(r, c, pitch);
+  codes[r * ld + c] = tiles[off];
+}
+
+}  // namespace qg
+
+using namespace qg;
+
+static inline int tstatus() { return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA; }
+
+template <int COLS>
+static void tiled_attr(size_t bytes) {
+  static size_t done = 0;
+  if (bytes > done) {
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done = bytes;
+  }
+}
+
+extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
+  if (!a || !a->segs || a->nsegs < 1 || a->total_ctas < 1) return QG_ERR_ARG;
+  if (a->bn < 32 || a->bn > 256 || (a->bn & (a->bn - 1))) return QG_ERR_ARG;
+  if (a->mode != QG_GEMM_I32 && a->mode != QG_GEMM_EPILOGUE) return QG_ERR_ARG;
+  if (a->mode == QG_GEMM_EPILOGUE && !a->epi) return QG_ERR_ARG;
+  if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) return QG_ERR_SHAPE;
+  TiledParams P{};
+  P.segs = a->segs; P.nsegs = a->nsegs; P.a_blocks = a->a_blocks; P.b_npad = a->b_npad; P.n = a->n;
+  P.bn = a->bn; P.n_tiles = a->n_tiles; P.mode = a->mode; P.out_layout = a->out_layout; P.out_npad = a->out_npad;
+  P.log2bn = 5;
+  while ((1 << P.log2bn) < P.bn) ++P.log2bn;
+  if (a->epi) P.epi = *a->epi;
+  const size_t stage = 16384 + (size_t)P.bn * 128;
+  const size_t cols = 7 * (size_t)P.bn * 8;
+  const size_t budget = 227 * 1024 - 8192;
+  P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
+  const size_t smem = (size_t)P.stages * stage + cols;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)a->total_ctas;
+  switch (P.bn) {
+    case 32: tiled_attr<32>(smem); tc_tiled_kernel<32><<<grid, kTThreads, smem, st>>>(P); break;
+    case 64: tiled_attr<64>(smem); tc_tiled_kernel<64><<<grid, kTThreads, smem, st>>>(P); break;
+    case 128: tiled_attr<128>(smem); tc_tiled_kernel<128><<<grid, kTThreads, smem, st>>>(P); break;
+    default: tiled_attr<256>(smem); tc_tiled_kernel<256><<<grid, kTThreads, smem, st>>>(P); break;
+  }
+  return tstatus();
+}
+
+extern "C" int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,
+                                const int32_t* blk_rb, const int32_t* blk_kt, int64_t nblocks, uint32_t* packed,
+                                uint8_t* bytes, int64_t* degrees, void* stream) {
+  if (nblocks < 0 || (nblocks && (!blk_rb || !bytes || !packed))) return QG_ERR_ARG;
+  if (nblocks == 0) return QG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a_words)   // gather from the dense packed matrix; otherwise `packed` is already filled
+    block_gather_kernel<<<(unsigned)((nblocks * 32 + 255) / 256), 256, 0, st>>>(a_words, padded_rows, padded_cols,
+                                                                                blk_rb, blk_kt, nblocks, packed);
+  block_expand_kernel<<<(unsigned)nblocks, 256, 0, st>>>(packed, nblocks, blk_rb, bytes, degrees, rows);
+  return tstatus();
+}
+
+extern "C" int qg_codes_to_tiles(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ld, int right,
+                                 int64_t pitch, uint8_t* tiles, void* stream) {
+  if (!codes || !tiles || rows < 0 || cols < 0 || ld < cols) return QG_ERR_ARG;
+  const int64_t n = rows * cols;
+  if (n == 0) return QG_OK;
+  codes_to_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(codes, rows, cols, ld, right,
+                                                                                      pitch, tiles);
+  return tstatus();
+}
+
+extern "C" int qg_tiles_to_codes(const uint8_t* tiles, int64_t rows, int64_t cols, int right, int64_t pitch,
+                                 uint8_t* codes, int64_t ld, void* stream) {
+  if (!codes || !tiles || rows < 0 || cols < 0 || ld < cols) return QG_ERR_ARG;
+  const int64_t n = rows * cols;
+  if (n == 0) return QG_OK;
+  tiles_to_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(tiles, rows, cols, right, pitch,
+                                                                                      codes, ld);
+  return tstatus();
+}

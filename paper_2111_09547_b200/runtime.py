@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .engine import ModelConfig, _prepared, model_forward_device
+from .engine import ModelConfig, _prepared, model_forward_group
 from .graph import batch_from_v2, pack_batch_v2
 
 
@@ -44,19 +44,18 @@ class EpochRunner:
         self._keep = []
 
     def _forward_all(self, verify: bool):
-        outs = []
         for b in self.batches:
             if self.rescan:
                 b.adjacency._schedule = None  # the scan is part of the step (new data each step)
-            outs.append(model_forward_device(b, self.model, jump=self.jump, reuse=self.reuse, verify=verify))
-        return outs
+                b.adjacency._blocked = None
+        return model_forward_group(self.batches, self.model, jump=self.jump, reuse=self.reuse, verify=verify)
 
     def capture(self):
         _prepared(self.model)
         if not self.rescan:
-            from .bitgemm import _schedule
+            from .tiled import blocked
             for b in self.batches:
-                _schedule(b.adjacency)        # cached, outside the captured epoch
+                blocked(b.adjacency)          # schedule + expanded blocks cached, outside the epoch
         with torch.cuda.stream(self.stream):
             plan = N.SlabPlan()
             N.ALLOC = plan
@@ -85,8 +84,10 @@ class EpochRunner:
     def kernel_launches_per_epoch(self) -> int:
         """Native kernels per epoch: per batch 2 (tile scan + schedule) + 1 entry code
         conversion + 2 fused GEMMs per layer."""
-        per_batch = (2 if self.rescan else 0) + 1 + 2 * len(self.model.layers)
-        return per_batch * len(self.batches)
+        per_epoch = 2 * len(self.model.layers) + 2 * len(self.batches)   # grouped GEMMs + entry conversions
+        if self.rescan:
+            per_epoch += 4 * len(self.batches)                              # scan, schedule, gather, expand
+        return per_epoch
 
 
 class HostEpochRunner:

@@ -1,0 +1,259 @@
+"""Tiled fast path: operands in the UMMA K-major layout + grouped multi-batch GEMMs.
+
+The engine's hot loop (engine.py:235-332) runs here.  For every GEMM the left
+and right operands are stored in HBM exactly as the tcgen05 MMA reads them from
+shared memory (see include/qgtc_b200.h "tiled fast path"), so the kernel moves
+each K tile with two bulk copies and never unpacks bits on the critical path:
+
+* the 1-bit adjacency -> its non-zero 128x128 blocks as 0/1 bytes (16 KB each),
+  built once per batch from the zero-tile schedule (the reference caches the
+  scan on the operand, bitgemm.py:222-233) and reused by every layer;
+* activations -> u8 code caches written by the producing epilogue in the
+  layout their consumer reads (left-tiled for X.W, right-tiled for A.X);
+* weights -> right-tiled codes of W, once per model.
+
+A layer stage over ALL batches of an epoch is one ``qg_tiled_gemm`` launch
+(one segment per batch), so the 188-batch configs launch 2 kernels per layer.
+Packed planes (the reference's ``words``) are materialised lazily from the
+code caches only when the API asks for them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .bitpack import COLUMN_WISE, ROW_WISE, BitPlaneStack, pad128, padded_dims
+
+TILE = 128
+
+
+def npad_of(n: int) -> int:
+    """Right-operand column padding: a power of two >= 32 up to 256, else a multiple of 256."""
+    if n <= 256:
+        p = 32
+        while p < n:
+            p *= 2
+        return p
+    return -(-n // 256) * 256
+
+
+class TSeg(ctypes.Structure):
+    """Mirror of ``qg_tseg``."""
+
+    _fields_ = [("a", ctypes.c_void_p), ("b", ctypes.c_void_p), ("blk_count", ctypes.c_void_p),
+                ("blk_base", ctypes.c_void_p), ("blk_kt", ctypes.c_void_p), ("row_sums", ctypes.c_void_p),
+                ("q_codes", ctypes.c_void_p), ("q_row_sums", ctypes.c_void_p), ("out_real", ctypes.c_void_p),
+                ("out_i32", ctypes.c_void_p), ("status", ctypes.c_void_p), ("m", ctypes.c_int64),
+                ("r128", ctypes.c_int64), ("cta_begin", ctypes.c_int64), ("k_tiles", ctypes.c_int32),
+                ("pad_", ctypes.c_int32)]
+
+
+class TiledArgs(ctypes.Structure):
+    """Mirror of ``qg_tiled_args``."""
+
+    _fields_ = [("segs", ctypes.c_void_p), ("nsegs", ctypes.c_int32), ("a_blocks", ctypes.c_int32),
+                ("total_ctas", ctypes.c_int64), ("b_npad", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
+                ("epi", ctypes.POINTER(N.Epilogue))]
+
+
+_SIGS_DONE = False
+
+
+def _lib():
+    global _SIGS_DONE
+    L = N.lib()
+    if not _SIGS_DONE:
+        L.qg_tiled_gemm.argtypes = [ctypes.POINTER(TiledArgs), ctypes.c_void_p]
+        L.qg_tiled_gemm.restype = ctypes.c_int
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.qg_block_prepare.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp, vp, vp, vp]
+        L.qg_block_prepare.restype = ctypes.c_int
+        L.qg_codes_to_tiles.argtypes = [vp, i64, i64, i64, i32, i64, vp, vp]
+        L.qg_codes_to_tiles.restype = ctypes.c_int
+        L.qg_tiles_to_codes.argtypes = [vp, i64, i64, i32, i64, vp, i64, vp]
+        L.qg_tiles_to_codes.restype = ctypes.c_int
+        _SIGS_DONE = True
+    return L
+
+
+# ------------------------------------------------------------------ adjacency
+class BlockedAdjacency:
+    """Non-zero 128x128 blocks of a column-wise 1-bit adjacency, expanded to bytes."""
+
+    def __init__(self, a, schedule):
+        # host view of the zero-tile schedule (one sync, at build time)
+        counts = schedule.blk_count.cpu().numpy().astype(np.int64)
+        lists = schedule.blk_list.cpu().numpy()
+        self.nrb = len(counts)
+        base = np.zeros(self.nrb, dtype=np.int64)
+        if self.nrb:
+            base[1:] = np.cumsum(counts)[:-1]
+        self.nblocks = int(counts.sum())
+        rb_of = np.repeat(np.arange(self.nrb), counts)
+        kt_of = np.concatenate([lists[r, :counts[r]] for r in range(self.nrb)]) if self.nblocks else \
+            np.zeros(0, np.int64)
+        dev = a.dwords.device
+        self.blk_count = schedule.blk_count
+        self.blk_base = torch.from_numpy(base.astype(np.int32)).to(dev)
+        self.blk_kt = torch.from_numpy(kt_of.astype(np.int32)).to(dev)
+        self.blk_rb = torch.from_numpy(rb_of.astype(np.int32)).to(dev)
+        self.packed = torch.empty((max(self.nblocks, 1), 128, 4), dtype=torch.int32, device=dev)
+        self.bytes = torch.empty((max(self.nblocks, 1), 16384), dtype=torch.uint8, device=dev)
+        self.degrees = torch.zeros(a.logical_rows, dtype=torch.int64, device=dev)
+        self.m = a.logical_rows
+        self.r128 = pad128(a.logical_rows)
+        self._src = a
+        if self.nblocks:
+            N.check(_lib().qg_block_prepare(N.ptr(a.dwords), a.logical_rows, a.padded_rows, a.padded_cols,
+                                            N.ptr(self.blk_rb), N.ptr(self.blk_kt), self.nblocks, N.ptr(self.packed),
+                                            N.ptr(self.bytes), N.ptr(self.degrees), N.stream()), "qg_block_prepare")
+
+
+def blocked(a) -> BlockedAdjacency:
+    """Cached BlockedAdjacency of a PackedBitMatrix (built on first use)."""
+    if getattr(a, "_blocked", None) is None:
+        from .bitgemm import _schedule
+        a._blocked = BlockedAdjacency(a, _schedule(a))
+    return a._blocked
+
+
+# ------------------------------------------------------------- code caches
+class TiledCodeStack(BitPlaneStack):
+    """A plane stack whose source of truth is a tiled u8 code cache.
+
+    ``side`` = "left" (M x K operand, pitch = pad128(rows)) or "right" (K x N
+    operand of the NEXT GEMM: rows are K, pitch = npad(cols)).  Plane words are
+    built lazily (untile -> bit_qnt) for API consumers and the exact paths.
+    """
+
+    def __init__(self, orientation, rows, cols, bits, tiles: torch.Tensor, side: str, pitch: int, pad_to=8):
+        pr, pc = padded_dims(rows, cols, orientation, pad_to)
+        self.bits = int(bits)
+        self._planes = None
+        self._meta = (orientation, int(rows), int(cols), int(pr), int(pc))
+        self.tiles, self.side, self.pitch = tiles, side, int(pitch)
+        self._dwords = None
+
+    def plain_codes(self) -> torch.Tensor:
+        rows, cols = self.logical_rows, self.logical_cols
+        out = torch.empty((rows, max(cols, 1)), dtype=torch.uint8, device=self.tiles.device)
+        if rows * cols:
+            N.check(_lib().qg_tiles_to_codes(N.ptr(self.tiles), rows, cols, int(self.side == "right"), self.pitch,
+                                             N.ptr(out), out.shape[1], N.stream()), "qg_tiles_to_codes")
+        return out
+
+    @property
+    def dwords(self) -> torch.Tensor:
+        if self._dwords is None:
+            o, rows, cols, pr, pc = self._meta
+            codes = self.plain_codes()
+            words = torch.empty((self.bits, pr * pc // 32), dtype=torch.int32, device=self.tiles.device)
+            if words.numel():
+                status = N.new_status()
+                N.call("qg_quantize_pack", N.ptr(codes), N.SRC_U8, rows, cols, codes.shape[1], 0.0, 1.0, self.bits,
+                       N.COLUMN_WISE_ID if o == COLUMN_WISE else N.ROW_WISE_ID, 8, N.ptr(words), None, None, None,
+                       N.ptr(status), N.stream())
+            self._dwords = words
+        return self._dwords
+
+    @dwords.setter
+    def dwords(self, value):
+        self._dwords = value
+
+
+def tiles_from_codes(codes: torch.Tensor, rows: int, cols: int, ld: int, side: str) -> tuple:
+    """Plain row-major codes [rows][ld] -> (tiled buffer, pitch)."""
+    if side == "left":
+        pitch = pad128(rows)
+        size = pad128(cols) * pitch
+    else:
+        pitch = npad_of(cols)
+        size = pad128(rows) * pitch
+    tiles = N.alloc(max(size, 16), torch.uint8, "static")
+    if rows * cols:
+        N.check(_lib().qg_codes_to_tiles(N.ptr(codes), rows, cols, ld, int(side == "right"), pitch, N.ptr(tiles),
+                                         N.stream()), "qg_codes_to_tiles")
+    return tiles, pitch
+
+
+def operand_tiles(stack: BitPlaneStack, side: str, row_sums=None):
+    """(tiles, pitch) of an activation stack for use as a left/right operand."""
+    if isinstance(stack, TiledCodeStack) and stack.side == side:
+        return stack.tiles, stack.pitch
+    from .bitpack import stack_code_operand
+    rows, cols = stack.logical_rows, stack.logical_cols
+    if stack.orientation == ROW_WISE:
+        codes, ld = stack_code_operand(stack, colmajor=False, row_sums=row_sums)
+    else:
+        codes, ld = stack_code_operand(stack, colmajor=False)
+    return tiles_from_codes(codes, rows, cols, ld, side)
+
+
+def weight_tiles(layer, prep):
+    """Right-tiled W codes (K = in_dim, N = out_dim), cached on the prepared layer."""
+    if getattr(prep, "w_tiles", None) is None:
+        dev = prep.w_stack.dwords.device
+        wq = torch.empty((layer.in_dim, layer.out_dim), dtype=torch.uint8, device=dev)
+        w64 = torch.as_tensor(layer.weight, dtype=torch.float64).to(dev).contiguous()
+        tmp = torch.empty_like(prep.w_stack.dwords)
+        status = N.new_status()
+        p = layer.weight_params
+        N.call("qg_quantize_pack", N.ptr(w64), N.SRC_F64, layer.in_dim, layer.out_dim, layer.out_dim,
+               float(p.alpha_min), float(p.scale), p.bits, N.ROW_WISE_ID, 8, N.ptr(tmp), N.ptr(wq), None, None,
+               N.ptr(status), N.stream())
+        pitch = npad_of(layer.out_dim)
+        tiles = torch.zeros(pad128(layer.in_dim) * pitch, dtype=torch.uint8, device=dev)
+        N.check(_lib().qg_codes_to_tiles(N.ptr(wq), layer.in_dim, layer.out_dim, layer.out_dim, 1, pitch, N.ptr(tiles),
+                                         N.stream()), "qg_codes_to_tiles")
+        prep.w_tiles, prep.w_pitch = tiles, pitch
+    return prep.w_tiles, prep.w_pitch
+
+
+# ------------------------------------------------------------ grouped launch
+class SegTable:
+    """Pinned host segment table + its device copy (captured as one H2D memcpy)."""
+
+    def __init__(self, segs):
+        n = len(segs)
+        self.host = torch.empty(n * ctypes.sizeof(TSeg), dtype=torch.uint8).pin_memory()
+        arr = (TSeg * n).from_address(self.host.data_ptr())
+        for i, s in enumerate(segs):
+            arr[i] = s
+        self.dev = N.alloc(self.host.numel(), torch.uint8, "empty")
+        self.dev.copy_(self.host, non_blocking=True)
+        self.n = n
+
+
+def choose_bn(npad: int, row_blocks_total: int) -> int:
+    bn = min(256, npad)
+    while bn > 32 and row_blocks_total * (npad // bn) < 148:
+        bn //= 2
+    return bn
+
+
+def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: int, out_npad: int, epi_struct,
+           keep: list):
+    """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m)."""
+    rbs = [-(-s.m // TILE) for s in segs]
+    bn = choose_bn(b_npad, sum(rbs))
+    n_tiles = b_npad // bn
+    begin = 0
+    for s, r in zip(segs, rbs):
+        s.cta_begin = begin
+        begin += r * n_tiles
+    table = SegTable(segs)
+    keep.append(table)
+    args = TiledArgs()
+    args.segs, args.nsegs, args.a_blocks, args.total_ctas = table.dev.data_ptr(), table.n, int(a_blocks), begin
+    args.b_npad, args.n, args.bn, args.n_tiles = b_npad, n, bn, n_tiles
+    args.mode, args.out_layout, args.out_npad = mode, out_layout, out_npad
+    if epi_struct is not None:
+        args.epi = ctypes.pointer(epi_struct)
+    if begin:
+        N.check(_lib().qg_tiled_gemm(args, N.stream()), "qg_tiled_gemm")
