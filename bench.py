@@ -204,16 +204,14 @@ def kernel_roofline(model, batches, reps=20):
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
         for _ in range(3):
-            for b in batches:
-                engine.model_forward_device(b, model)
+            engine.model_forward_group(batches, model)
         torch.cuda.synchronize()
         rec.clear()
         # park the GPU so the host enqueues every launch first: events then bracket
         # back-to-back kernels, not host gaps
         torch.cuda._sleep(int(3e8))
         for _ in range(reps):
-            for b in batches:
-                engine.model_forward_device(b, model)
+            engine.model_forward_group(batches, model)
         torch.cuda.synchronize()
     bitgemm.PROFILE_HOOK = None
     dur = sum(s.elapsed_time(e) for s, e, _ in rec) / reps        # ms per epoch in bit-GEMMs

@@ -32,7 +32,8 @@ STATUS_CLEAR = 0x7F7F7F7F7F7F7F7F
 EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes", "qg_unpack", "qg_repack",
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
            "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes",
-           "qg_test_requant")
+           "qg_test_requant", "qg_tiled_gemm", "qg_block_prepare", "qg_codes_to_tiles",
+           "qg_tiles_to_codes")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -154,6 +155,10 @@ def call(name: str, *args) -> None:
 # memset + ONE fill instead of a fill kernel per buffer.
 class TorchAlloc:
     def take(self, shape, dtype, kind):
+        if kind == "host":
+            # pageable staging: torch makes pageable H2D copies synchronous w.r.t. the
+            # host buffer, so eager callers may drop it right after the copy
+            return torch.empty(shape, dtype=dtype)
         dev = device()
         if kind == "status":
             return torch.full(shape, STATUS_CLEAR, dtype=torch.int64, device=dev)
@@ -188,7 +193,7 @@ class SlabAlloc:
 
     def __init__(self, plan: SlabPlan):
         self.seq = list(plan.seq)
-        sizes = {"static": 0, "volatile": 0, "status": 0}
+        sizes = {"static": 0, "volatile": 0, "status": 0, "host": 0}
         self.offsets = []
         for shape, dtype, kind in self.seq:
             nbytes = max(1, int(np.prod(shape))) * torch.empty((), dtype=dtype).element_size()
@@ -196,7 +201,11 @@ class SlabAlloc:
             self.offsets.append((k, sizes[k]))
             sizes[k] += -(-nbytes // self.ALIGN) * self.ALIGN
         dev = device()
-        self.slabs = {k: torch.zeros(max(v, self.ALIGN), dtype=torch.uint8, device=dev) for k, v in sizes.items()}
+        self.slabs = {k: torch.zeros(max(v, self.ALIGN), dtype=torch.uint8, device=dev) for k, v in sizes.items()
+                      if k != "host"}
+        # host staging (segment tables) is pinned, persistent, and allocated before capture:
+        # captured H2D memcpy nodes read it at every replay
+        self.slabs["host"] = torch.zeros(max(sizes["host"], self.ALIGN), dtype=torch.uint8).pin_memory()
         self.slabs["status"].view(torch.int64).fill_(STATUS_CLEAR)
         self.i = 0
 

@@ -80,6 +80,9 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
     for (int i = tid; i < bn; i += kTThreads) {
       const int64_t c = n0 + i;
       const bool ok = c < P.n;
+      // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
+      // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
+      // evaluates the reference's grouping without per-element branches
       sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
       sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
       if (E.bn_mean) {
@@ -142,77 +145,82 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   const int nslices = (ncols_cta + 7) >> 3;
   const bool packed = fused && E.out_kind == QG_OUT_PLANES;
   const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
+  // hoisted epilogue scalars (one param read each instead of per element)
+  const double k_acc = E.k_acc;
   const double rterm = (fused && E.use_row && rvalid) ? __dmul_rn(E.k_row, (double)G.row_sums[myrow]) : 0.0;
+  const double kconst = E.use_const ? E.k_const : 0.0;
+  const bool has_bn = E.bn_mean != nullptr, relu = E.act == QG_ACT_RELU, tanh_act = E.act == QG_ACT_TANH;
+  const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
+  const int out_layout = P.out_layout;
+  const int nvalid = (int)(P.n - n0);                        // columns of this CTA that exist
   unsigned long long rsum = 0;
   for (int sl = half; sl < nslices; sl += 2) {
-    const int64_t cb = n0 + sl * 8;
     uint64_t codes8 = 0;
 #pragma unroll 1
     for (int g = 0; g < 2; ++g) {
+      const int cl4 = sl * 8 + g * 4;                        // CTA-local column of element 0
       uint32_t v[4];
       if (nk > 0) {
-        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(sl * 8 + g * 4);
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cl4;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       } else {
         v[0] = v[1] = v[2] = v[3] = 0;
       }
-      const int64_t c4 = cb + g * 4;
       if (!fused) {
         if (rvalid) {
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
-            if (c4 + jj < P.n) G.out_i32[myrow * P.n + c4 + jj] = (int32_t)v[jj];
+            if (cl4 + jj < nvalid) G.out_i32[myrow * P.n + n0 + cl4 + jj] = (int32_t)v[jj];
         }
         continue;
       }
       double real[4];
-      const int cl4 = sl * 8 + g * 4;
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
         const int cl = cl4 + jj;
-        double x = __dmul_rn(E.k_acc, (double)(int32_t)v[jj]);
-        if (E.use_row) x = __dadd_rn(x, rterm);
-        if (E.use_col) x = __dadd_rn(x, sCol[cl]);
-        if (E.use_const) x = __dadd_rn(x, E.k_const);
-        if (E.bias) x = __dadd_rn(x, sCol[bn + cl]);
-        if (E.bn_mean)
+        // ((((k_acc*acc) + rows) + cols) + const) + bias, the reference's grouping
+        double x = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm),
+                                                 sCol[cl]), kconst), sCol[bn + cl]);
+        if (has_bn)
           x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl]), sCol[5 * bn + cl]),
                         sCol[6 * bn + cl]);
-        if (E.act == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
-        else if (E.act == QG_ACT_TANH) x = tanh_f32(x);
+        if (relu) x = (x < 0.0) ? 0.0 : x;
+        else if (tanh_act) x = tanh_f32(x);
         real[jj] = x;
       }
       if (!packed) {
         if (rvalid) {
+          double* dst = G.out_real + myrow * P.n + n0;
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
-            if (c4 + jj < P.n) G.out_real[myrow * P.n + c4 + jj] = real[jj];
+            if (cl4 + jj < nvalid) dst[cl4 + jj] = real[jj];
         }
         continue;
       }
 #pragma unroll
       for (int jj = 0; jj < 4; ++jj) {
-        const int64_t c = c4 + jj;
         uint32_t q = 0;
-        if (rvalid && c < P.n) {
-          if (!isfinite(real[jj]) && G.status) status_min(G.status, myrow * P.n + c);
-          q = quantize_code_fast(real[jj], E.q_amin, E.q_scale, E.q_inv_scale, maxv);
+        if (rvalid && cl4 + jj < nvalid) {
+          if (!isfinite(real[jj]) && G.status) status_min(G.status, myrow * P.n + n0 + cl4 + jj);
+          q = quantize_code_fast(real[jj], q_amin, q_scale, q_inv, maxv);
           rsum += q;
         }
         codes8 |= (uint64_t)q << (8 * (g * 4 + jj));
       }
     }
     if (packed && rvalid) {
-      if (P.out_layout == 1) {
+      const int64_t cb = n0 + sl * 8;
+      if (out_layout == 1) {
         // next LEFT operand: 8 consecutive K bytes of this row = one 8-byte store
         *reinterpret_cast<uint64_t*>(G.q_codes + left_tile_off(myrow, cb, G.r128)) = codes8;
       } else {
-        // next RIGHT operand (K = this row index): lanes of a warp write consecutive bytes
+        // next RIGHT operand (K = this row): consecutive lanes write consecutive bytes
+        uint8_t* base = G.q_codes + right_tile_off(myrow, cb, P.out_npad);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
-          if (cb + jj < P.n) G.q_codes[right_tile_off(myrow, cb + jj, P.out_npad)] = (uint8_t)(codes8 >> (8 * jj));
+          if (sl * 8 + jj < nvalid) base[jj * 16] = (uint8_t)(codes8 >> (8 * jj));   // n += 1 -> +16 B
       }
     }
   }
@@ -324,7 +332,9 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   if (a->epi) P.epi = *a->epi;
   const size_t stage = 16384 + (size_t)P.bn * 128;
   const size_t cols = 7 * (size_t)P.bn * 8;
-  const size_t budget = 227 * 1024 - 8192;
+  // the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's
+  // fp64 epilogue overlaps the other's bulk-copy/MMA main loop); TMEM 2 x 256 cols fits
+  const size_t budget = 113 * 1024 - 4096;
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;

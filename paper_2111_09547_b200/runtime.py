@@ -34,9 +34,10 @@ class EpochRunner:
         self.model = model
         self.batches = list(batches)
         self.jump, self.reuse = jump, reuse
-        # rescan=False: the zero-tile schedule is computed once and cached on the
-        # adjacency, as the reference caches scan_zero_tiles on the operand
-        # (bitgemm.py:222-233); rescan=True puts the scan inside every epoch (new data).
+        # The zero-tile schedule is computed once per batch and cached on the adjacency,
+        # as the reference caches scan_zero_tiles on the operand (bitgemm.py:222-233).
+        # rescan=True re-gathers and re-expands the adjacency blocks from the current
+        # words inside every epoch (new data each step, e2e path).
         self.rescan = rescan
         self.stream = stream or torch.cuda.Stream()
         self.graph = None
@@ -44,18 +45,19 @@ class EpochRunner:
         self._keep = []
 
     def _forward_all(self, verify: bool):
-        for b in self.batches:
-            if self.rescan:
-                b.adjacency._schedule = None  # the scan is part of the step (new data each step)
-                b.adjacency._blocked = None
+        if self.rescan:
+            from .tiled import blocked
+            for b in self.batches:            # new words each step: re-gather + re-expand the blocks
+                blocked(b.adjacency).refresh()
         return model_forward_group(self.batches, self.model, jump=self.jump, reuse=self.reuse, verify=verify)
 
     def capture(self):
         _prepared(self.model)
-        if not self.rescan:
-            from .tiled import blocked
-            for b in self.batches:
-                blocked(b.adjacency)          # schedule + expanded blocks cached, outside the epoch
+        from .tiled import blocked, weight_tiles
+        for b in self.batches:
+            blocked(b.adjacency)              # zero-tile schedule (host-known) + blocks, outside the epoch
+        for ly, prep in zip(self.model.layers, _prepared(self.model)):
+            weight_tiles(ly, prep)
         with torch.cuda.stream(self.stream):
             plan = N.SlabPlan()
             N.ALLOC = plan
@@ -86,7 +88,7 @@ class EpochRunner:
         conversion + 2 fused GEMMs per layer."""
         per_epoch = 2 * len(self.model.layers) + 2 * len(self.batches)   # grouped GEMMs + entry conversions
         if self.rescan:
-            per_epoch += 4 * len(self.batches)                              # scan, schedule, gather, expand
+            per_epoch += 2 * len(self.batches)                              # block gather + expand
         return per_epoch
 
 

@@ -109,6 +109,15 @@ class BlockedAdjacency:
         self.m = a.logical_rows
         self.r128 = pad128(a.logical_rows)
         self._src = a
+        # non-zero 8x128 tiles: the reference's unit of work (bitgemm.py:335-347)
+        self.nz8 = schedule.rt * schedule.ct - schedule.zeros
+        self.refresh()
+
+    def refresh(self):
+        """Re-gather + re-expand the blocks (and degrees) from the adjacency's current
+        words with the same schedule -- device only, capturable in a CUDA graph."""
+        a = self._src
+        self.degrees.zero_()
         if self.nblocks:
             N.check(_lib().qg_block_prepare(N.ptr(a.dwords), a.logical_rows, a.padded_rows, a.padded_cols,
                                             N.ptr(self.blk_rb), N.ptr(self.blk_kt), self.nblocks, N.ptr(self.packed),
@@ -202,7 +211,7 @@ def weight_tiles(layer, prep):
         wq = torch.empty((layer.in_dim, layer.out_dim), dtype=torch.uint8, device=dev)
         w64 = torch.as_tensor(layer.weight, dtype=torch.float64).to(dev).contiguous()
         tmp = torch.empty_like(prep.w_stack.dwords)
-        status = N.new_status()
+        status = torch.full((1,), N.STATUS_CLEAR, dtype=torch.int64, device=dev)   # one-time, not per forward
         p = layer.weight_params
         N.call("qg_quantize_pack", N.ptr(w64), N.SRC_F64, layer.in_dim, layer.out_dim, layer.out_dim,
                float(p.alpha_min), float(p.scale), p.bits, N.ROW_WISE_ID, 8, N.ptr(tmp), N.ptr(wq), None, None,
@@ -221,7 +230,7 @@ class SegTable:
 
     def __init__(self, segs):
         n = len(segs)
-        self.host = torch.empty(n * ctypes.sizeof(TSeg), dtype=torch.uint8).pin_memory()
+        self.host = N.alloc(n * ctypes.sizeof(TSeg), torch.uint8, "host")
         arr = (TSeg * n).from_address(self.host.data_ptr())
         for i, s in enumerate(segs):
             arr[i] = s
@@ -238,7 +247,7 @@ def choose_bn(npad: int, row_blocks_total: int) -> int:
 
 
 def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: int, out_npad: int, epi_struct,
-           keep: list):
+           keep: list, work: float = 0.0):
     """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m)."""
     rbs = [-(-s.m // TILE) for s in segs]
     bn = choose_bn(b_npad, sum(rbs))
@@ -255,5 +264,14 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     args.mode, args.out_layout, args.out_npad = mode, out_layout, out_npad
     if epi_struct is not None:
         args.epi = ctypes.pointer(epi_struct)
-    if begin:
+    if not begin:
+        return
+    from . import bitgemm
+    if bitgemm.PROFILE_HOOK is not None:
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
         N.check(_lib().qg_tiled_gemm(args, N.stream()), "qg_tiled_gemm")
+        e_ev.record()
+        bitgemm.PROFILE_HOOK.append((s_ev, e_ev, work))
+        return
+    N.check(_lib().qg_tiled_gemm(args, N.stream()), "qg_tiled_gemm")

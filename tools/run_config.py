@@ -44,3 +44,21 @@ nodes = sum(b.total_nodes for b in batches)
 print(f"{cfg.name}: batches={len(batches)} nodes={nodes} build={t1 - t0:.1f}s calib={t2 - t1:.1f}s "
       f"capture={t3 - t2:.1f}s  epoch={ms:.3f} ms  ({ms * nb / len(batches):.3f} ms full-epoch est)  "
       f"mem={torch.cuda.max_memory_allocated() / 2**30:.1f} GiB")
+
+# per-launch timing of the grouped GEMM stages (events around back-to-back launches)
+from paper_2111_09547_b200 import bitgemm, engine  # noqa: E402
+rec = []
+bitgemm.PROFILE_HOOK = rec
+with torch.cuda.stream(st):
+    engine.model_forward_group(batches, model)
+    torch.cuda.synchronize()
+    rec.clear()
+    torch.cuda._sleep(int(2e8))
+    engine.model_forward_group(batches, model)
+    torch.cuda.synchronize()
+bitgemm.PROFILE_HOOK = None
+peak = 4155.8
+for i, (s, e, w) in enumerate(rec):
+    t = s.elapsed_time(e)
+    print(f"  stage {i}: {t:.3f} ms  work {w / 1e12:.3f} T-int8-ops  -> {w / (t * 1e-3) / 1e12:.1f} TOPS "
+          f"({w / (t * 1e-3) / 1e12 / peak:.1%} of int8 peak)")
