@@ -80,6 +80,23 @@ __device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, do
   return k < maxv ? k : maxv;
 }
 
+// Branch-free candidate of quantize_code_fast for the epilogue's common case:
+// returns the code and ORs into `fb` whether the cheap floor may be wrong (the
+// quotient is within 2^-40 of an integer) -- the caller then recomputes with
+// quantize_code_fast.  a <= 0 / NaN -> 0 via fmax; large quotients clamp through
+// fmin before the 2^52 trick so its integer read stays exact.
+__device__ __forceinline__ uint32_t quantize_code_nb(double x, double amin, double inv_scale, double maxp1,
+                                                     uint32_t maxv, bool& fb) {
+  const double a = __dsub_rn(x, amin);
+  const double q0 = __dmul_rn(fmax(a, 0.0), inv_scale);
+  const double qc = fmin(q0, maxp1);
+  const double t = __dadd_rd(qc, 0x1p52);
+  const double frac = __dsub_rn(qc, __dsub_rn(t, 0x1p52));
+  const uint32_t k = (uint32_t)__double2loint(t);
+  fb |= (a > 0.0) & (q0 < maxp1) & !((frac > 0x1p-40) & (frac < 1.0 - 0x1p-40));
+  return k < maxv ? k : maxv;
+}
+
 // Reference formulation (tests): floor of the IEEE quotient, clamped.
 __device__ __forceinline__ uint32_t quantize_code_ref(double x, double amin, double scale, uint32_t maxv) {
   const double v = floor(__ddiv_rn(__dsub_rn(x, amin), scale));

@@ -780,7 +780,12 @@ __global__ void test_requant_kernel(const double* x, int64_t n, double amin, dou
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t maxv = (1u << bits) - 1u;
-  out[i] = quantize_code_fast(x[i], amin, scale, inv, maxv);
+  const uint32_t fast = quantize_code_fast(x[i], amin, scale, inv, maxv);
+  // the tiled epilogue's form: branch-free candidate, exact pass when flagged
+  bool fb = false;
+  uint32_t nb = quantize_code_nb(x[i], amin, inv, (double)maxv + 1.0, maxv, fb);
+  if (fb) nb = fast;
+  out[i] = nb == fast ? fast : 0xFFFFFFFFu;
   ref[i] = quantize_code_ref(x[i], amin, scale, maxv);
 }
 }  // namespace qg

@@ -34,6 +34,13 @@ struct TiledParams {
 
 constexpr int kTThreads = 256;
 
+// exact requant of one element with the non-finite report (rare path, kept out of line)
+static __device__ __noinline__ uint32_t requant_exact(double x, double amin, double scale, double inv, uint32_t maxv,
+                                                      int64_t* status, int64_t flat) {
+  if (!isfinite(x) && status) status_min(status, flat);
+  return quantize_code_fast(x, amin, scale, inv, maxv);
+}
+
 template <int TMEM_COLS>
 __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -153,79 +160,89 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
   const int out_layout = P.out_layout;
   const int nvalid = (int)(P.n - n0);                        // columns of this CTA that exist
-  unsigned long long rsum = 0;
+  const double maxp1 = (double)maxv + 1.0;
+  uint32_t rsum = 0;                                        // <= 256 cols x 255: fits u32
   for (int sl = half; sl < nslices; sl += 2) {
-    uint64_t codes8 = 0;
-#pragma unroll 1
-    for (int g = 0; g < 2; ++g) {
-      const int cl4 = sl * 8 + g * 4;                        // CTA-local column of element 0
-      uint32_t v[4];
-      if (nk > 0) {
-        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cl4;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      } else {
-        v[0] = v[1] = v[2] = v[3] = 0;
-      }
-      if (!fused) {
-        if (rvalid) {
+    const int cl8 = sl * 8;                                 // CTA-local column of element 0
+    uint32_t v[8];
+    if (nk > 0) {
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cl8;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                     "=r"(v[7])
+                   : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    } else {
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            if (cl4 + jj < nvalid) G.out_i32[myrow * P.n + n0 + cl4 + jj] = (int32_t)v[jj];
-        }
-        continue;
-      }
-      double real[4];
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int cl = cl4 + jj;
-        // ((((k_acc*acc) + rows) + cols) + const) + bias, the reference's grouping
-        double x = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm),
-                                                 sCol[cl]), kconst), sCol[bn + cl]);
-        if (has_bn)
-          x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl]), sCol[5 * bn + cl]),
-                        sCol[6 * bn + cl]);
-        if (relu) x = (x < 0.0) ? 0.0 : x;
-        else if (tanh_act) x = tanh_f32(x);
-        real[jj] = x;
-      }
-      if (!packed) {
-        if (rvalid) {
-          double* dst = G.out_real + myrow * P.n + n0;
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            if (cl4 + jj < nvalid) dst[cl4 + jj] = real[jj];
-        }
-        continue;
-      }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        uint32_t q = 0;
-        if (rvalid && cl4 + jj < nvalid) {
-          if (!isfinite(real[jj]) && G.status) status_min(G.status, myrow * P.n + n0 + cl4 + jj);
-          q = quantize_code_fast(real[jj], q_amin, q_scale, q_inv, maxv);
-          rsum += q;
-        }
-        codes8 |= (uint64_t)q << (8 * (g * 4 + jj));
-      }
+      for (int jj = 0; jj < 8; ++jj) v[jj] = 0;
     }
-    if (packed && rvalid) {
-      const int64_t cb = n0 + sl * 8;
+    if (!fused) {
+      if (rvalid) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cl8 + jj < nvalid) G.out_i32[myrow * P.n + n0 + cl8 + jj] = (int32_t)v[jj];
+      }
+      continue;
+    }
+    // 8 independent fp64 chains: ((((k_acc*acc) + rows) + cols) + const) + bias, the
+    // reference's grouping, then BN and the activation
+    double real[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int cl = cl8 + jj;
+      double x = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm),
+                                               sCol[cl]), kconst), sCol[bn + cl]);
+      if (has_bn)
+        x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl]), sCol[5 * bn + cl]),
+                      sCol[6 * bn + cl]);
+      if (relu) x = (x < 0.0) ? 0.0 : x;
+      else if (tanh_act) x = tanh_f32(x);
+      real[jj] = x;
+    }
+    if (!packed) {
+      if (rvalid) {
+        double* dst = G.out_real + myrow * P.n + n0;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cl8 + jj < nvalid) dst[cl8 + jj] = real[jj];
+      }
+      continue;
+    }
+    // requant: branch-free candidates; one (rare, divergent) exact pass for ragged
+    // edges, non-finite values or quotients within 2^-40 of an integer
+    bool slow = !(rvalid && cl8 + 8 <= nvalid);
+    uint32_t q[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      q[jj] = quantize_code_nb(real[jj], q_amin, q_inv, maxp1, maxv, slow);
+      slow |= !(fabs(real[jj]) <= 1.7976931348623157e308);
+    }
+    if (slow) {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        q[jj] = (rvalid && cl8 + jj < nvalid)
+                    ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, G.status, myrow * P.n + n0 + cl8 + jj)
+                    : 0u;
+    }
+    const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+    rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    if (rvalid) {
+      const int64_t cb = n0 + cl8;
       if (out_layout == 1) {
         // next LEFT operand: 8 consecutive K bytes of this row = one 8-byte store
-        *reinterpret_cast<uint64_t*>(G.q_codes + left_tile_off(myrow, cb, G.r128)) = codes8;
+        *reinterpret_cast<uint2*>(G.q_codes + left_tile_off(myrow, cb, G.r128)) = make_uint2(lo, hi);
       } else {
         // next RIGHT operand (K = this row): consecutive lanes write consecutive bytes
         uint8_t* base = G.q_codes + right_tile_off(myrow, cb, P.out_npad);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
-          if (sl * 8 + jj < nvalid) base[jj * 16] = (uint8_t)(codes8 >> (8 * jj));   // n += 1 -> +16 B
+          if (cl8 + jj < nvalid) base[jj * 16] = (uint8_t)q[jj];   // n += 1 -> +16 B
       }
     }
   }
   if (packed && G.q_row_sums) {
-    if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], rsum);
+    if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], (unsigned long long)rsum);
     __syncthreads();
     if (tid < 128 && rb * 128 + tid < G.m && sRowSum[tid])
       atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[tid]);
