@@ -93,7 +93,10 @@ __device__ __forceinline__ uint32_t quantize_code_nb(double x, double amin, doub
   const double t = __dadd_rd(qc, 0x1p52);
   const double frac = __dsub_rn(qc, __dsub_rn(t, 0x1p52));
   const uint32_t k = (uint32_t)__double2loint(t);
-  fb |= (a > 0.0) & (q0 < maxp1) & !((frac > 0x1p-40) & (frac < 1.0 - 0x1p-40));
+  // suspicious: 0 < q0 < maxp1 (a q0 that underflowed to 0 has a true quotient < 1)
+  // and frac within 2^-40 of an integer
+  const double h = 0.5 * maxp1;
+  fb |= (fabs(__dsub_rn(q0, h)) < h) & (fabs(__dsub_rn(frac, 0.5)) >= 0.5 - 0x1p-40);
   return k < maxv ? k : maxv;
 }
 

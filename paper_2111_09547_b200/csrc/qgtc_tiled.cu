@@ -41,6 +41,113 @@ static __device__ __noinline__ uint32_t requant_exact(double x, double amin, dou
   return quantize_code_fast(x, amin, scale, inv, maxv);
 }
 
+// Per-thread epilogue context: this lane owns one accumulator row (TMEM lane) and
+// walks 8-column slices first, first+2, ...
+struct EpiLane {
+  uint32_t tmem_row;
+  bool has_acc, rvalid;
+  int first, nslices, nvalid;
+  int64_t myrow, n0;
+  __device__ __forceinline__ void load8(int cl8, uint32_t (&v)[8]) const {
+    if (has_acc) {
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                     "=r"(v[7])
+                   : "r"(tmem_row + (uint32_t)cl8));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) v[jj] = 0;
+    }
+  }
+};
+
+// Fused epilogue over this lane's slices, specialised on activation and BN so the
+// 8 fp64 chains of a slice are straight-line code the scheduler can interleave.
+// Dequant: ((((k_acc*acc) + rows) + cols) + const) + bias -- the reference's
+// grouping (bitgemm.py:156-160); absent terms are +0.0 (exact, see sCol fill).
+// Returns this lane's requantized code sum (packed output) for the row sums.
+template <int ACT, bool HAS_BN, bool ROW_ONLY>
+__device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
+                                               const double* __restrict__ sCol, double rterm) {
+  const qg_epilogue& E = P.epi;
+  const int bn = P.bn;
+  const double* sC = sCol;
+  const double* sB = sCol + bn;
+  const double* sMean = sCol + 2 * bn;
+  const double* sDen = sCol + 3 * bn;
+  const double* sGam = sCol + 5 * bn;
+  const double* sBeta = sCol + 6 * bn;
+  const double k_acc = E.k_acc;
+  const double kconst = E.use_const ? E.k_const : 0.0;
+  const bool packed = E.out_kind == QG_OUT_PLANES;
+  const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
+  const double maxp1 = (double)maxv + 1.0;
+  const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
+  const int out_layout = P.out_layout;
+  uint32_t rsum = 0;                                        // <= 256 cols x 255: fits u32
+  for (int sl = L.first; sl < L.nslices; sl += 2) {
+    const int cl8 = sl * 8;
+    uint32_t v[8];
+    L.load8(cl8, v);
+    double real[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int cl = cl8 + jj;
+      double x = __dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm);
+      // ROW_ONLY (aggregation: exact 0/1 left operand, no bias): the reference adds
+      // nothing else; otherwise the absent terms are +0.0
+      if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), kconst), sB[cl]);
+      if (HAS_BN) x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sMean[cl]), sDen[cl]), sGam[cl]), sBeta[cl]);
+      if (ACT == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
+      if (ACT == QG_ACT_TANH) x = tanh_f32(x);
+      real[jj] = x;
+    }
+    if (!packed) {
+      if (L.rvalid) {
+        double* dst = G.out_real + L.myrow * P.n + L.n0;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cl8 + jj < L.nvalid) dst[cl8 + jj] = real[jj];
+      }
+      continue;
+    }
+    // requant: branch-free candidates; one (rare, divergent) exact pass for ragged
+    // edges, non-finite values or quotients within 2^-40 of an integer
+    bool slow = !(L.rvalid && cl8 + 8 <= L.nvalid);
+    uint32_t q[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      q[jj] = quantize_code_nb(real[jj], q_amin, q_inv, maxp1, maxv, slow);
+      slow |= !(fabs(real[jj]) <= 1.7976931348623157e308);
+    }
+    if (slow) {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        q[jj] = (L.rvalid && cl8 + jj < L.nvalid)
+                    ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, G.status, L.myrow * P.n + L.n0 + cl8 + jj)
+                    : 0u;
+    }
+    const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+    rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    if (L.rvalid) {
+      const int64_t cb = L.n0 + cl8;
+      if (out_layout == 1) {
+        // next LEFT operand: 8 consecutive K bytes of this row = one 8-byte store
+        *reinterpret_cast<uint2*>(G.q_codes + left_tile_off(L.myrow, cb, G.r128)) = make_uint2(lo, hi);
+      } else {
+        // next RIGHT operand (K = this row): consecutive lanes write consecutive bytes
+        uint8_t* base = G.q_codes + right_tile_off(L.myrow, cb, P.out_npad);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)q[jj];   // n += 1 -> +16 B
+      }
+    }
+  }
+  return rsum;
+}
+
 template <int TMEM_COLS>
 __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -151,94 +258,46 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   const int ncols_cta = rem_cols <= 0 ? 0 : (rem_cols < bn ? (int)rem_cols : bn);
   const int nslices = (ncols_cta + 7) >> 3;
   const bool packed = fused && E.out_kind == QG_OUT_PLANES;
-  const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
-  // hoisted epilogue scalars (one param read each instead of per element)
-  const double k_acc = E.k_acc;
-  const double rterm = (fused && E.use_row && rvalid) ? __dmul_rn(E.k_row, (double)G.row_sums[myrow]) : 0.0;
-  const double kconst = E.use_const ? E.k_const : 0.0;
-  const bool has_bn = E.bn_mean != nullptr, relu = E.act == QG_ACT_RELU, tanh_act = E.act == QG_ACT_TANH;
-  const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
-  const int out_layout = P.out_layout;
-  const int nvalid = (int)(P.n - n0);                        // columns of this CTA that exist
-  const double maxp1 = (double)maxv + 1.0;
-  uint32_t rsum = 0;                                        // <= 256 cols x 255: fits u32
-  for (int sl = half; sl < nslices; sl += 2) {
-    const int cl8 = sl * 8;                                 // CTA-local column of element 0
-    uint32_t v[8];
-    if (nk > 0) {
-      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)cl8;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                     "=r"(v[7])
-                   : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    } else {
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) v[jj] = 0;
-    }
-    if (!fused) {
+  EpiLane L;
+  L.tmem_row = tmem + ((uint32_t)(quad * 32) << 16);
+  L.has_acc = nk > 0;
+  L.first = half;
+  L.nslices = nslices;
+  L.nvalid = (int)(P.n - n0);
+  L.rvalid = myrow < G.m;
+  L.myrow = myrow;
+  L.n0 = n0;
+  uint32_t rsum = 0;
+  if (!fused) {
+    for (int sl = half; sl < nslices; sl += 2) {
+      uint32_t v[8];
+      L.load8(sl * 8, v);
       if (rvalid) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
-          if (cl8 + jj < nvalid) G.out_i32[myrow * P.n + n0 + cl8 + jj] = (int32_t)v[jj];
+          if (sl * 8 + jj < L.nvalid) G.out_i32[myrow * P.n + n0 + sl * 8 + jj] = (int32_t)v[jj];
       }
-      continue;
     }
-    // 8 independent fp64 chains: ((((k_acc*acc) + rows) + cols) + const) + bias, the
-    // reference's grouping, then BN and the activation
-    double real[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int cl = cl8 + jj;
-      double x = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm),
-                                               sCol[cl]), kconst), sCol[bn + cl]);
-      if (has_bn)
-        x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sCol[2 * bn + cl]), sCol[3 * bn + cl]), sCol[5 * bn + cl]),
-                      sCol[6 * bn + cl]);
-      if (relu) x = (x < 0.0) ? 0.0 : x;
-      else if (tanh_act) x = tanh_f32(x);
-      real[jj] = x;
-    }
-    if (!packed) {
-      if (rvalid) {
-        double* dst = G.out_real + myrow * P.n + n0;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (cl8 + jj < nvalid) dst[cl8 + jj] = real[jj];
-      }
-      continue;
-    }
-    // requant: branch-free candidates; one (rare, divergent) exact pass for ragged
-    // edges, non-finite values or quotients within 2^-40 of an integer
-    bool slow = !(rvalid && cl8 + 8 <= nvalid);
-    uint32_t q[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      q[jj] = quantize_code_nb(real[jj], q_amin, q_inv, maxp1, maxv, slow);
-      slow |= !(fabs(real[jj]) <= 1.7976931348623157e308);
-    }
-    if (slow) {
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-        q[jj] = (rvalid && cl8 + jj < nvalid)
-                    ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, G.status, myrow * P.n + n0 + cl8 + jj)
-                    : 0u;
-    }
-    const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-    const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
-    rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-    if (rvalid) {
-      const int64_t cb = n0 + cl8;
-      if (out_layout == 1) {
-        // next LEFT operand: 8 consecutive K bytes of this row = one 8-byte store
-        *reinterpret_cast<uint2*>(G.q_codes + left_tile_off(myrow, cb, G.r128)) = make_uint2(lo, hi);
-      } else {
-        // next RIGHT operand (K = this row): consecutive lanes write consecutive bytes
-        uint8_t* base = G.q_codes + right_tile_off(myrow, cb, P.out_npad);
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (cl8 + jj < nvalid) base[jj * 16] = (uint8_t)q[jj];   // n += 1 -> +16 B
-      }
+  } else {
+    // one uniform dispatch per CTA: the slice loop below is straight-line per variant
+    const double rterm = (E.use_row && rvalid) ? __dmul_rn(E.k_row, (double)G.row_sums[myrow]) : 0.0;
+    const bool row_only = !E.use_col && !E.use_const && !E.bias;
+    switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
+#define QG_EPI_CASE(i, A, B, R) \
+  case i: rsum = epi_slices<A, B, R>(P, G, L, sCol, rterm); break;
+      QG_EPI_CASE(0, QG_ACT_NONE, false, false)
+      QG_EPI_CASE(1, QG_ACT_NONE, false, true)
+      QG_EPI_CASE(2, QG_ACT_NONE, true, false)
+      QG_EPI_CASE(3, QG_ACT_NONE, true, true)
+      QG_EPI_CASE(4, QG_ACT_RELU, false, false)
+      QG_EPI_CASE(5, QG_ACT_RELU, false, true)
+      QG_EPI_CASE(6, QG_ACT_RELU, true, false)
+      QG_EPI_CASE(7, QG_ACT_RELU, true, true)
+      QG_EPI_CASE(8, QG_ACT_TANH, false, false)
+      QG_EPI_CASE(9, QG_ACT_TANH, false, true)
+      QG_EPI_CASE(10, QG_ACT_TANH, true, false)
+      default: rsum = epi_slices<QG_ACT_TANH, true, true>(P, G, L, sCol, rterm); break;
+#undef QG_EPI_CASE
     }
   }
   if (packed && G.q_row_sums) {
