@@ -80,24 +80,39 @@ __device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, do
   return k < maxv ? k : maxv;
 }
 
-// Branch-free candidate of quantize_code_fast for the epilogue's common case:
-// returns the code and ORs into `fb` whether the cheap floor may be wrong (the
-// quotient is within 2^-40 of an integer) -- the caller then recomputes with
-// quantize_code_fast.  a <= 0 / NaN -> 0 via fmax; large quotients clamp through
-// fmin before the 2^52 trick so its integer read stays exact.
-__device__ __forceinline__ uint32_t quantize_code_nb(double x, double amin, double inv_scale, double maxp1,
-                                                     uint32_t maxv, bool& fb) {
-  const double a = __dsub_rn(x, amin);
-  const double q0 = __dmul_rn(fmax(a, 0.0), inv_scale);
-  const double qc = fmin(q0, maxp1);
-  const double t = __dadd_rd(qc, 0x1p52);
-  const double frac = __dsub_rn(qc, __dsub_rn(t, 0x1p52));
-  const uint32_t k = (uint32_t)__double2loint(t);
-  // suspicious: 0 < q0 < maxp1 (a q0 that underflowed to 0 has a true quotient < 1)
-  // and frac within 2^-40 of an integer
-  const double h = 0.5 * maxp1;
-  fb |= (fabs(__dsub_rn(q0, h)) < h) & (fabs(__dsub_rn(frac, 0.5)) >= 0.5 - 0x1p-40);
-  return k < maxv ? k : maxv;
+// Epilogue requant with three fp64 ops.  q0 = RN(RN(x - amin) * RN(1/scale)) is
+// within 2^-44 of the true quotient for quotients < 2^8; r = RN(q0 + 2^12) then has
+// ulp 2^-40, so for r in [2^12, 2^13) its mantissa is (floor << 40) | frac, frac in
+// units of 2^-40.  Everything after that is integer work on r's two words:
+//   r < 2^12 (q0 < 0, also -0/negative NaN)  -> 0        r >= 2^13 / +inf / NaN -> maxv
+//   otherwise k = mantissa bits [40, 52), clamped to maxv.
+// When frac is within one unit of an integer boundary b with 1 <= b <= maxv, the
+// reference's RN(a / scale) could sit on either side: `fb` asks the caller for the
+// exact path (quantize_code_fast).  Outside that window the margin (>= 2^-40 -
+// 2^-41 - 2^-44) keeps floor(RN(a / scale)) == k.  Bit-identity: tests/test_gpu_kernels.
+__device__ __forceinline__ uint32_t quantize_code_r12(double x, double amin, double inv_scale, uint32_t maxv,
+                                                      bool& fb) {
+  const double r = __dadd_rn(__dmul_rn(__dsub_rn(x, amin), inv_scale), 0x1p12);
+  const int hi = __double2hiint(r);
+  const uint32_t lo = (uint32_t)__double2loint(r);
+  // negative r (sign bit) clamps to 0 first so the subtraction cannot wrap; then
+  // below 0x40B00000 (r < 2^12) -> d < 0 -> code 0; inside [2^12, 2^13): k in bits
+  // 8..19; 2^13 and up (incl. +inf/+NaN) -> >= 0x1000 -> maxv
+  const int d = max(hi, 0) - 0x40B00000;
+  const int kc = d >> 8;
+  const uint32_t code = (uint32_t)min(max(kc, 0), (int)maxv);
+  // near an integer (conservative superset: frac in {-1, 0, 1} units of 2^-40 checked
+  // on the low word, top frac byte in {0x00, 0xff}); boundary b = round(k + frac)
+  const bool near = (lo + 1u <= 2u) & (((uint32_t)(hi + 1) & 0xfeu) == 0u);
+  const uint32_t b = (uint32_t)((d + 0x80) >> 8);
+  fb |= near & (b - 1u < maxv);
+  return code;
+}
+
+// Exact int32 -> fp64 without the MIO conversion unit: 2^52 + (v + 2^31) built from
+// bits, minus the same constant (exact: an integer below 2^53).
+__device__ __forceinline__ double i32_to_f64(uint32_t v) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)(v ^ 0x80000000u)), 4503601774854144.0);
 }
 
 // Reference formulation (tests): floor of the IEEE quotient, clamped.

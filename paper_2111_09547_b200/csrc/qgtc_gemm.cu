@@ -783,8 +783,8 @@ __global__ void test_requant_kernel(const double* x, int64_t n, double amin, dou
   const uint32_t fast = quantize_code_fast(x[i], amin, scale, inv, maxv);
   // the tiled epilogue's form: branch-free candidate, exact pass when flagged
   bool fb = false;
-  uint32_t nb = quantize_code_nb(x[i], amin, inv, (double)maxv + 1.0, maxv, fb);
-  if (fb) nb = fast;
+  uint32_t nb = quantize_code_r12(x[i], amin, inv, maxv, fb);
+  if (fb || !isfinite(x[i])) nb = fast;
   out[i] = nb == fast ? fast : 0xFFFFFFFFu;
   ref[i] = quantize_code_ref(x[i], amin, scale, maxv);
 }

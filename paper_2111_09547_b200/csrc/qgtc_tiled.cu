@@ -82,9 +82,14 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   const double kconst = E.use_const ? E.k_const : 0.0;
   const bool packed = E.out_kind == QG_OUT_PLANES;
   const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
-  const double maxp1 = (double)maxv + 1.0;
   const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
   const int out_layout = P.out_layout;
+  // segment fields in registers (G lives in global memory; the code stores below
+  // could alias it, so the compiler would otherwise reload every slice)
+  uint8_t* const q_codes = G.q_codes;
+  double* const out_real = G.out_real;
+  int64_t* const status = G.status;
+  const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
   uint32_t rsum = 0;                                        // <= 256 cols x 255: fits u32
   for (int sl = L.first; sl < L.nslices; sl += 2) {
     const int cl8 = sl * 8;
@@ -94,18 +99,26 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
       const int cl = cl8 + jj;
-      double x = __dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm);
+      double x = __dadd_rn(__dmul_rn(k_acc, i32_to_f64(v[jj])), rterm);
       // ROW_ONLY (aggregation: exact 0/1 left operand, no bias): the reference adds
       // nothing else; otherwise the absent terms are +0.0
       if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), kconst), sB[cl]);
       if (HAS_BN) x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sMean[cl]), sDen[cl]), sGam[cl]), sBeta[cl]);
-      if (ACT == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
+      if (ACT == QG_ACT_RELU) {
+        if (packed) {
+          // sign mask: -0 also maps to +0, which requantizes to the same code
+          const int hi = __double2hiint(x), m = ~(hi >> 31);
+          x = __hiloint2double(hi & m, __double2loint(x) & m);
+        } else {
+          x = (x < 0.0) ? 0.0 : x;
+        }
+      }
       if (ACT == QG_ACT_TANH) x = tanh_f32(x);
       real[jj] = x;
     }
     if (!packed) {
       if (L.rvalid) {
-        double* dst = G.out_real + L.myrow * P.n + L.n0;
+        double* dst = out_real + L.myrow * pn + L.n0;
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
           if (cl8 + jj < L.nvalid) dst[cl8 + jj] = real[jj];
@@ -113,19 +126,19 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
       continue;
     }
     // requant: branch-free candidates; one (rare, divergent) exact pass for ragged
-    // edges, non-finite values or quotients within 2^-40 of an integer
+    // edges, non-finite values or quotients within 2^-40 of a code boundary
     bool slow = !(L.rvalid && cl8 + 8 <= L.nvalid);
     uint32_t q[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
-      q[jj] = quantize_code_nb(real[jj], q_amin, q_inv, maxp1, maxv, slow);
-      slow |= !(fabs(real[jj]) <= 1.7976931348623157e308);
+      q[jj] = quantize_code_r12(real[jj], q_amin, q_inv, maxv, slow);
+      slow |= ((uint32_t)__double2hiint(real[jj]) & 0x7ff00000u) == 0x7ff00000u;
     }
     if (slow) {
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj)
         q[jj] = (L.rvalid && cl8 + jj < L.nvalid)
-                    ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, G.status, L.myrow * P.n + L.n0 + cl8 + jj)
+                    ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, status, L.myrow * pn + L.n0 + cl8 + jj)
                     : 0u;
     }
     const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
@@ -135,10 +148,10 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
       const int64_t cb = L.n0 + cl8;
       if (out_layout == 1) {
         // next LEFT operand: 8 consecutive K bytes of this row = one 8-byte store
-        *reinterpret_cast<uint2*>(G.q_codes + left_tile_off(L.myrow, cb, G.r128)) = make_uint2(lo, hi);
+        *reinterpret_cast<uint2*>(q_codes + left_tile_off(L.myrow, cb, r128)) = make_uint2(lo, hi);
       } else {
         // next RIGHT operand (K = this row): consecutive lanes write consecutive bytes
-        uint8_t* base = G.q_codes + right_tile_off(L.myrow, cb, P.out_npad);
+        uint8_t* base = q_codes + right_tile_off(L.myrow, cb, out_npad);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
           if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)q[jj];   // n += 1 -> +16 B

@@ -68,6 +68,9 @@ def test_filtered_requant_is_bit_identical():
             scale = (amax - amin) / (1 << bits)
             x = rng.uniform(amin - 0.3 * (amax - amin), amax + 0.3 * (amax - amin), n)
             _requant_check(x, amin, amax, bits)
+            # far outside the grid (quotients beyond +-2^12 exercise the range clamps)
+            far = np.concatenate([amin - rng.uniform(1, 10000, 4096) * scale, amin + rng.uniform(1, 10000, 4096) * scale])
+            _requant_check(far, amin, amax, bits)
             # adversarial: exactly on and one ulp around every code boundary
             k = np.arange(-2, (1 << bits) + 3, dtype=np.float64)
             b = amin + k * scale
