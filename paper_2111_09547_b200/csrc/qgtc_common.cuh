@@ -82,37 +82,27 @@ __device__ __forceinline__ uint32_t quantize_code_fast(double x, double amin, do
 
 // Epilogue requant with three fp64 ops.  q0 = RN(RN(x - amin) * RN(1/scale)) is
 // within 2^-44 of the true quotient for quotients < 2^8; r = RN(q0 + 2^12) then has
-// ulp 2^-40, so for r in [2^12, 2^13) its mantissa is (floor << 40) | frac, frac in
-// units of 2^-40.  Everything after that is integer work on r's two words:
-//   r < 2^12 (q0 < 0, also -0/negative NaN)  -> 0        r >= 2^13 / +inf / NaN -> maxv
-//   otherwise k = mantissa bits [40, 52), clamped to maxv.
-// When frac is within one unit of an integer boundary b with 1 <= b <= maxv, the
-// reference's RN(a / scale) could sit on either side: `fb` asks the caller for the
-// exact path (quantize_code_fast).  Outside that window the margin (>= 2^-40 -
-// 2^-41 - 2^-44) keeps floor(RN(a / scale)) == k.  Bit-identity: tests/test_gpu_kernels.
-__device__ __forceinline__ uint32_t quantize_code_r12(double x, double amin, double inv_scale, uint32_t maxv,
-                                                      bool& fb) {
+// ulp 2^-40, so for r in [2^12, 2^13) its high word is 0x40B00000 + (floor << 8) +
+// (top 8 fraction bits) and its low word the rest of the fraction (units of 2^-40).
+// The fast decode is integer-only and valid when the caller's screen passes:
+//   hi < 0x40C00000 unsigned  -> r in [+0, 2^13): finite, not negative, q0 < 4096
+//   not (lo + 1 <= 2 && hi != 0x40B00000) -> the fraction is >= 2 units from an
+//       integer, so floor(RN(a / scale)) == floor(q0) (margin 2^-39 - 2^-41 - 2^-44);
+//       r == 2^12 exactly (q0 within 2^-41 of 0, e.g. ReLU zeros) is code 0 either way.
+// Anything the screen flags goes to quantize_code_fast (exact, with the IEEE
+// division fallback).  Bit-identity: tests/test_gpu_kernels.py.
+struct R12 {
+  uint32_t code;
+  bool flag;   // screen failed: recompute exactly
+};
+__device__ __forceinline__ R12 quantize_code_r12(double x, double amin, double inv_scale, uint32_t maxv) {
   const double r = __dadd_rn(__dmul_rn(__dsub_rn(x, amin), inv_scale), 0x1p12);
-  const int hi = __double2hiint(r);
-  const uint32_t lo = (uint32_t)__double2loint(r);
-  // negative r (sign bit) clamps to 0 first so the subtraction cannot wrap; then
-  // below 0x40B00000 (r < 2^12) -> d < 0 -> code 0; inside [2^12, 2^13): k in bits
-  // 8..19; 2^13 and up (incl. +inf/+NaN) -> >= 0x1000 -> maxv
-  const int d = max(hi, 0) - 0x40B00000;
-  const int kc = d >> 8;
-  const uint32_t code = (uint32_t)min(max(kc, 0), (int)maxv);
-  // near an integer (conservative superset: frac in {-1, 0, 1} units of 2^-40 checked
-  // on the low word, top frac byte in {0x00, 0xff}); boundary b = round(k + frac)
-  const bool near = (lo + 1u <= 2u) & (((uint32_t)(hi + 1) & 0xfeu) == 0u);
-  const uint32_t b = (uint32_t)((d + 0x80) >> 8);
-  fb |= near & (b - 1u < maxv);
-  return code;
-}
-
-// Exact int32 -> fp64 without the MIO conversion unit: 2^52 + (v + 2^31) built from
-// bits, minus the same constant (exact: an integer below 2^53).
-__device__ __forceinline__ double i32_to_f64(uint32_t v) {
-  return __dsub_rn(__hiloint2double(0x43300000, (int)(v ^ 0x80000000u)), 4503601774854144.0);
+  const uint32_t hi = (uint32_t)__double2hiint(r), lo = (uint32_t)__double2loint(r);
+  const int kc = (int)(hi >> 8) - 0x40B000;            // floor for r in [2^12, 2^13)
+  R12 o;
+  o.code = (uint32_t)min(max(kc, 0), (int)maxv);
+  o.flag = (hi >= 0x40C00000u) | ((lo + 1u <= 2u) & (hi != 0x40B00000u));
+  return o;
 }
 
 // Reference formulation (tests): floor of the IEEE quotient, clamped.
@@ -291,6 +281,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // 1-D bulk copy global -> shared (TMA engine), completion counted on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -782,9 +782,8 @@ __global__ void test_requant_kernel(const double* x, int64_t n, double amin, dou
   const uint32_t maxv = (1u << bits) - 1u;
   const uint32_t fast = quantize_code_fast(x[i], amin, scale, inv, maxv);
   // the tiled epilogue's form: branch-free candidate, exact pass when flagged
-  bool fb = false;
-  uint32_t nb = quantize_code_r12(x[i], amin, inv, maxv, fb);
-  if (fb || !isfinite(x[i])) nb = fast;
+  const R12 c = quantize_code_r12(x[i], amin, inv, maxv);
+  const uint32_t nb = (c.flag || !isfinite(x[i])) ? fast : c.code;
   out[i] = nb == fast ? fast : 0xFFFFFFFFu;
   ref[i] = quantize_code_ref(x[i], amin, scale, maxv);
 }

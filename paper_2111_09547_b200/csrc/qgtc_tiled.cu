@@ -76,8 +76,8 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   const double* sB = sCol + bn;
   const double* sMean = sCol + 2 * bn;
   const double* sDen = sCol + 3 * bn;
-  const double* sGam = sCol + 5 * bn;
-  const double* sBeta = sCol + 6 * bn;
+  const double* sGam = sCol + 4 * bn;
+  const double* sBeta = sCol + 5 * bn;
   const double k_acc = E.k_acc;
   const double kconst = E.use_const ? E.k_const : 0.0;
   const bool packed = E.out_kind == QG_OUT_PLANES;
@@ -99,7 +99,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
       const int cl = cl8 + jj;
-      double x = __dadd_rn(__dmul_rn(k_acc, i32_to_f64(v[jj])), rterm);
+      double x = __dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm);
       // ROW_ONLY (aggregation: exact 0/1 left operand, no bias): the reference adds
       // nothing else; otherwise the absent terms are +0.0
       if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), kconst), sB[cl]);
@@ -127,14 +127,17 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     }
     // requant: branch-free candidates; one (rare, divergent) exact pass for ragged
     // edges, non-finite values or quotients within 2^-40 of a code boundary
-    bool slow = !(L.rvalid && cl8 + 8 <= L.nvalid);
+    const bool full = L.rvalid && cl8 + 8 <= L.nvalid;
+    bool slow = !full;
     uint32_t q[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
-      q[jj] = quantize_code_r12(real[jj], q_amin, q_inv, maxv, slow);
-      slow |= ((uint32_t)__double2hiint(real[jj]) & 0x7ff00000u) == 0x7ff00000u;
+      const R12 c = quantize_code_r12(real[jj], q_amin, q_inv, maxv);
+      q[jj] = c.code;
+      slow |= c.flag;
     }
     if (slow) {
+      // non-finite x always lands here: r is then inf/NaN (hi >= 0x7ff00000) or negative
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj)
         q[jj] = (L.rvalid && cl8 + jj < L.nvalid)
@@ -152,9 +155,14 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
       } else {
         // next RIGHT operand (K = this row): consecutive lanes write consecutive bytes
         uint8_t* base = q_codes + right_tile_off(L.myrow, cb, out_npad);
+        if (full) {
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)q[jj];   // n += 1 -> +16 B
+          for (int jj = 0; jj < 8; ++jj) base[jj * 16] = (uint8_t)q[jj];   // n += 1 -> +16 B
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)q[jj];
+        }
       }
     }
   }
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u;
   uint8_t* stage0 = smem;
   const uint32_t stage_bytes = a_bytes + b_bytes;
-  double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);   // [7][bn] per-column constants
+  double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);   // [2 or 6][bn] per-column constants
 
   int nk, kbase = 0;
   if (P.a_blocks) { nk = G.blk_count[rb]; kbase = G.blk_base[rb]; }
@@ -215,8 +223,8 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
       if (E.bn_mean) {
         sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
         sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
-        sCol[5 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
-        sCol[6 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+        sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
+        sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
       }
     }
   }
@@ -420,7 +428,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   while ((1 << P.log2bn) < P.bn) ++P.log2bn;
   if (a->epi) P.epi = *a->epi;
   const size_t stage = 16384 + (size_t)P.bn * 128;
-  const size_t cols = 7 * (size_t)P.bn * 8;
+  const size_t cols = (a->epi && a->epi->bn_mean ? 6 : 2) * (size_t)P.bn * 8;
   // the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's
   // fp64 epilogue overlaps the other's bulk-copy/MMA main loop); TMEM 2 x 256 cols fits
   const size_t budget = 113 * 1024 - 4096;
