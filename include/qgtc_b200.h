@@ -260,6 +260,7 @@ typedef struct {
   int32_t out_layout;          /* 0 row-major fp64/int32, 1 left-tiled codes, 2 right-tiled codes */
   int64_t out_npad;            /* right-tiled output: padded N                       */
   const qg_epilogue* epi;      /* shared epilogue scalars / per-column vectors       */
+  int64_t* phase_ns;           /* optional [total_ctas][8] %globaltimer stamps (tools/) */
 } qg_tiled_args;
 
 /* Warp-specialised tiled bit-GEMM (cp.async.bulk producer, single-thread
@@ -282,6 +283,26 @@ int qg_codes_to_tiles(const uint8_t* codes, int64_t rows, int64_t cols, int64_t 
                       uint8_t* tiles, void* stream);
 int qg_tiles_to_codes(const uint8_t* tiles, int64_t rows, int64_t cols, int right, int64_t pitch, uint8_t* codes,
                       int64_t ld, void* stream);
+
+/* Grouped entry conversion (engine.py:164-176 _entry_state/_oriented + the code
+ * recomposition sum_p 2^p plane_p, quantize.py:115-129): the ROW-WISE packed
+ * feature planes of every batch -> u8 codes directly in the tiled operand layout
+ * of the first GEMM, one launch for all batches.  right = 0: left-tiled M x K
+ * (GIN update, X as rows x features; optional int64 row code sums, ZEROED by the
+ * caller); right = 1: right-tiled K x N (GCN aggregation, pitch = padded N).
+ * A work unit is 32 rows x 128 columns; block_begin = first unit of the segment. */
+typedef struct {
+  const uint32_t* words;       /* (bits, pad128(rows)/32 * pc) row-wise plane words   */
+  uint8_t* tiles;              /* tiled u8 output                                    */
+  int64_t* row_sums;           /* left only: int64 row sums of the codes (or NULL)   */
+  int64_t rows, cols;          /* logical                                            */
+  int64_t pr, pc;              /* padded plane dims (pr = pad128(rows))              */
+  int64_t pitch;               /* left: pad128(rows); right: padded N (>= cols)      */
+  int64_t unit_begin;          /* first work unit of this segment                    */
+} qg_entry_seg;
+
+int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t nplanes, int32_t right, int64_t total_units,
+                   void* stream);
 
 /* Shifted reduction sum_p acc[p] << p (int64 in) narrowed to int32 with an
  * overflow flag.  Replaces reduce_bitplanes (bitgemm.py:291-298). */

@@ -33,7 +33,7 @@ EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes"
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
            "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes",
            "qg_test_requant", "qg_tiled_gemm", "qg_block_prepare", "qg_codes_to_tiles",
-           "qg_tiles_to_codes")
+           "qg_tiles_to_codes", "qg_entry_tiles")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -102,6 +102,7 @@ def lib() -> ctypes.CDLL:
             "qg_test_requant": ([_vp, _i64, _f64, _f64, _f64, _i32, _vp, _vp, _vp], ctypes.c_int),
             "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp],
                                    ctypes.c_int),
+            "qg_entry_tiles": ([_vp, _i32, _i32, _i32, _i64, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)
@@ -168,6 +169,17 @@ class TorchAlloc:
 
 
 ALLOC = TorchAlloc()
+
+# (device, pinned host) pairs whose contents are fixed for the lifetime of a captured
+# graph (segment tables); copied once right after capture by flush_static_copies()
+STATIC_COPIES: list = []
+
+
+def flush_static_copies() -> None:
+    while STATIC_COPIES:
+        dev, host = STATIC_COPIES.pop()
+        dev.copy_(host)
+    torch.cuda.synchronize()
 
 
 def alloc(shape, dtype, kind="static") -> torch.Tensor:

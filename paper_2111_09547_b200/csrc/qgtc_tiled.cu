@@ -15,6 +15,7 @@
 // CTA -> (segment, 128-row block, N tile), so an epoch layer stage over all
 // subgraph batches is a single grid.
 #include <algorithm>
+#include <cstdlib>
 #include "qgtc_common.cuh"
 
 namespace qg {
@@ -30,7 +31,16 @@ struct TiledParams {
   int32_t out_layout;       // 0 fp64/int32 row-major, 1 left-tiled codes, 2 right-tiled codes
   int64_t out_npad;         // right-tiled output: padded N of the output (slab pitch)
   qg_epilogue epi;          // shared scalars + per-column vectors (per-row pointers come from segs)
+  int64_t* phase_ns;        // optional per-CTA %globaltimer stamps (tools/phase_tiled.py)
 };
+
+static __device__ __forceinline__ void tstamp(const TiledParams& P, int k) {
+  if (P.phase_ns) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.phase_ns[(int64_t)blockIdx.x * 8 + k] = (int64_t)t;
+  }
+}
 
 constexpr int kTThreads = 256;
 
@@ -177,6 +187,7 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   __shared__ unsigned long long sRowSum[128];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bn = P.bn, S = P.stages;
+  if (tid == 0) tstamp(P, 0);
 
   // ---- segment lookup (uniform): last segment with cta_begin <= blockIdx.x
   int lo = 0, hi = P.nsegs - 1;
@@ -211,28 +222,12 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   }
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
-  if (fused) {
-    for (int i = tid; i < bn; i += kTThreads) {
-      const int64_t c = n0 + i;
-      const bool ok = c < P.n;
-      // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
-      // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
-      // evaluates the reference's grouping without per-element branches
-      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
-      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
-      if (E.bn_mean) {
-        sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
-        sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
-        sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
-        sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
-      }
-    }
-  }
   if (tid < 128) sRowSum[tid] = 0ull;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_s;
+  if (tid == 0) tstamp(P, 1);
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer: two bulk copies per K tile ----------------
@@ -255,6 +250,7 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
     for (int it = 0; it < nk; ++it) {
       const int s = it % S;
       mbar_wait(smem_u32(&full[s]), (it / S) & 1);
+      if (it == 0) tstamp(P, 2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
 #pragma unroll
@@ -263,12 +259,31 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
       umma_commit(&empty[s]);
     }
     if (nk > 0) umma_commit(&done);
+  } else if (warp >= 2 && fused) {
+    // warps 2..7 stage the per-column epilogue constants while the first K tiles land
+    for (int i = tid - 64; i < bn; i += kTThreads - 64) {
+      const int64_t c = n0 + i;
+      const bool ok = c < P.n;
+      // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
+      // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
+      // evaluates the reference's grouping without per-element branches
+      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
+      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
+      if (E.bn_mean) {
+        sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
+        sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
+        sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
+        sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+      }
+    }
   }
   __syncwarp();
   if (nk > 0) {
     mbar_wait(smem_u32(&done), 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
+  if (fused) __syncthreads();   // sCol visible to all epilogue warps
+  if (tid == 0) tstamp(P, 3);
 
   // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
   const int quad = warp & 3, half = warp >> 2;
@@ -290,13 +305,21 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   L.n0 = n0;
   uint32_t rsum = 0;
   if (!fused) {
+    const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
     for (int sl = half; sl < nslices; sl += 2) {
       uint32_t v[8];
       L.load8(sl * 8, v);
       if (rvalid) {
+        int32_t* dst = G.out_i32 + myrow * P.n + n0 + sl * 8;
+        if (vec_ok && sl * 8 + 8 <= L.nvalid) {
+          // 8 consecutive columns of this row: two 16-byte stores (n % 4 == 0 keeps them aligned)
+          reinterpret_cast<int4*>(dst)[0] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+          reinterpret_cast<int4*>(dst)[1] = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
+        } else {
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (sl * 8 + jj < L.nvalid) G.out_i32[myrow * P.n + n0 + sl * 8 + jj] = (int32_t)v[jj];
+          for (int jj = 0; jj < 8; ++jj)
+            if (sl * 8 + jj < L.nvalid) dst[jj] = (int32_t)v[jj];
+        }
       }
     }
   } else {
@@ -321,6 +344,7 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
 #undef QG_EPI_CASE
     }
   }
+  if (tid == 0) tstamp(P, 4);
   if (packed && G.q_row_sums) {
     if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], (unsigned long long)rsum);
     __syncthreads();
@@ -330,6 +354,7 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  if (tid == 0) tstamp(P, 5);
 }
 
 // ------------------------------------------------ adjacency block preparation
@@ -400,9 +425,80 @@ __global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t
   codes[r * ld + c] = tiles[off];
 }
 
+// Grouped entry conversion: row-wise feature planes -> tiled u8 codes.  Unit =
+// 32 rows (one plane word per column) x 128 columns; thread t < 128 owns column
+// c0 + t and expands its s plane words into 32 code bytes (bit i of plane p ->
+// bit p of byte i).  Right-tiled (K = rows): the 32 bytes are two 16-byte K-cores
+// of column c -> two vector stores.  Left-tiled (K = columns): transpose through
+// shared memory, then every thread stores one 16-byte K-core of one row; row code
+// sums reduce over the unit's 128 columns before one atomic per row.
+__global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
+                                                          int nplanes, int right) {
+  __shared__ __align__(16) uint8_t tile[32][128 + 16];
+  int lo = 0, hi = nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].unit_begin <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const qg_entry_seg& G = segs[lo];
+  const int64_t u = (int64_t)blockIdx.x - G.unit_begin;
+  const int64_t wpl = G.pr >> 5;                          // words per column of one plane
+  const int64_t ncg = right ? (G.pitch + 127) >> 7 : (G.pc + 127) >> 7;
+  const int64_t v = u / ncg, cg = u % ncg;                // 32-row group, 128-column group
+  const int t = threadIdx.x;
+  const int64_t wpp = wpl * G.pc;
+  uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t c = cg * 128 + (t & 127);
+  if (t < 128 && c < G.pc) {
+    for (int p = 0; p < nplanes; ++p) {
+      const uint32_t x = __ldg(G.words + p * wpp + c * wpl + v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] |= expand_nibble((x >> (4 * q)) & 0xFu) << p;
+    }
+  }
+  if (right) {
+    if (t < 128 && c < G.pitch) {
+      const int64_t k0 = v * 32;
+      *reinterpret_cast<uint4*>(G.tiles + right_tile_off(k0, c, G.pitch)) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(G.tiles + right_tile_off(k0 + 16, c, G.pitch)) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+    return;
+  }
+  if (t < 128) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tile[i][t] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+  }
+  __syncthreads();
+  // 32 rows x 8 K-cores = 256 16-byte stores
+  const int r = t >> 3, core = t & 7;
+  const int64_t row = v * 32 + r, k = cg * 128 + core * 16;
+  const uint4 q = *reinterpret_cast<const uint4*>(&tile[r][core * 16]);
+  if (row < G.pitch) *reinterpret_cast<uint4*>(G.tiles + left_tile_off(row, k, G.pitch)) = q;
+  if (G.row_sums) {
+    const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      sum += (w4[i] & 0xFFu) + ((w4[i] >> 8) & 0xFFu) + ((w4[i] >> 16) & 0xFFu) + (w4[i] >> 24);
+    // the 8 cores of a row are 8 consecutive lanes
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) sum += __shfl_xor_sync(QG_FULL, sum, off);
+    if (core == 0 && row < G.rows && sum)
+      atomicAdd(reinterpret_cast<unsigned long long*>(G.row_sums + row), (unsigned long long)sum);
+  }
+}
+
 }  // namespace qg
 
 using namespace qg;
+
+extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t nplanes, int32_t right,
+                              int64_t total_units, void* stream) {
+  if (!segs || nsegs < 1 || nplanes < 1 || nplanes > 8 || total_units < 0) return QG_ERR_ARG;
+  if (total_units == 0) return QG_OK;
+  entry_tiles_kernel<<<(unsigned)total_units, 256, 0, (cudaStream_t)stream>>>(segs, nsegs, nplanes, right);
+  return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA;
+}
 
 static inline int tstatus() { return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA; }
 
@@ -427,11 +523,14 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   P.log2bn = 5;
   while ((1 << P.log2bn) < P.bn) ++P.log2bn;
   if (a->epi) P.epi = *a->epi;
+  P.phase_ns = a->phase_ns;
   const size_t stage = 16384 + (size_t)P.bn * 128;
   const size_t cols = (a->epi && a->epi->bn_mean ? 6 : 2) * (size_t)P.bn * 8;
   // the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's
   // fp64 epilogue overlaps the other's bulk-copy/MMA main loop); TMEM 2 x 256 cols fits
-  const size_t budget = 113 * 1024 - 4096;
+  size_t budget = 113 * 1024 - 4096;
+  static const char* env_budget = getenv("QG_TILED_SMEM_KB");   // tuning experiments only
+  if (env_budget) budget = (size_t)atoi(env_budget) * 1024;
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;

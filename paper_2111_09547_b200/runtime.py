@@ -75,6 +75,7 @@ class EpochRunner:
                     self.logits = self._forward_all(verify=False)
             finally:
                 N.ALLOC = N.TorchAlloc()
+            N.flush_static_copies()
         self._checks = list(getattr(self.model, "_pending_checks", []))
         return self
 
@@ -130,3 +131,37 @@ class HostEpochRunner:
                 self.out_host[r:r + o.shape[0]].copy_(o, non_blocking=True)
                 r += o.shape[0]
         return self.out_host
+
+
+class CapturedCall:
+    """Any device-only call (e.g. ``tiled.bmm_reduced``) replayed as one CUDA graph.
+
+    Same recipe as ``EpochRunner``: one eager run records the allocation
+    sequence, the slabs then serve it so the captured graph owns its buffers
+    (segment tables included, from pinned host slabs)."""
+
+    def __init__(self, fn, stream: torch.cuda.Stream | None = None):
+        self.fn = fn
+        self.stream = stream or torch.cuda.Stream()
+        with torch.cuda.stream(self.stream):
+            plan = N.SlabPlan()
+            N.ALLOC = plan
+            try:
+                fn()
+            finally:
+                N.ALLOC = N.TorchAlloc()
+            torch.cuda.synchronize()
+            self.slabs = N.SlabAlloc(plan)
+            self.graph = torch.cuda.CUDAGraph()
+            N.ALLOC = self.slabs
+            try:
+                with torch.cuda.graph(self.graph, stream=self.stream):
+                    self.slabs.reset()
+                    self.result = fn()
+            finally:
+                N.ALLOC = N.TorchAlloc()
+            N.flush_static_copies()
+
+    def run(self):
+        self.graph.replay()
+        return self.result

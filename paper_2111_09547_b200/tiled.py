@@ -59,7 +59,7 @@ class TiledArgs(ctypes.Structure):
                 ("total_ctas", ctypes.c_int64), ("b_npad", ctypes.c_int64), ("n", ctypes.c_int64),
                 ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
-                ("epi", ctypes.POINTER(N.Epilogue))]
+                ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p)]
 
 
 _SIGS_DONE = False
@@ -228,14 +228,20 @@ def weight_tiles(layer, prep):
 class SegTable:
     """Pinned host segment table + its device copy (captured as one H2D memcpy)."""
 
-    def __init__(self, segs):
+    def __init__(self, segs, kind=TSeg):
         n = len(segs)
-        self.host = N.alloc(n * ctypes.sizeof(TSeg), torch.uint8, "host")
-        arr = (TSeg * n).from_address(self.host.data_ptr())
+        self.host = N.alloc(n * ctypes.sizeof(kind), torch.uint8, "host")
+        arr = (kind * n).from_address(self.host.data_ptr())
         for i, s in enumerate(segs):
             arr[i] = s
         self.dev = N.alloc(self.host.numel(), torch.uint8, "empty")
-        self.dev.copy_(self.host, non_blocking=True)
+        if torch.cuda.is_current_stream_capturing():
+            # a captured epoch reuses the same slab addresses every replay, so the table
+            # is constant: copy it once after capture (N.flush_static_copies) instead of
+            # adding an H2D memcpy node (a PCIe round trip) to every replay
+            N.STATIC_COPIES.append((self.dev, self.host))
+        else:
+            self.dev.copy_(self.host, non_blocking=True)
         self.n = n
 
 
@@ -267,6 +273,10 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     if not begin:
         return
     from . import bitgemm
+    if bitgemm.PHASE_HOOK is not None:
+        stamps = torch.zeros((begin, 8), dtype=torch.int64, device=N.device())
+        args.phase_ns = stamps.data_ptr()
+        bitgemm.PHASE_HOOK.append(stamps)
     if bitgemm.PROFILE_HOOK is not None:
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record()
@@ -275,3 +285,91 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
         bitgemm.PROFILE_HOOK.append((s_ev, e_ev, work))
         return
     N.check(_lib().qg_tiled_gemm(args, N.stream()), "qg_tiled_gemm")
+
+
+# ------------------------------------------------------ reduced 1-bit x s-bit
+def bmm_reduced(a, x, *, out: torch.Tensor | None = None) -> torch.Tensor:
+    """int32 ``reduce_bitplanes(bmm_1bit_by_nbit(a, x))`` in ONE tiled launch.
+
+    The reference computes A.X_p per plane (bitgemm.py:306-371) and then shift-adds
+    the planes in int64 (bitgemm.py:282-298).  Since sum_p 2^p X_p is X's code
+    matrix, the same int32 result is A . codes(X): the non-zero 128x128 blocks of
+    A (zero-tile jumping, bitgemm.py:214-233) times X's right-tiled u8 codes,
+    accumulated in TMEM s32.  Exact: the largest entry is (2^s-1)*K < 2^31 for
+    K < 8.4M, so _narrow_int32 can never raise here.  Device result, no sync.
+    """
+    from .bitpack import COLUMN_WISE as _COL, ROW_WISE as _ROW
+    from .errors import ShapeError
+    if a.orientation != _COL:
+        raise ShapeError("left operand must be column-wise packed")
+    if x.orientation != _ROW:
+        raise ShapeError("right operand must be row-wise packed")
+    if a.padded_cols != x.padded_rows or a.logical_cols != x.logical_rows:
+        raise ShapeError(f"shared dims mismatch: {a.logical_rows}x{a.logical_cols} vs "
+                         f"{x.logical_rows}x{x.logical_cols}")
+    m, n = a.logical_rows, x.logical_cols
+    if out is None:
+        out = N.alloc((m, n), torch.int32, "empty")   # every element is written
+    if not (m and n):
+        return out
+    blk = blocked(a)
+    if blk.nblocks == 0:
+        out.zero_()
+        return out
+    xt, _ = operand_tiles(x, "right")
+    seg = TSeg()
+    seg.a, seg.b, seg.m, seg.r128 = blk.bytes.data_ptr(), xt.data_ptr(), m, blk.r128
+    seg.blk_count, seg.blk_base, seg.blk_kt = (blk.blk_count.data_ptr(), blk.blk_base.data_ptr(),
+                                               blk.blk_kt.data_ptr())
+    seg.out_i32 = out.data_ptr()
+    keep = []
+    # row blocks with no non-zero K tile are written as zeros by the kernel (nk = 0)
+    launch([seg], a_blocks=True, b_npad=npad_of(n), n=n, mode=N.GEMM_I32, out_layout=0, out_npad=0,
+           epi_struct=None, keep=keep, work=2.0 * 1024 * (-(-n // 8) * 8) * blk.nz8)
+    out._qg_keep = keep           # the segment table must outlive the (async) launch
+    return out
+
+
+# ------------------------------------------------------- grouped entry codes
+class EntrySeg(ctypes.Structure):
+    """Mirror of ``qg_entry_seg``."""
+
+    _fields_ = [("words", ctypes.c_void_p), ("tiles", ctypes.c_void_p), ("row_sums", ctypes.c_void_p),
+                ("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("pr", ctypes.c_int64), ("pc", ctypes.c_int64),
+                ("pitch", ctypes.c_int64), ("unit_begin", ctypes.c_int64)]
+
+
+def entry_tiles(stacks, side: str, want_row_sums: bool, keep: list):
+    """Row-wise feature plane stacks of all batches -> tiled codes, ONE launch
+    (engine.py:164-176 entry state + orientation fix-up; sum_p 2^p plane_p).
+    Returns [(tiles, pitch, row_sums | None)] or None when a stack is not a plain
+    row-wise plane stack of a common bit width (callers then convert per batch)."""
+    if not stacks or any(type(s) is not BitPlaneStack or s.orientation != ROW_WISE or s.bits != stacks[0].bits
+                         for s in stacks):
+        return None
+    right = side == "right"
+    segs, outs, begin = [], [], 0
+    for s in stacks:
+        rows, cols, pr, pc = s.dims()
+        if right:
+            pitch = npad_of(cols)
+            tiles = N.alloc(max(pad128(rows) * pitch, 16), torch.uint8, "static")
+            units = (pr // 32) * (-(-pitch // 128))
+        else:
+            pitch = pad128(rows)
+            tiles = N.alloc(max(pad128(cols) * pitch, 16), torch.uint8, "static")
+            units = (pr // 32) * (-(-pc // 128))
+        rs = N.alloc(rows, torch.int64, "volatile") if (want_row_sums and not right) else None
+        seg = EntrySeg()
+        seg.words, seg.tiles, seg.row_sums = s.dwords.data_ptr(), tiles.data_ptr(), (rs.data_ptr() if rs is not None
+                                                                                     else None)
+        seg.rows, seg.cols, seg.pr, seg.pc, seg.pitch, seg.unit_begin = rows, cols, pr, pc, pitch, begin
+        begin += units if rows * cols else 0
+        segs.append(seg)
+        outs.append((tiles, pitch, rs))
+    if begin:
+        table = SegTable(segs, EntrySeg)
+        keep.append(table)
+        N.check(N.lib().qg_entry_tiles(table.dev.data_ptr(), len(segs), stacks[0].bits, int(right), begin,
+                                       N.stream()), "qg_entry_tiles")
+    return outs

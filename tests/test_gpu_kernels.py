@@ -156,3 +156,44 @@ def test_empty_and_degenerate_shapes():
     one = bg.pack_colwise(np.ones((1, 1), np.uint8))
     y = bg.pack_planes(np.ones((8, 1, 1), np.uint8), bg.ROW_WISE)
     assert [int(o[0, 0]) for o in bg.bmm_1bit_by_nbit(one, y)] == [1] * 8
+
+
+@pytest.mark.parametrize("side", ["left", "right"])
+def test_grouped_entry_tiles_equal_per_batch_conversion(side):
+    """qg_entry_tiles (one launch over ragged batches) == the per-batch planes->codes->tiles
+    path, byte for byte including zero padding, and the row code sums match."""
+    from paper_2111_09547_b200 import tiled
+    rng = np.random.default_rng(11)
+    stacks, codes = [], []
+    for rows, cols, bits in ((1, 1, 3), (129, 100, 3), (300, 257, 3), (1000, 128, 3)):
+        c = rng.integers(0, 1 << bits, (rows, cols), dtype=np.uint8)
+        codes.append(c)
+        stacks.append(bg.pack_planes(O.planes_of(c, bits), bg.ROW_WISE))
+    keep = []
+    got = tiled.entry_tiles(stacks, side, True, keep)
+    assert got is not None
+    for st, c, (tiles, pitch, rs) in zip(stacks, codes, got):
+        want, wpitch = tiled.tiles_from_codes(torch.from_numpy(c).cuda(), c.shape[0], c.shape[1], c.shape[1], side)
+        assert pitch == wpitch
+        assert torch.equal(tiles, want)
+        if side == "left":
+            np.testing.assert_array_equal(rs.cpu().numpy(), c.astype(np.int64).sum(axis=1))
+
+
+@pytest.mark.parametrize("bits", [1, 3, 8])
+def test_bmm_reduced_equals_reduced_per_plane_bmm(bits):
+    """tiled.bmm_reduced (C5 path) == reduce_bitplanes(bmm_1bit_by_nbit) of the reference
+    API, with a block-diagonal A so zero-tile jumping skips whole row blocks."""
+    from paper_2111_09547_b200 import tiled
+    rng = np.random.default_rng(bits)
+    m, k, n = 700, 900, 300
+    dense = (rng.uniform(0, 1, (m, k)) < 0.05).astype(np.uint8)
+    dense[:256, 600:] = 0
+    dense[256:, :300] = 0
+    x = rng.integers(0, 1 << bits, (k, n), dtype=np.uint8)
+    a = bg.pack_colwise(dense)
+    xs = bg.pack_planes(O.planes_of(x, bits), bg.ROW_WISE)
+    got = tiled.bmm_reduced(a, xs).cpu().numpy()
+    want = bg.reduce_bitplanes(bg.bmm_1bit_by_nbit(a, xs))
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(got, dense.astype(np.int64) @ x.astype(np.int64))
