@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "QGNN inference ms/epoch per bitwidth; bit-GEMM effective TOPS vs TC peak"
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
 INT8_PEAK_FILE = os.path.join(ROOT, "profiles", "int8_peak.json")
 
@@ -48,6 +49,8 @@ def parse():
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=12.0)
+    p.add_argument("--no-c5", action="store_true")
+    p.add_argument("--c5-n", type=int, default=16384)
     return p.parse_args()
 
 
@@ -141,12 +144,31 @@ def int8_peak_tops():
 
 
 # --------------------------------------------------------------- workload
-def build_workload(cfg_name, bits, seed):
+def build_workload(cfg_name, bits, seed, batch_ids=None):
+    """Batches (all, or ``batch_ids``) + a model calibrated on global batch 0 (cli.py:209)."""
     from paper_2111_09547_b200 import synth
     cfg = synth.with_bits(synth.CONFIGS[cfg_name], bits)
-    batches, feats, _ = synth.planted_batches(cfg, seed=seed)
-    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=seed)
+    if batch_ids is None:
+        batches, feats, _ = synth.planted_batches(cfg, seed=seed)
+        model = synth.calibrated_model(cfg, batches[0], feats[0], seed=seed)
+        return cfg, batches, feats, model
+    b0, f0, _ = synth.planted_batches(cfg, seed=seed, batch_ids=[0])
+    model = synth.calibrated_model(cfg, b0[0], f0[0], seed=seed)
+    batches, feats, _ = synth.planted_batches(cfg, seed=seed, batch_ids=batch_ids)
     return cfg, batches, feats, model
+
+
+class ShardedStep:
+    """One sharded epoch step: this rank's epoch graph over its LPT share of the batches,
+    then ONE all_gather_into_tensor of the logits (NCCL) -- paper_2111_09547_b200.shard."""
+
+    def __init__(self, runner, gather):
+        self.runner, self.gather, self.stream = runner, gather, runner.stream
+
+    def run(self):
+        outs = self.runner.run()
+        self.gather.gather(outs)
+        return outs
 
 
 def time_device_epochs(runner, steps, warmup, world):
@@ -196,28 +218,32 @@ def time_e2e(host_runner, steps, warmup, world):
 
 
 def kernel_roofline(model, batches, reps=20):
-    """Average duration of the bit-GEMM launches of one epoch (events on the launch stream)."""
+    """Bit-GEMM launch durations inside the epoch graph.  CUDA events cannot sit between
+    the kernels of one graph, so an identical epoch graph is captured with per-CTA
+    %globaltimer stamps (first CTA entry -> last CTA exit = the launch's span); it is
+    replayed like a timed step (L2 flushed before each replay) and CUDA events around
+    each replay give the step time the spans are a share of."""
     import torch
-    from paper_2111_09547_b200 import bitgemm, engine
-    rec = []
-    bitgemm.PROFILE_HOOK = rec
-    st = torch.cuda.Stream()
-    with torch.cuda.stream(st):
-        for _ in range(3):
-            engine.model_forward_group(batches, model)
-        torch.cuda.synchronize()
-        rec.clear()
-        # park the GPU so the host enqueues every launch first: events then bracket
-        # back-to-back kernels, not host gaps
-        torch.cuda._sleep(int(3e8))
-        for _ in range(reps):
-            engine.model_forward_group(batches, model)
-        torch.cuda.synchronize()
-    bitgemm.PROFILE_HOOK = None
-    dur = sum(s.elapsed_time(e) for s, e, _ in rec) / reps        # ms per epoch in bit-GEMMs
-    ops = sum(o for _, _, o in rec) / reps
-    launches = len(rec) / reps
-    return dur, ops, launches
+    from paper_2111_09547_b200.runtime import EpochRunner
+    r = EpochRunner(model, batches, rescan=False).capture(stamps=True)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    spans, ops, launches, step_ms = 0.0, 0.0, 0, 0.0
+    with torch.cuda.stream(r.stream):
+        for i in range(reps + 3):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(r.stream)
+            r.run()
+            e.record(r.stream)
+            torch.cuda.synchronize()
+            if i < 3:
+                continue
+            ks = r.kernel_spans()
+            spans += sum(t for t, _ in ks)
+            ops += sum(w for _, w in ks)
+            launches += len(ks)
+            step_ms += s.elapsed_time(e)
+    return spans / reps, ops / reps, launches / reps, step_ms / reps
 
 
 # ------------------------------------------------------------- CPU oracle
@@ -306,7 +332,7 @@ def reference_arm(args, world, rank):
             times.append(time.perf_counter() - t0)
     ms = float(np.mean(times)) * 1e3
     line = {
-        "metric": "QGNN inference ms/epoch (GIN 3x64, 4-bit); bit-GEMM effective TOPS",
+        "metric": METRIC,
         "value": ms, "unit": "ms/epoch", "impl": "reference", "n_gpus": args.gpus, "steps": steps,
         "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": f"u{args.bits}", "data": "synthetic",
@@ -327,17 +353,33 @@ def ours(args, world, rank):
     from paper_2111_09547_b200.runtime import EpochRunner, HostEpochRunner
 
     N.lib()
-    cfg, batches, feats, model = build_workload(args.config, args.bits, seed=rank)
+    from paper_2111_09547_b200 import shard, synth
+    base = synth.with_bits(synth.CONFIGS[args.config], args.bits)
+    sizes = synth.batch_part_sizes(base)
+    sharded = world > 1 and len(sizes) > 1
+    if sharded:
+        # strong scaling over independent subgraph batches: LPT plan, same on every rank
+        costs = [shard.batch_cost(s, base.in_dim, base.bits) for s in sizes]
+        plan = shard.assign_lpt(costs, world)
+        cfg, batches, feats, model = build_workload(args.config, args.bits, seed=0, batch_ids=plan[rank])
+    else:
+        # replicas (a single-batch config cannot shard): every rank its own epoch
+        cfg, batches, feats, model = build_workload(args.config, args.bits, seed=rank)
     runner = EpochRunner(model, batches, rescan=False).capture()
-    total_ms, clocks = time_device_epochs(runner, args.steps, args.warmup, world)
+    step = runner
+    if sharded:
+        rows = [int(s.sum()) for s in sizes]
+        step = ShardedStep(runner, shard.LogitGather(plan, rows, model.layers[-1].out_dim, torch.device("cuda")))
+    total_ms, clocks = time_device_epochs(step, args.steps, args.warmup, world)
     total_ms = max_over_ranks(world, total_ms)
-    ms_epoch = total_ms / (args.steps * world)
+    epochs = args.steps if sharded else args.steps * world
+    ms_epoch = total_ms / epochs
     launches = runner.kernel_launches_per_epoch() * args.steps
 
     # end to end through the public runtime: pinned H2D -> graph -> D2H every step
     host = HostEpochRunner(model, batches)
     e2e_ms, e2e_wall = time_e2e(host, args.steps, min(args.warmup, 5), world)
-    e2e_ms = max_over_ranks(world, e2e_ms) / (args.steps * world)
+    e2e_ms = max_over_ranks(world, e2e_ms) / epochs
 
     # parity of the e2e path against the device path
     with torch.cuda.stream(runner.stream):
@@ -349,7 +391,7 @@ def ours(args, world, rank):
     e2e_parity = bool(torch.equal(dev_logits, host_out))
 
     # roofline of the dominant kernel (bit-GEMM) -- algorithmic int8-MAC work per launch
-    gemm_ms, gemm_ops, gemm_launches = kernel_roofline(model, batches)
+    gemm_ms, gemm_ops, gemm_launches, stamped_step_ms = kernel_roofline(model, batches)
     peak, peak_src = int8_peak_tops()
     achieved = gemm_ops / (gemm_ms * 1e-3) / 1e12
     traffic = None
@@ -363,7 +405,7 @@ def ours(args, world, rank):
         for b in batches for ly in model.layers) / (ms_epoch * 1e-3) / 1e12
 
     sweep = {}
-    if not args.no_sweep:
+    if not args.no_sweep and not sharded:
         for bits in range(1, 9):
             if bits == args.bits:
                 sweep[str(bits)] = round(ms_epoch, 5)
@@ -373,6 +415,18 @@ def ours(args, world, rank):
             k = max(20, args.steps // 4)
             t, _ = time_device_epochs(rr, k, 5, world)
             sweep[str(bits)] = round(max_over_ranks(world, t) / (k * world), 5)
+            del rr, bb, mm
+
+    # configs[4] (C5): the standalone 1-bit x s-bit bit-GEMM at M=N=K=16k -- where the
+    # kernel is tensor-pipe bound rather than launch/latency bound like the C2 epoch
+    c5 = None
+    if not args.no_c5:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from c5_sweep import run_point
+        c5 = run_point(args.c5_n, 0.1, args.bits, reps=10, int8_peak=peak)
+        c5.update({"bound": "tensor", "peak": peak, "unit": "TOPS",
+                   "config": "C5: A Bernoulli(0.1) 1-bit x X uniform codes, reduce_bitplanes(bmm_1bit_by_nbit) "
+                             "in one tc_tiled_kernel launch, CUDA-graph replays timed with CUDA events"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -381,29 +435,37 @@ def ours(args, world, rank):
     if rank != 0:
         return
     line = {
-        "metric": "QGNN inference ms/epoch (GIN 3x64, 4-bit); bit-GEMM effective TOPS",
+        "metric": METRIC,
         "value": round(ms_epoch, 5), "unit": "ms/epoch", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_epoch, 5), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": f"u{args.bits} codes / s32 acc / fp64 epilogue",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "dtype": f"u{args.bits} codes / s32 acc / fp64 epilogue",
         "data": "synthetic planted-partition graph, U[0,1) features, random-init weights",
-        "config": {"workload": cfg.name, "model": "batched-gin 3 layers hidden 64", "bits": args.bits,
+        "config": {"workload": cfg.name, "model": f"batched-{cfg.model} {cfg.layers} layers hidden {cfg.hidden}", "bits": args.bits,
                    "nodes": cfg.num_nodes, "edges_undirected": cfg.num_edges, "parts": cfg.num_parts,
                    "batches": len(batches), "in_dim": cfg.in_dim, "classes": cfg.classes,
-                   "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}"},
+                   "l2": "flushed between steps (256 MB write)",
+                   "parallelism": (f"batch-sharded x{world} (LPT, 1 NCCL all_gather of logits per epoch)"
+                                   if sharded else f"replicas x{world}")},
         "sweep_ms_per_epoch_by_bits": sweep,
         "effective_tops": round(eff_tops, 3),
-        "roofline": {"bound": "tensor", "kernel": "tc_bitgemm_kernel (tcgen05.mma kind::i8)",
+        "roofline": {"bound": "tensor", "kernel": "tc_tiled_kernel (tcgen05.mma kind::i8, cp.async.bulk ring)",
                      "achieved": round(achieved, 3), "peak": peak, "unit": "TOPS",
                      "frac": round(achieved / peak, 5), "traffic": traffic, "peak_source": peak_src,
                      "work": "2 x 1024 x N_padded int8-MACs per non-zero 8x128 left tile (one u8 MAC "
-                             "retires all bit-plane pairs); durations from CUDA events per launch",
+                             "retires all bit-plane pairs)",
+                     "durations": "per-launch span (first CTA entry -> last CTA exit, %globaltimer) inside "
+                                  "an identical stamped epoch graph replayed after an L2 flush; CUDA events "
+                                  "around each replay give stamped_step_ms",
                      "launches_per_epoch": gemm_launches, "kernel_ms_per_epoch": round(gemm_ms, 5),
-                     "kernel_share_of_step": round(gemm_ms / ms_epoch, 3)},
+                     "stamped_step_ms": round(stamped_step_ms, 5),
+                     "kernel_share_of_step": round(gemm_ms / stamped_step_ms, 3)},
+        "gemm_roofline_c5": c5,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_ms, 5), "unit": "ms/epoch", "h2d_bytes_per_step": host.h2d_bytes,
                 "d2h_bytes_per_step": host.d2h_bytes, "wall_ms_per_step": round(e2e_wall / args.steps, 5),
                 "parity_vs_device_path": "bit-exact" if e2e_parity else "MISMATCH",
-                "path": "pinned QGT2 images -> 1 H2D -> epoch CUDA graph -> fp64 logits -> 1 D2H"},
+                "path": "ONE CUDA graph per step: pinned QGT3 images (schedule + non-zero 128x128 adjacency blocks + feature planes) -> 1 H2D -> block expansion + epoch -> fp64 logits -> 1 D2H"},
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -360,3 +360,125 @@ def batch_from_v2(header_bytes: bytes, dev_buf: torch.Tensor, base: int = 0) -> 
         params = QuantParams(amin, amax, xbits)
     return SubgraphBatch(node_ids=node_ids, adjacency=adj, features=feats, boundaries=boundaries,
                          x_params=params)
+
+
+# ------------------------------------------------------- QGT3 tile-sparse wire
+# QGT2 ships the dense packed adjacency (pad8(n) x pad128(n) bits) although a
+# block-diagonal batch has mostly all-zero 8x128 tiles (C2: ~92%).  QGT3 ships the
+# zero-tile-jumping schedule and ONLY the non-zero 128x128 bit blocks (2 KB each,
+# 128 rows x 4 words, the device `packed` layout of tiled.BlockedAdjacency), so the
+# single H2D carries ~8x fewer bytes and the device expands the blocks straight
+# into the tensor-core operand layout (qg_block_prepare, no gather).
+#   header (96 B): magic "QGT3", u16 version, u16 flags, u32 num_subgraphs,
+#   u32 total_nodes, u8 feature_bits, u8 x_bits, u16 reserved, f64 amin, f64 amax,
+#   u32 adj_pr, u32 adj_pc, u32 feat_pr, u32 feat_pc, u32 in_dim, u32 n_row_blocks,
+#   u32 n_blocks, u64 nonzero_8x128_tiles
+#   sections (256-B aligned): boundaries u32[ns+1], node_ids u32[total],
+#   blk_count i32[nrb], blk_base i32[nrb], blk_kt i32[nb], blk_rb i32[nb],
+#   blocks u32[nb][128][4], feature plane words.
+V3_MAGIC = b"QGT3"
+_V3_HEADER = struct.Struct("<4sHHIIBBHddIIIIIIIQ")
+
+
+def _v3_layout(ns: int, total: int, nrb: int, nb: int, feat_words: int):
+    def up(x):
+        return -(-x // _V2_ALIGN) * _V2_ALIGN
+    o = [up(_V3_HEADER.size)]
+    for size in (4 * (ns + 1), 4 * total, 4 * nrb, 4 * nrb, 4 * nb, 4 * nb, 2048 * nb, 4 * feat_words):
+        o.append(up(o[-1] + size))
+    return o        # boundaries, ids, count, base, kt, rb, blocks, feats, end
+
+
+def pack_batch_v3(b: SubgraphBatch) -> bytes:
+    """QGT3 image of a batch: schedule + non-zero 128x128 adjacency blocks + feature planes."""
+    from .tiled import blocked
+    a, f = b.adjacency, b.features
+    blk = blocked(a)
+    fw = 0 if f is None else int(f.dwords.numel())
+    ns, total, nrb, nb = b.num_subgraphs, b.total_nodes, blk.nrb, blk.nblocks
+    o = _v3_layout(ns, total, nrb, nb, fw)
+    out = bytearray(o[-1])
+    xp = b.x_params
+    _V3_HEADER.pack_into(out, 0, V3_MAGIC, 1, 0, ns, total, 0 if f is None else f.bits,
+                         0 if xp is None else xp.bits, 0, 0.0 if xp is None else xp.alpha_min,
+                         0.0 if xp is None else xp.alpha_max, a.padded_rows, a.padded_cols,
+                         0 if f is None else f.padded_rows, 0 if f is None else f.padded_cols,
+                         0 if f is None else f.logical_cols, nrb, nb, int(blk.nz8))
+    secs = [b.boundaries.astype("<u4"), b.node_ids.astype("<u4"),
+            blk.blk_count.cpu().numpy().astype("<i4"), blk.blk_base.cpu().numpy().astype("<i4"),
+            blk.blk_kt.cpu().numpy().astype("<i4"), blk.blk_rb.cpu().numpy().astype("<i4"),
+            blk.packed[:nb].cpu().numpy().astype("<i4")]
+    if f is not None:
+        secs.append(f.dwords.cpu().numpy().astype("<i4"))
+    for off, arr in zip(o, secs):
+        raw = arr.tobytes()
+        out[off:off + len(raw)] = raw
+    return bytes(out)
+
+
+class BlockSparseAdjacency(PackedBitMatrix):
+    """Column-wise 1-bit adjacency known only by its non-zero 128x128 blocks (QGT3).
+
+    The engine reads the blocks directly; the dense ``words`` (the reference's
+    layout) are scattered from them on first access, for API parity."""
+
+    def __init__(self, total, pr, pc, blocked_adj):
+        self.orientation = COLUMN_WISE
+        self.logical_rows = self.logical_cols = int(total)
+        self.padded_rows, self.padded_cols = int(pr), int(pc)
+        self._tilemap = None
+        self._schedule = None
+        self._np = None
+        self._dense = None
+        self._blocked = blocked_adj
+
+    @property
+    def dwords(self) -> torch.Tensor:
+        if self._dense is None:
+            blk = self._blocked
+            pr, pc = self.padded_rows, self.padded_cols
+            rows128 = -(-pr // 128) * 128
+            dense = torch.zeros((rows128, pc // 32), dtype=torch.int32, device=blk.packed.device)
+            if blk.nblocks:
+                view = dense.view(rows128 // 128, 128, pc // 128, 4)
+                view[blk.blk_rb.long(), :, blk.blk_kt.long(), :] = blk.packed[:blk.nblocks]
+            self._dense = dense[:pr].reshape(-1)
+        return self._dense
+
+    @dwords.setter
+    def dwords(self, value):
+        self._dense = value
+
+
+def batch_from_v3(header_bytes: bytes, dev_buf: torch.Tensor, base: int = 0) -> SubgraphBatch:
+    """Device views of a QGT3 image resident at ``dev_buf[base:]``; blocks are expanded by
+    ``BlockedAdjacency.refresh()`` (the epoch graph does it every step)."""
+    from .tiled import BlockedAdjacency
+    (magic, version, _flags, ns, total, fbits, xbits, _r, amin, amax, apr, apc, fpr, fpc, in_dim, nrb, nb,
+     nz8) = _V3_HEADER.unpack_from(header_bytes)
+    if magic != V3_MAGIC:
+        raise FormatError(f"bad compound-buffer magic {magic!r}")
+    if version != 1:
+        raise FormatError(f"unsupported compound-buffer version {version}")
+    fw = fbits * fpr * fpc // 32
+    o = _v3_layout(ns, total, nrb, nb, fw)
+    if len(header_bytes) < o[2]:
+        raise FormatError("compound buffer shorter than its id sections")
+    if (base + o[2]) % 256:
+        raise FormatError("QGT3 image must start 256-byte aligned")
+    boundaries = np.frombuffer(header_bytes, dtype="<u4", count=ns + 1, offset=o[0]).astype(np.int64)
+    node_ids = np.frombuffer(header_bytes, dtype="<u4", count=total, offset=o[1]).astype(np.int64)
+
+    def view(k, count, dtype=torch.int32):
+        return dev_buf[base + o[k]: base + o[k] + 4 * count].view(dtype)
+
+    blk = BlockedAdjacency.from_blocks(total, apr, view(2, nrb), view(3, nrb), view(4, nb), view(5, nb),
+                                       view(6, nb * 512).view(max(nb, 0), 128, 4), nb, nz8)
+    adj = BlockSparseAdjacency(total, apr, apc, blk)
+    blk._src = adj
+    feats = params = None
+    if fbits:
+        feats = BitPlaneStack._wrap(ROW_WISE, total, in_dim, fpr, fpc, view(7, fw).reshape(fbits, -1))
+        params = QuantParams(amin, amax, xbits)
+    return SubgraphBatch(node_ids=node_ids, adjacency=adj, features=feats, boundaries=boundaries,
+                         x_params=params)

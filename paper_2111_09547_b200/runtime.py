@@ -23,7 +23,7 @@ import torch
 
 from . import _native as N
 from .engine import ModelConfig, _prepared, model_forward_group
-from .graph import batch_from_v2, pack_batch_v2
+from .graph import batch_from_v3, pack_batch_v3
 
 
 class EpochRunner:
@@ -51,7 +51,12 @@ class EpochRunner:
                 blocked(b.adjacency).refresh()
         return model_forward_group(self.batches, self.model, jump=self.jump, reuse=self.reuse, verify=verify)
 
-    def capture(self):
+    def capture(self, pre=None, post=None, stamps: bool = False):
+        """Capture the epoch; ``pre()`` / ``post(logits)`` are captured before / after it
+        (HostEpochRunner: the H2D of the step's images and the D2H of the logits).
+        ``stamps``: every tiled GEMM CTA records %globaltimer at entry/exit (bench.py's
+        in-graph kernel durations; CUDA events cannot sit between a graph's kernels)."""
+        from . import bitgemm
         _prepared(self.model)
         from .tiled import blocked, weight_tiles
         for b in self.batches:
@@ -70,11 +75,19 @@ class EpochRunner:
             self.graph = torch.cuda.CUDAGraph()
             N.ALLOC = self.slabs
             try:
+                self.stamps = []
+                if stamps:
+                    bitgemm.PHASE_HOOK = self.stamps
                 with torch.cuda.graph(self.graph, stream=self.stream):
+                    if pre is not None:
+                        pre()
                     self.slabs.reset()              # 1 memset + 1 fill per epoch
                     self.logits = self._forward_all(verify=False)
+                    if post is not None:
+                        post(self.logits)
             finally:
                 N.ALLOC = N.TorchAlloc()
+                bitgemm.PHASE_HOOK = None
             N.flush_static_copies()
         self._checks = list(getattr(self.model, "_pending_checks", []))
         return self
@@ -84,52 +97,74 @@ class EpochRunner:
         self.graph.replay()
         return self.logits
 
+    def kernel_spans(self):
+        """[(span_ms, algorithmic_ops)] of the tiled GEMM launches of the LAST replay
+        (capture(stamps=True)): first CTA entry -> last CTA exit on %globaltimer."""
+        out = []
+        for st, work in self.stamps:
+            s = st.cpu().numpy()
+            s = s[s[:, 0] > 0]
+            if len(s):
+                out.append(((s[:, 5].max() - s[:, 0].min()) / 1e6, work))
+        return out
+
     def kernel_launches_per_epoch(self) -> int:
-        """Native kernels per epoch: per batch 2 (tile scan + schedule) + 1 entry code
-        conversion + 2 fused GEMMs per layer."""
-        per_epoch = 2 * len(self.model.layers) + 2 * len(self.batches)   # grouped GEMMs + entry conversions
+        """Native (libqgtc_b200) kernels per epoch: 1 grouped entry conversion + 2 grouped
+        fused GEMMs per layer; with rescan, per batch the block expansion (+ the gather
+        from dense words unless the blocks were shipped, QGT3)."""
+        from .tiled import blocked
+        per_epoch = 1 + 2 * len(self.model.layers)
         if self.rescan:
-            per_epoch += 2 * len(self.batches)                              # block gather + expand
+            per_epoch += sum(2 if getattr(blocked(b.adjacency), "_gather", True) else 1 for b in self.batches)
         return per_epoch
 
 
 class HostEpochRunner:
-    """End-to-end epoch: pinned host QGT2 images -> one H2D -> epoch graph -> one D2H."""
+    """End-to-end epoch as ONE CUDA graph: pinned host QGT3 images -> one H2D ->
+    block expansion + the epoch -> one D2H of the fp64 logits into pinned memory.
+
+    QGT3 (graph.pack_batch_v3) ships only the non-zero 128x128 adjacency blocks,
+    so the H2D carries the zero-tile-jumping schedule instead of the dense bits."""
 
     def __init__(self, model: ModelConfig, batches: list, **kw):
         self.model = model
-        images = [pack_batch_v2(b) for b in batches]
+        images = [pack_batch_v3(b) for b in batches]
         self.offsets = np.cumsum([0] + [len(im) for im in images])
         self.host = torch.empty(int(self.offsets[-1]), dtype=torch.uint8).pin_memory()
         self.load(images)
         self.device = torch.empty_like(self.host, device=N.device())
         self.device.copy_(self.host)
-        views = [batch_from_v2(im, self.device, int(o)) for im, o in zip(images, self.offsets)]
-        self.inner = EpochRunner(model, views, rescan=True, **kw).capture()
+        views = [batch_from_v3(im, self.device, int(o)) for im, o in zip(images, self.offsets)]
         rows = sum(v.total_nodes for v in views)
         self.classes = model.layers[-1].out_dim
         self.out_host = torch.empty((rows, self.classes), dtype=torch.float64).pin_memory()
         self.h2d_bytes = int(self.offsets[-1])
         self.d2h_bytes = rows * self.classes * 8
+        self.inner = EpochRunner(model, views, rescan=True, **kw).capture(pre=self._h2d, post=self._d2h)
+
+    def _h2d(self):
+        self.device.copy_(self.host, non_blocking=True)
+
+    def _d2h(self, outs):
+        r = 0
+        for o in outs:
+            self.out_host[r:r + o.shape[0]].copy_(o, non_blocking=True)
+            r += o.shape[0]
 
     @property
     def stream(self):
         return self.inner.stream
 
     def load(self, images) -> None:
-        """Place a step's QGT2 images into the pinned staging area (host memcpy)."""
+        """Place a step's QGT3 images into the pinned staging area (host memcpy)."""
         for im, o in zip(images, self.offsets):
             self.host[int(o):int(o) + len(im)] = torch.frombuffer(bytearray(im), dtype=torch.uint8)
 
     def run_host(self) -> torch.Tensor:
-        """H2D + epoch graph + D2H on the runner's stream; returns the pinned logits."""
+        """H2D + epoch + D2H: one graph launch on the runner's stream; returns the pinned logits
+        (valid after the stream synchronises)."""
         with torch.cuda.stream(self.stream):
-            self.device.copy_(self.host, non_blocking=True)
-            outs = self.inner.run()
-            r = 0
-            for o in outs:
-                self.out_host[r:r + o.shape[0]].copy_(o, non_blocking=True)
-                r += o.shape[0]
+            self.inner.run()
         return self.out_host
 
 

@@ -161,3 +161,11 @@ def random_codes_stack(rows: int, cols: int, bits: int, orientation: str, seed: 
     N.call("qg_quantize_pack", N.ptr(codes), N.SRC_U8, rows, cols, cols, 0.0, 1.0, bits, oid, pad_to,
            N.ptr(planes), None, None, None, N.ptr(status), N.stream())
     return BitPlaneStack._wrap(orientation, rows, cols, pr, pc, planes), codes
+
+
+def batch_part_sizes(cfg: GraphConfig) -> list:
+    """Node count of every part, per batch (parts batched in order, cli.py:179-186) --
+    host-only, so ranks can plan the shard assignment before building anything."""
+    sizes = np.diff(part_bounds(cfg))
+    n_batches = -(-cfg.num_parts // cfg.parts_per_batch)
+    return [sizes[b * cfg.parts_per_batch:(b + 1) * cfg.parts_per_batch] for b in range(n_batches)]

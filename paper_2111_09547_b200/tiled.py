@@ -113,12 +113,37 @@ class BlockedAdjacency:
         self.nz8 = schedule.rt * schedule.ct - schedule.zeros
         self.refresh()
 
+    @classmethod
+    def from_blocks(cls, rows, padded_rows, blk_count, blk_base, blk_kt, blk_rb, packed, nblocks, nz8):
+        """Adopt a shipped schedule + packed blocks (QGT3 wire views); ``refresh()``
+        expands them (no gather: the dense words never exist on the device)."""
+        self = cls.__new__(cls)
+        self.nrb = int(blk_count.numel())
+        self.nblocks = int(nblocks)
+        dev = blk_count.device
+        self.blk_count, self.blk_base, self.blk_kt, self.blk_rb = blk_count, blk_base, blk_kt, blk_rb
+        self.packed = packed if nblocks else torch.zeros((1, 128, 4), dtype=torch.int32, device=dev)
+        self.bytes = torch.empty((max(self.nblocks, 1), 16384), dtype=torch.uint8, device=dev)
+        self.degrees = torch.zeros(int(rows), dtype=torch.int64, device=dev)
+        self.m = int(rows)
+        self.r128 = pad128(int(rows))
+        self.nz8 = int(nz8)
+        self._src = None
+        self._gather = False
+        self.refresh()
+        return self
+
     def refresh(self):
         """Re-gather + re-expand the blocks (and degrees) from the adjacency's current
         words with the same schedule -- device only, capturable in a CUDA graph."""
         a = self._src
         self.degrees.zero_()
         if self.nblocks:
+            if not getattr(self, "_gather", True):      # shipped blocks: expand only
+                N.check(_lib().qg_block_prepare(None, self.m, 0, 0, N.ptr(self.blk_rb), N.ptr(self.blk_kt),
+                                                self.nblocks, N.ptr(self.packed), N.ptr(self.bytes),
+                                                N.ptr(self.degrees), N.stream()), "qg_block_prepare")
+                return
             N.check(_lib().qg_block_prepare(N.ptr(a.dwords), a.logical_rows, a.padded_rows, a.padded_cols,
                                             N.ptr(self.blk_rb), N.ptr(self.blk_kt), self.nblocks, N.ptr(self.packed),
                                             N.ptr(self.bytes), N.ptr(self.degrees), N.stream()), "qg_block_prepare")
@@ -276,7 +301,7 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     if bitgemm.PHASE_HOOK is not None:
         stamps = torch.zeros((begin, 8), dtype=torch.int64, device=N.device())
         args.phase_ns = stamps.data_ptr()
-        bitgemm.PHASE_HOOK.append(stamps)
+        bitgemm.PHASE_HOOK.append((stamps, work))
     if bitgemm.PROFILE_HOOK is not None:
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record()

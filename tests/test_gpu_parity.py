@@ -221,6 +221,33 @@ def test_compound_buffer_roundtrip_matches_golden(i):
     np.testing.assert_array_equal(bg.model_forward(back, _model_from_case(c)), c.logits)
 
 
+@pytest.mark.parametrize("i", range(6))
+def test_tile_sparse_wire_format_roundtrip(i):
+    """QGT3 (schedule + non-zero 128x128 blocks only): the rebuilt dense words equal the
+    original adjacency, and the end-to-end runner (one graph: H2D -> epoch -> D2H)
+    reproduces the reference logits bit for bit."""
+    import torch
+
+    from paper_2111_09547_b200 import graph
+    from paper_2111_09547_b200.runtime import HostEpochRunner
+    c = model_case(load("model"), i)
+    batch, _ = _batch_from_case(c)
+    img = graph.pack_batch_v3(batch)
+    dev = torch.from_numpy(np.frombuffer(img, dtype=np.uint8).copy()).cuda()
+    back = graph.batch_from_v3(img, dev, 0)
+    np.testing.assert_array_equal(back.adjacency.words, batch.adjacency.words)
+    assert back.features == batch.features
+    np.testing.assert_array_equal(back.degrees(), batch.degrees())
+    model = _model_from_case(c)
+    np.testing.assert_array_equal(bg.model_forward(back, model), c.logits)
+    host = HostEpochRunner(model, [batch])
+    assert host.h2d_bytes == len(img)
+    for _ in range(2):
+        out = host.run_host()
+        host.stream.synchronize()
+        np.testing.assert_array_equal(out.numpy(), c.logits)
+
+
 def test_bindings_match_golden():
     from paper_2111_09547_b200 import bindings as bb
     d = load("bindings")

@@ -23,7 +23,7 @@ bitgemm.PHASE_HOOK = rec
 engine.model_forward_group(batches, model)
 torch.cuda.synchronize()
 bitgemm.PHASE_HOOK = None
-for i, st in enumerate(rec):
+for i, (st, _) in enumerate(rec):
     s = st.cpu().numpy().astype(np.float64)
     s = s[s[:, 0] > 0]
     t0 = s[:, 0].min()
