@@ -170,6 +170,13 @@ typedef struct {
   int64_t q_codes_ld;
   int32_t q_codes_colmajor;
   int32_t q_skip_planes;       /* 1: write only the code cache (planes built lazily) */
+  /* Tiled fast path, packed output only: affine screen of the requantized code.
+   * y = P_c*acc + G_c*row_term + R_c approximates the reference quotient
+   * (x - q_amin)/q_scale within screen_tol (host-derived bound on both chains'
+   * rounding); codes whose y lies within screen_tol of a code boundary are
+   * recomputed with the exact reference expression.  0 disables the screen. */
+  double screen_tol;
+  double screen_r0;            /* 2^12 + RN(-q_amin * q_inv_scale): ReLU floor in r-space */
 } qg_epilogue;
 
 /*

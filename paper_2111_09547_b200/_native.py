@@ -53,7 +53,7 @@ class Epilogue(ctypes.Structure):
         ("q_prows", _i64), ("q_pcols", _i64),
         ("out_real", _vp), ("q_planes", _vp), ("q_row_sums", _vp), ("status", _vp),
         ("q_codes", _vp), ("q_codes_ld", _i64), ("q_codes_colmajor", ctypes.c_int32),
-        ("q_skip_planes", ctypes.c_int32),
+        ("q_skip_planes", ctypes.c_int32), ("screen_tol", _f64), ("screen_r0", _f64),
     ]
 
 

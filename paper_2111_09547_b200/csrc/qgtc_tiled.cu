@@ -51,6 +51,22 @@ static __device__ __noinline__ uint32_t requant_exact(double x, double amin, dou
   return quantize_code_fast(x, amin, scale, inv, maxv);
 }
 
+// Exact reference requant of one element, column constants from global memory (the
+// screened epilogue's rare fallback; identical expression to epi_slices, absent
+// terms +0.0).
+static __device__ __noinline__ uint32_t exact_code_global(const qg_epilogue& E, uint32_t accbits, double rterm,
+                                                          int64_t c, uint32_t maxv, int64_t* status, int64_t flat) {
+  double x = __dadd_rn(__dmul_rn(E.k_acc, (double)(int32_t)accbits), rterm);
+  const double sC = E.use_col ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
+  const double kc = E.use_const ? E.k_const : 0.0;
+  const double sB = E.bias ? E.bias[c] : 0.0;
+  x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC), kc), sB);
+  if (E.bn_mean)
+    x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, E.bn_mean[c]), E.bn_denom[c]), E.bn_gamma[c]), E.bn_beta[c]);
+  if (E.act == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
+  return requant_exact(x, E.q_amin, E.q_scale, E.q_inv_scale, maxv, status, flat);
+}
+
 // Per-thread epilogue context: this lane owns one accumulator row (TMEM lane) and
 // walks 8-column slices first, first+2, ...
 struct EpiLane {
@@ -179,12 +195,104 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   return rsum;
 }
 
+// Screened fused requant (packed hidden outputs, act none/relu): per element
+//   r = fma(P_c, acc, fma(G_c, row_term, R_c))  [+ max with the ReLU floor]
+// is 2^12 + y, y ~ (x - q_amin)/q_scale within screen_tol of the reference quotient,
+// so floor(y) is the reference code unless y is within screen_tol of a code boundary
+// 1..maxv (boundaries at 0 and maxv+1 clip to the same code on both sides).  The
+// high word of r in [2^12, 2^13) holds 0x40B00000 + (floor << 8) + top fraction bits.
+// Flagged slices (rare) and ragged edges take exact_code_global.
+template <bool RELU>
+__device__ __forceinline__ uint32_t epi_slices_screen(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
+                                                      const double* __restrict__ sCol, double rterm) {
+  const qg_epilogue& E = P.epi;
+  const int bn = P.bn;
+  const double* sP = sCol;
+  const double* sG = sCol + bn;
+  const double* sR = sCol + 2 * bn;
+  const uint32_t maxv = (1u << E.q_bits) - 1u;
+  const double r0 = E.screen_r0;
+  const uint32_t tb = (uint32_t)(E.screen_tol * 0x1p40) + 4u;    // tolerance in 2^-40 units (< 2^31)
+  const uint32_t tb2 = 2u * tb;
+  const int out_layout = P.out_layout;
+  uint8_t* const q_codes = G.q_codes;
+  int64_t* const status = G.status;
+  const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
+  const int nsl16 = (L.nslices + 1) >> 1;                  // 16-column slices
+  uint32_t rsum = 0;
+  for (int sl = L.first; sl < nsl16; sl += 2) {
+    const int c16 = sl * 16;
+    uint32_t v[16];
+    if (L.has_acc) {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(L.tmem_row + (uint32_t)c16));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) v[jj] = 0;
+    }
+    bool slow = false;
+    uint32_t q[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int cl = c16 + jj;
+      double r = __fma_rn(sP[cl], (double)(int32_t)v[jj], __fma_rn(sG[cl], rterm, sR[cl]));
+      if (RELU) r = fmax(r, r0);
+      const uint32_t hi = (uint32_t)__double2hiint(r), lo = (uint32_t)__double2loint(r);
+      // code: floor of y = r - 2^12 for r in [2^12, 2^13), clamped; negative / tiny r -> 0,
+      // r >= 2^13 -> maxv (arithmetic shift keeps negative r negative)
+      const int kc = (__double2hiint(r) >> 8) - 0x40B000;
+      q[jj] = (uint32_t)min(max(kc, 0), (int)maxv);
+      // near a boundary B in [1, maxv]: the 40-bit fraction of r within tb of 0 or 1
+      const uint32_t t = lo + tb;
+      const uint32_t hc = hi + (t < lo ? 1u : 0u);
+      const int B = ((int)hc >> 8) - 0x40B000;
+      slow |= ((hc & 0xFFu) == 0u) & (t < tb2) & (B >= 1) & (c16 + jj < L.nvalid);
+    }
+    if (slow && L.rvalid) {
+#pragma unroll 1
+      for (int jj = 0; jj < 16; ++jj)
+        if (c16 + jj < L.nvalid)
+          q[jj] = exact_code_global(E, v[jj], rterm, L.n0 + c16 + jj, maxv, status, L.myrow * pn + L.n0 + c16 + jj);
+    }
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8) {
+      const uint32_t* qq = q + 8 * h8;
+      const int cl8 = c16 + 8 * h8;
+      const uint32_t lo = qq[0] | (qq[1] << 8) | (qq[2] << 16) | (qq[3] << 24);
+      const uint32_t hi = qq[4] | (qq[5] << 8) | (qq[6] << 16) | (qq[7] << 24);
+      rsum += ((qq[0] + qq[1]) + (qq[2] + qq[3])) + ((qq[4] + qq[5]) + (qq[6] + qq[7]));
+      if (L.rvalid && cl8 < L.nvalid) {
+        const int64_t cb = L.n0 + cl8;
+        if (out_layout == 1) {
+          *reinterpret_cast<uint2*>(q_codes + left_tile_off(L.myrow, cb, r128)) = make_uint2(lo, hi);
+        } else {
+          uint8_t* base = q_codes + right_tile_off(L.myrow, cb, out_npad);
+          if (cl8 + 8 <= L.nvalid) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) base[jj * 16] = (uint8_t)qq[jj];
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)qq[jj];
+          }
+        }
+      }
+    }
+  }
+  return rsum;
+}
+
 template <int TMEM_COLS>
 __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[8], empty[8], done;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[128];
+  __shared__ double sRowTerm[128];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bn = P.bn, S = P.stages;
   if (tid == 0) tstamp(P, 0);
@@ -206,9 +314,13 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   const uint32_t stage_bytes = a_bytes + b_bytes;
   double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);   // [2 or 6][bn] per-column constants
 
+  // schedule arrays are static for the lifetime of a launch sequence (built before the
+  // epoch, or shipped by the step's H2D which precedes every kernel): readable before
+  // griddepcontrol.wait
   int nk, kbase = 0;
   if (P.a_blocks) { nk = G.blk_count[rb]; kbase = G.blk_base[rb]; }
   else nk = G.k_tiles;
+  asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
@@ -222,7 +334,12 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   }
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
+  const bool screen = fused && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
+                      (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
   if (tid < 128) sRowSum[tid] = 0ull;
+  // everything below may read the predecessor grid's outputs (activations, row sums,
+  // per-forward epilogue vectors)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -260,8 +377,37 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
     }
     if (nk > 0) umma_commit(&done);
   } else if (warp >= 2 && fused) {
-    // warps 2..7 stage the per-column epilogue constants while the first K tiles land
-    for (int i = tid - 64; i < bn; i += kTThreads - 64) {
+    // warps 2..7 stage the epilogue constants while the main loop runs: the row terms
+    // RN(k_row * row_sum) (predecessor outputs) and the per-column constants
+    const int t = tid - 64;
+    if (t < 128) {
+      const int64_t row = rb * 128 + t;
+      sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
+    }
+    if (screen) {
+    // screened requant: per-column affine coefficients P_c, G_c, R_c (see epi_slices_screen)
+    for (int i = t; i < bn; i += kTThreads - 64) {
+      const int64_t c = n0 + i;
+      double pc = 0.0, gc = 0.0, rc = 0x1p12;
+      if (c < P.n) {
+        const double inv = E.q_inv_scale;
+        const double sC = E.use_col ? E.k_col * (double)E.col_sums[c] : 0.0;
+        const double base = (sC + (E.use_const ? E.k_const : 0.0)) + (E.bias ? E.bias[c] : 0.0);
+        double g = 1.0, center = base;
+        if (E.bn_mean) {
+          g = E.bn_gamma[c] / E.bn_denom[c];
+          center = (base - E.bn_mean[c]) * g + E.bn_beta[c];
+        }
+        gc = g * inv;
+        pc = E.k_acc * gc;
+        rc = 0x1p12 + (center - E.q_amin) * inv;
+      }
+      sCol[i] = pc;
+      sCol[bn + i] = gc;
+      sCol[2 * bn + i] = rc;
+    }
+    } else {
+    for (int i = t; i < bn; i += kTThreads - 64) {
       const int64_t c = n0 + i;
       const bool ok = c < P.n;
       // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
@@ -275,6 +421,7 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
         sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
         sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
       }
+    }
     }
   }
   __syncwarp();
@@ -324,9 +471,12 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
     }
   } else {
     // one uniform dispatch per CTA: the slice loop below is straight-line per variant
-    const double rterm = (E.use_row && rvalid) ? __dmul_rn(E.k_row, (double)G.row_sums[myrow]) : 0.0;
+    const double rterm = rvalid ? sRowTerm[quad * 32 + lane] : 0.0;
     const bool row_only = !E.use_col && !E.use_const && !E.bias;
-    switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
+    if (screen) {
+      rsum = E.act == QG_ACT_RELU ? epi_slices_screen<true>(P, G, L, sCol, rterm)
+                                  : epi_slices_screen<false>(P, G, L, sCol, rterm);
+    } else switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
 #define QG_EPI_CASE(i, A, B, R) \
   case i: rsum = epi_slices<A, B, R>(P, G, L, sCol, rterm); break;
       QG_EPI_CASE(0, QG_ACT_NONE, false, false)
@@ -511,6 +661,26 @@ static void tiled_attr(size_t bytes) {
   }
 }
 
+// Programmatic dependent launch: the grid may start while its stream predecessor is
+// still running; the kernel's griddepcontrol.wait (after its prologue) orders every
+// read of predecessor outputs, so launch latency + TMEM/barrier setup overlap the
+// previous layer's tail.  Captured into CUDA graphs as programmatic edges.
+template <int COLS>
+static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
+  static const bool pdl = getenv("QG_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS>, P);
+}
+
 extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   if (!a || !a->segs || a->nsegs < 1 || a->total_ctas < 1) return QG_ERR_ARG;
   if (a->bn < 32 || a->bn > 256 || (a->bn & (a->bn - 1))) return QG_ERR_ARG;
@@ -525,7 +695,9 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   if (a->epi) P.epi = *a->epi;
   P.phase_ns = a->phase_ns;
   const size_t stage = 16384 + (size_t)P.bn * 128;
-  const size_t cols = (a->epi && a->epi->bn_mean ? 6 : 2) * (size_t)P.bn * 8;
+  const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
+                      (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
+  const size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
   // the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's
   // fp64 epilogue overlaps the other's bulk-copy/MMA main loop); TMEM 2 x 256 cols fits
   size_t budget = 113 * 1024 - 4096;
@@ -536,10 +708,10 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = (unsigned)a->total_ctas;
   switch (P.bn) {
-    case 32: tiled_attr<32>(smem); tc_tiled_kernel<32><<<grid, kTThreads, smem, st>>>(P); break;
-    case 64: tiled_attr<64>(smem); tc_tiled_kernel<64><<<grid, kTThreads, smem, st>>>(P); break;
-    case 128: tiled_attr<128>(smem); tc_tiled_kernel<128><<<grid, kTThreads, smem, st>>>(P); break;
-    default: tiled_attr<256>(smem); tc_tiled_kernel<256><<<grid, kTThreads, smem, st>>>(P); break;
+    case 32: tiled_attr<32>(smem); launch_tiled<32>(P, grid, smem, st); break;
+    case 64: tiled_attr<64>(smem); launch_tiled<64>(P, grid, smem, st); break;
+    case 128: tiled_attr<128>(smem); launch_tiled<128>(P, grid, smem, st); break;
+    default: tiled_attr<256>(smem); launch_tiled<256>(P, grid, smem, st); break;
   }
   return tstatus();
 }

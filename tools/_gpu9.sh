@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python tools/cold_step.py C2 4 > gpurun_out/cold.log 2>&1
+QG_NO_PDL=1 timeout 300 python tools/cold_step.py C2 4 > gpurun_out/cold_nopdl.log 2>&1
+timeout 300 python tools/run_config.py C3 > gpurun_out/c3.log 2>&1
+timeout 600 python tools/run_config.py C4 8 > gpurun_out/c4.log 2>&1
