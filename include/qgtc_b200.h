@@ -276,6 +276,13 @@ typedef struct {
  * engine.py:320-332 for a whole epoch layer stage. */
 int qg_tiled_gemm(const qg_tiled_args* args, void* stream);
 
+/* Every GEMM stage of an epoch (<= 8, e.g. 2 per layer over all batches) in ONE
+ * persistent cooperative launch: CTAs sweep each stage's tiles and meet at a grid
+ * barrier before the next stage.  Same arithmetic as nstages qg_tiled_gemm calls in
+ * order; grid_bar is 9 caller-owned device words (barrier + per-stage tile counters,
+ * zeroed by the call, stream-ordered). */
+int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint32_t* grid_bar, void* stream);
+
 /* Gather the non-zero 128x128 blocks (blk_rb/blk_kt) of a column-wise 1-bit matrix
  * into `packed` (2 KB each; skipped when a_words == NULL and `packed` is already
  * filled, e.g. shipped by the QGT2 tile-sparse wire format), expand them to 16 KB

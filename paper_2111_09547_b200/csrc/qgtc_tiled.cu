@@ -16,6 +16,7 @@
 // subgraph batches is a single grid.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include "qgtc_common.cuh"
 
 namespace qg {
@@ -31,14 +32,15 @@ struct TiledParams {
   int32_t out_layout;       // 0 fp64/int32 row-major, 1 left-tiled codes, 2 right-tiled codes
   int64_t out_npad;         // right-tiled output: padded N of the output (slab pitch)
   qg_epilogue epi;          // shared scalars + per-column vectors (per-row pointers come from segs)
-  int64_t* phase_ns;        // optional per-CTA %globaltimer stamps (tools/phase_tiled.py)
+  int64_t* phase_ns;        // optional per-tile %globaltimer stamps (tools/phase_tiled.py)
+  int64_t total_ctas;       // work items (segment, row block, N tile) of this stage
 };
 
-static __device__ __forceinline__ void tstamp(const TiledParams& P, int k) {
+static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
   if (P.phase_ns) {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    P.phase_ns[(int64_t)blockIdx.x * 8 + k] = (int64_t)t;
+    P.phase_ns[tile * 8 + k] = (int64_t)t;
   }
 }
 
@@ -286,72 +288,70 @@ __device__ __forceinline__ uint32_t epi_slices_screen(const TiledParams& P, cons
   return rsum;
 }
 
-template <int TMEM_COLS>
-__global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], done;
-  __shared__ uint32_t tmem_base_s;
-  __shared__ unsigned long long sRowSum[128];
-  __shared__ double sRowTerm[128];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bn = P.bn, S = P.stages;
-  if (tid == 0) tstamp(P, 0);
+// Per-CTA state that persists across the tiles one CTA processes (the persistent
+// epoch kernel runs many tiles of many stages through the same ring / TMEM).
+struct TileRing {
+  uint8_t* stage0;            // S ring slots of (16 KB + bn_max * 128 B)
+  double* sCol;               // per-column epilogue constants
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* done;
+  unsigned long long* sRowSum;
+  double* sRowTerm;
+  uint32_t tmem;
+  int S;
+  uint32_t it0;               // ring position (K tiles issued so far)
+  uint32_t ndone;             // accumulator phases completed so far
+};
 
-  // ---- segment lookup (uniform): last segment with cta_begin <= blockIdx.x
+// One work item: (segment, 128-row block, N tile) -> fused GEMM tile.  Ends with a
+// CTA barrier so the next tile may overwrite TMEM / shared staging.
+template <int TMEM_COLS>
+__device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, TileRing& R) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bn = P.bn, S = R.S;
+  if (tid == 0) tstamp(P, tile, 0);
+
+  // ---- segment lookup (uniform): last segment with cta_begin <= tile
   int lo = 0, hi = P.nsegs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (P.segs[mid].cta_begin <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
+    if (P.segs[mid].cta_begin <= tile) lo = mid; else hi = mid - 1;
   }
   const qg_tseg& G = P.segs[lo];
-  const int64_t local = (int64_t)blockIdx.x - G.cta_begin;
+  const int64_t local = tile - G.cta_begin;
   const int64_t rb = local / P.n_tiles;
   const int nt = (int)(local % P.n_tiles);
   const int64_t n0 = (int64_t)nt * bn;
 
   const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u;
-  uint8_t* stage0 = smem;
+  uint8_t* stage0 = R.stage0;
   const uint32_t stage_bytes = a_bytes + b_bytes;
-  double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);   // [2 or 6][bn] per-column constants
+  double* sCol = R.sCol;
+  uint64_t* full = R.full;
+  uint64_t* empty = R.empty;
+  const uint32_t tmem = R.tmem;
+  const uint32_t it0 = R.it0;
 
-  // schedule arrays are static for the lifetime of a launch sequence (built before the
-  // epoch, or shipped by the step's H2D which precedes every kernel): readable before
-  // griddepcontrol.wait
   int nk, kbase = 0;
   if (P.a_blocks) { nk = G.blk_count[rb]; kbase = G.blk_base[rb]; }
   else nk = G.k_tiles;
-  asm volatile("griddepcontrol.launch_dependents;");
+  R.it0 += (uint32_t)nk;                                  // every thread tracks the ring position
 
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 32) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(&done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
   const bool screen = fused && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
                       (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
-  if (tid < 128) sRowSum[tid] = 0ull;
-  // everything below may read the predecessor grid's outputs (activations, row sums,
-  // per-forward epilogue vectors)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base_s;
-  if (tid == 0) tstamp(P, 1);
+  if (tid < 128) R.sRowSum[tid] = 0ull;
+  if (tid == 0) tstamp(P, tile, 1);
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer: two bulk copies per K tile ----------------
     const uint8_t* bbase = G.b + (n0 >> 3) * 1024;
     for (int it = 0; it < nk; ++it) {
-      const int s = it % S;
-      if (it >= S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
+      const uint32_t g = it0 + (uint32_t)it;
+      const int s = (int)(g % (uint32_t)S);
+      if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
       int kt;
       const uint8_t* asrc;
       if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
@@ -365,9 +365,10 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = idesc_u8(bn);
     for (int it = 0; it < nk; ++it) {
-      const int s = it % S;
-      mbar_wait(smem_u32(&full[s]), (it / S) & 1);
-      if (it == 0) tstamp(P, 2);
+      const uint32_t g = it0 + (uint32_t)it;
+      const int s = (int)(g % (uint32_t)S);
+      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+      if (it == 0) tstamp(P, tile, 2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
 #pragma unroll
@@ -375,62 +376,63 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
         umma_i8(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc, (it > 0 || kk > 0) ? 1u : 0u);
       umma_commit(&empty[s]);
     }
-    if (nk > 0) umma_commit(&done);
+    if (nk > 0) umma_commit(R.done);
   } else if (warp >= 2 && fused) {
     // warps 2..7 stage the epilogue constants while the main loop runs: the row terms
     // RN(k_row * row_sum) (predecessor outputs) and the per-column constants
     const int t = tid - 64;
     if (t < 128) {
       const int64_t row = rb * 128 + t;
-      sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
+      R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
     }
     if (screen) {
-    // screened requant: per-column affine coefficients P_c, G_c, R_c (see epi_slices_screen)
-    for (int i = t; i < bn; i += kTThreads - 64) {
-      const int64_t c = n0 + i;
-      double pc = 0.0, gc = 0.0, rc = 0x1p12;
-      if (c < P.n) {
-        const double inv = E.q_inv_scale;
-        const double sC = E.use_col ? E.k_col * (double)E.col_sums[c] : 0.0;
-        const double base = (sC + (E.use_const ? E.k_const : 0.0)) + (E.bias ? E.bias[c] : 0.0);
-        double g = 1.0, center = base;
-        if (E.bn_mean) {
-          g = E.bn_gamma[c] / E.bn_denom[c];
-          center = (base - E.bn_mean[c]) * g + E.bn_beta[c];
+      // screened requant: per-column affine coefficients P_c, G_c, R_c (see epi_slices_screen)
+      for (int i = t; i < bn; i += kTThreads - 64) {
+        const int64_t c = n0 + i;
+        double pc = 0.0, gc = 0.0, rc = 0x1p12;
+        if (c < P.n) {
+          const double inv = E.q_inv_scale;
+          const double sC = E.use_col ? E.k_col * (double)E.col_sums[c] : 0.0;
+          const double base = (sC + (E.use_const ? E.k_const : 0.0)) + (E.bias ? E.bias[c] : 0.0);
+          double g = 1.0, center = base;
+          if (E.bn_mean) {
+            g = E.bn_gamma[c] / E.bn_denom[c];
+            center = (base - E.bn_mean[c]) * g + E.bn_beta[c];
+          }
+          gc = g * inv;
+          pc = E.k_acc * gc;
+          rc = 0x1p12 + (center - E.q_amin) * inv;
         }
-        gc = g * inv;
-        pc = E.k_acc * gc;
-        rc = 0x1p12 + (center - E.q_amin) * inv;
+        sCol[i] = pc;
+        sCol[bn + i] = gc;
+        sCol[2 * bn + i] = rc;
       }
-      sCol[i] = pc;
-      sCol[bn + i] = gc;
-      sCol[2 * bn + i] = rc;
-    }
     } else {
-    for (int i = t; i < bn; i += kTThreads - 64) {
-      const int64_t c = n0 + i;
-      const bool ok = c < P.n;
-      // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
-      // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
-      // evaluates the reference's grouping without per-element branches
-      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
-      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
-      if (E.bn_mean) {
-        sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
-        sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
-        sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
-        sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+      for (int i = t; i < bn; i += kTThreads - 64) {
+        const int64_t c = n0 + i;
+        const bool ok = c < P.n;
+        // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
+        // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
+        // evaluates the reference's grouping without per-element branches
+        sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
+        sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
+        if (E.bn_mean) {
+          sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
+          sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
+          sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
+          sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+        }
       }
-    }
     }
   }
   __syncwarp();
   if (nk > 0) {
-    mbar_wait(smem_u32(&done), 0);
+    mbar_wait(smem_u32(R.done), R.ndone & 1);
+    R.ndone += 1;
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
-  if (fused) __syncthreads();   // sCol visible to all epilogue warps
-  if (tid == 0) tstamp(P, 3);
+  __syncthreads();   // sCol / row terms / zeroed row sums visible to all epilogue warps
+  if (tid == 0) tstamp(P, tile, 3);
 
   // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
   const int quad = warp & 3, half = warp >> 2;
@@ -470,15 +472,15 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
       }
     }
   } else {
-    // one uniform dispatch per CTA: the slice loop below is straight-line per variant
-    const double rterm = rvalid ? sRowTerm[quad * 32 + lane] : 0.0;
+    // one uniform dispatch per tile: the slice loop below is straight-line per variant
+    const double rterm = rvalid ? R.sRowTerm[quad * 32 + lane] : 0.0;
     const bool row_only = !E.use_col && !E.use_const && !E.bias;
     if (screen) {
       rsum = E.act == QG_ACT_RELU ? epi_slices_screen<true>(P, G, L, sCol, rterm)
                                   : epi_slices_screen<false>(P, G, L, sCol, rterm);
     } else switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
-#define QG_EPI_CASE(i, A, B, R) \
-  case i: rsum = epi_slices<A, B, R>(P, G, L, sCol, rterm); break;
+#define QG_EPI_CASE(i, A, B, Rw) \
+  case i: rsum = epi_slices<A, B, Rw>(P, G, L, sCol, rterm); break;
       QG_EPI_CASE(0, QG_ACT_NONE, false, false)
       QG_EPI_CASE(1, QG_ACT_NONE, false, true)
       QG_EPI_CASE(2, QG_ACT_NONE, true, false)
@@ -494,17 +496,140 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
 #undef QG_EPI_CASE
     }
   }
-  if (tid == 0) tstamp(P, 4);
+  if (tid == 0) tstamp(P, tile, 4);
   if (packed && G.q_row_sums) {
-    if (rsum) atomicAdd(&sRowSum[quad * 32 + lane], (unsigned long long)rsum);
+    if (rsum) atomicAdd(&R.sRowSum[quad * 32 + lane], (unsigned long long)rsum);
     __syncthreads();
-    if (tid < 128 && rb * 128 + tid < G.m && sRowSum[tid])
-      atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[tid]);
+    if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[tid])
+      atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
-  if (tid == 0) tstamp(P, 5);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (tid == 0) tstamp(P, tile, 5);
+}
+
+// CTA setup shared by both kernels: TMEM allocation, ring barriers.
+template <int TMEM_COLS>
+__device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                            uint64_t* done, uint32_t* tmem_base_s, unsigned long long* sRowSum,
+                                            double* sRowTerm, int S, uint32_t stage_bytes_max) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_s)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  R.stage0 = smem;
+  R.sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes_max);
+  R.full = full;
+  R.empty = empty;
+  R.done = done;
+  R.sRowSum = sRowSum;
+  R.sRowTerm = sRowTerm;
+  R.S = S;
+  R.it0 = 0;
+  R.ndone = 0;
+}
+
+template <int TMEM_COLS>
+__global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ unsigned long long sRowSum[128];
+  __shared__ double sRowTerm[128];
+  TileRing R;
+  // schedule arrays and the segment table are static for the lifetime of a launch
+  // sequence; only predecessor OUTPUTS need griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
+                         16384u + (uint32_t)P.bn * 128u);
+  // everything below may read the predecessor grid's outputs (activations, row sums,
+  // per-forward epilogue vectors)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  R.tmem = tmem_base_s;
+  tiled_tile<TMEM_COLS>(P, (int64_t)blockIdx.x, R);
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
+}
+
+// ------------------------------------------------ persistent epoch kernel
+// All GEMM stages of an epoch (2 per layer, every batch) in ONE cooperative launch:
+// CTAs loop over each stage's tiles, then meet at a grid barrier before the next
+// stage (whose operands the previous stage's epilogues wrote).  TMEM, the mbarrier
+// ring and the per-CTA prologue are paid once per epoch instead of once per stage.
+constexpr int kMaxEpochStages = 8;
+struct EpochParams {
+  TiledParams st[kMaxEpochStages];
+  int32_t nstages;
+  int32_t ring_stages;
+  uint32_t stage_bytes_max;
+  unsigned int* grid_bar;   // zeroed before the launch
+};
+
+static __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int target = (gen + 1u) * nblocks;
+    // release: this CTA's epilogue stores (ordered by the CTA barrier) before the arrival
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  ++gen;
+  __syncthreads();
+  // the next stage reads the previous stage's generic-proxy stores with bulk copies
+  // (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Dynamic tile scheduler: one counter per stage (zeroed with the barrier word); the
+// CTA's next tile is broadcast through shared memory.
+static __device__ __forceinline__ int64_t next_tile(unsigned int* ctr, int64_t* s_tile) {
+  __syncthreads();
+  if (threadIdx.x == 0) *s_tile = (int64_t)atomicAdd(ctr, 1u);
+  __syncthreads();
+  return *s_tile;
+}
+
+template <int TMEM_COLS>
+__global__ void __maxnreg__(112) tc_tiled_epoch_kernel(const __grid_constant__ EpochParams EP) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ unsigned long long sRowSum[128];
+  __shared__ double sRowTerm[128];
+  TileRing R;
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, &done, &tmem_base_s, sRowSum, sRowTerm, EP.ring_stages,
+                         EP.stage_bytes_max);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  R.tmem = tmem_base_s;
+  __shared__ int64_t s_tile;
+  unsigned int gen = 0;
+  for (int st = 0; st < EP.nstages; ++st) {
+    const TiledParams& P = EP.st[st];
+    // first tile static (every CTA has one while tiles last), the rest claimed dynamically
+    for (int64_t tile = blockIdx.x; tile < P.total_ctas;
+         tile = (int64_t)gridDim.x + next_tile(EP.grid_bar + 1 + st, &s_tile))
+      tiled_tile<TMEM_COLS>(P, tile, R);
+    if (st + 1 < EP.nstages) grid_sync(EP.grid_bar, gridDim.x, gen);
+  }
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
 }
 
 // ------------------------------------------------ adjacency block preparation
@@ -657,6 +782,8 @@ static void tiled_attr(size_t bytes) {
   static size_t done = 0;
   if (bytes > done) {
     cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     done = bytes;
   }
 }
@@ -681,29 +808,44 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
   cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS>, P);
 }
 
-extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
-  if (!a || !a->segs || a->nsegs < 1 || a->total_ctas < 1) return QG_ERR_ARG;
-  if (a->bn < 32 || a->bn > 256 || (a->bn & (a->bn - 1))) return QG_ERR_ARG;
-  if (a->mode != QG_GEMM_I32 && a->mode != QG_GEMM_EPILOGUE) return QG_ERR_ARG;
-  if (a->mode == QG_GEMM_EPILOGUE && !a->epi) return QG_ERR_ARG;
-  if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) return QG_ERR_SHAPE;
-  TiledParams P{};
+// qg_tiled_args -> kernel parameters; returns the per-column constant bytes the
+// epilogue stages in shared memory (0 on an argument error, see *rc).
+static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
+  rc = QG_OK;
+  if (!a || !a->segs || a->nsegs < 1 || a->total_ctas < 1) { rc = QG_ERR_ARG; return 0; }
+  if (a->bn < 32 || a->bn > 256 || (a->bn & (a->bn - 1))) { rc = QG_ERR_ARG; return 0; }
+  if (a->mode != QG_GEMM_I32 && a->mode != QG_GEMM_EPILOGUE) { rc = QG_ERR_ARG; return 0; }
+  if (a->mode == QG_GEMM_EPILOGUE && !a->epi) { rc = QG_ERR_ARG; return 0; }
+  if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) { rc = QG_ERR_SHAPE; return 0; }
+  P = TiledParams{};
   P.segs = a->segs; P.nsegs = a->nsegs; P.a_blocks = a->a_blocks; P.b_npad = a->b_npad; P.n = a->n;
   P.bn = a->bn; P.n_tiles = a->n_tiles; P.mode = a->mode; P.out_layout = a->out_layout; P.out_npad = a->out_npad;
   P.log2bn = 5;
   while ((1 << P.log2bn) < P.bn) ++P.log2bn;
   if (a->epi) P.epi = *a->epi;
   P.phase_ns = a->phase_ns;
-  const size_t stage = 16384 + (size_t)P.bn * 128;
+  P.total_ctas = a->total_ctas;
   const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
                       (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
-  const size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
-  // the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's
-  // fp64 epilogue overlaps the other's bulk-copy/MMA main loop); TMEM 2 x 256 cols fits
+  return (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
+}
+
+// the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's fp64
+// epilogue overlaps the other's bulk-copy/MMA main loop); TMEM 2 x 256 cols fits
+static size_t smem_budget() {
   size_t budget = 113 * 1024 - 4096;
   static const char* env_budget = getenv("QG_TILED_SMEM_KB");   // tuning experiments only
   if (env_budget) budget = (size_t)atoi(env_budget) * 1024;
-  P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
+  return budget;
+}
+
+extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
+  TiledParams P;
+  int rc;
+  const size_t cols = tiled_params(a, P, rc);
+  if (rc != QG_OK) return rc;
+  const size_t stage = 16384 + (size_t)P.bn * 128;
+  P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = (unsigned)a->total_ctas;
@@ -714,6 +856,99 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     default: tiled_attr<256>(smem); launch_tiled<256>(P, grid, smem, st); break;
   }
   return tstatus();
+}
+
+template <int COLS>
+static int launch_epoch(EpochParams& EP, size_t smem, int64_t max_tiles, cudaStream_t st) {
+  static size_t attr_done = 0;
+  if (smem > attr_done) {
+    cudaFuncSetAttribute(tc_tiled_epoch_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tc_tiled_epoch_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    attr_done = smem;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_tiled_epoch_kernel<COLS>, kTThreads, smem);
+  static const char* env_per_sm = getenv("QG_EPOCH_PER_SM");    // co-residency experiments
+  if (env_per_sm) per_sm = atoi(env_per_sm);
+  // TMEM: COLS <= 256 columns per CTA, so every co-resident CTA can allocate (512 per SM)
+  per_sm = std::min(per_sm, 512 / COLS);
+  if (per_sm < 1) return QG_ERR_UNSUPPORTED;
+  const int64_t grid = std::min<int64_t>(max_tiles, (int64_t)sms * per_sm);
+  static const bool dbg = getenv("QG_DEBUG_EPOCH") != nullptr;
+  if (dbg) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, tc_tiled_epoch_kernel<COLS>);
+    int per_sm_single = 0;
+    cudaFuncAttributes fb{};
+    cudaFuncGetAttributes(&fb, tc_tiled_kernel<COLS>);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_single, tc_tiled_kernel<COLS>, kTThreads, smem);
+    int smem_sm = 0, smem_blk = 0, p2 = 0, p3 = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, tc_tiled_epoch_kernel<COLS>, kTThreads, 90 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p3, tc_tiled_epoch_kernel<COLS>, kTThreads, 60 * 1024);
+    fprintf(stderr, "params=%zu tiledparams=%zu\n", sizeof(EpochParams), sizeof(TiledParams));
+    fprintf(stderr, "qg_tiled_epoch: COLS=%d smem=%zu per_sm=%d grid=%lld stages=%d ring=%d regs=%d static=%zu "
+            "maxThreads=%d | single-stage kernel regs=%d per_sm=%d | smem/SM=%d smem/blk=%d occ@90K=%d occ@60K=%d\n",
+            COLS, smem, per_sm, (long long)grid, EP.nstages, EP.ring_stages, fa.numRegs, fa.sharedSizeBytes,
+            fa.maxThreadsPerBlock, fb.numRegs, per_sm_single, smem_sm, smem_blk, p2, p3);
+  }
+  cudaMemsetAsync(EP.grid_bar, 0, sizeof(unsigned int) * (1 + kMaxEpochStages), st);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kTThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;          // grid barrier: all CTAs co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, tc_tiled_epoch_kernel<COLS>, EP);
+  if (dbg && err != cudaSuccess) fprintf(stderr, "qg_tiled_epoch launch: %s\n", cudaGetErrorString(err));
+  return tstatus();
+}
+
+extern "C" int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint32_t* grid_bar, void* stream) {
+  if (!stages || nstages < 1 || nstages > kMaxEpochStages || !grid_bar) return QG_ERR_ARG;
+  EpochParams EP{};
+  size_t cols_max = 0;
+  int bn_max = 32;
+  int64_t max_tiles = 1;
+  for (int i = 0; i < nstages; ++i) {
+    int rc;
+    const size_t cols = tiled_params(&stages[i], EP.st[i], rc);
+    if (rc != QG_OK) return rc;
+    cols_max = std::max(cols_max, cols);
+    bn_max = std::max(bn_max, EP.st[i].bn);
+    max_tiles = std::max<int64_t>(max_tiles, EP.st[i].total_ctas);
+  }
+  const size_t stage = 16384 + (size_t)bn_max * 128;
+  const int ring = (int)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols_max) / stage));
+  for (int i = 0; i < nstages; ++i) EP.st[i].stages = ring;
+  EP.nstages = nstages;
+  EP.ring_stages = ring;
+  EP.stage_bytes_max = (uint32_t)stage;
+  EP.grid_bar = grid_bar;
+  const size_t smem = (size_t)ring * stage + cols_max;
+  if (getenv("QG_DEBUG_EPOCH"))
+    for (int i = 0; i < nstages; ++i)
+      fprintf(stderr, "  stage %d: segs=%p nsegs=%d total=%lld bn=%d n_tiles=%d a_blocks=%d mode=%d n=%lld b_npad=%lld\n",
+              i, (const void*)EP.st[i].segs, EP.st[i].nsegs, (long long)EP.st[i].total_ctas, EP.st[i].bn,
+              EP.st[i].n_tiles, EP.st[i].a_blocks, EP.st[i].mode, (long long)EP.st[i].n, (long long)EP.st[i].b_npad);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (bn_max) {
+    case 32: return launch_epoch<32>(EP, smem, max_tiles, st);
+    case 64: return launch_epoch<64>(EP, smem, max_tiles, st);
+    case 128: return launch_epoch<128>(EP, smem, max_tiles, st);
+    default: return launch_epoch<256>(EP, smem, max_tiles, st);
+  }
 }
 
 extern "C" int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,

@@ -109,11 +109,13 @@ class EpochRunner:
         return out
 
     def kernel_launches_per_epoch(self) -> int:
-        """Native (libqgtc_b200) kernels per epoch: 1 grouped entry conversion + 2 grouped
-        fused GEMMs per layer; with rescan, per batch the block expansion (+ the gather
+        """Native (libqgtc_b200) kernels per epoch: 1 grouped entry conversion + the GEMM
+        stages (2 per layer) as one persistent epoch kernel per 8 stages; with rescan, per batch the block expansion (+ the gather
         from dense words unless the blocks were shipped, QGT3)."""
-        from .tiled import blocked
-        per_epoch = 1 + 2 * len(self.model.layers)
+        from . import engine
+        from .tiled import MAX_EPOCH_STAGES, blocked
+        stages = 2 * len(self.model.layers)
+        per_epoch = 1 + (-(-stages // MAX_EPOCH_STAGES) if engine.FUSED_EPOCH else stages)
         if self.rescan:
             per_epoch += sum(2 if getattr(blocked(b.adjacency), "_gather", True) else 1 for b in self.batches)
         return per_epoch

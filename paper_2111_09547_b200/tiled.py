@@ -21,6 +21,7 @@ code caches only when the API asks for them.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -64,6 +65,11 @@ class TiledArgs(ctypes.Structure):
 
 _SIGS_DONE = False
 
+# When a list, launch() records stage arguments instead of launching (engine's fused
+# epoch); flush_epoch() then issues them as qg_tiled_epoch launches.
+EPOCH = None
+MAX_EPOCH_STAGES = 8
+
 
 def _lib():
     global _SIGS_DONE
@@ -78,6 +84,8 @@ def _lib():
         L.qg_codes_to_tiles.restype = ctypes.c_int
         L.qg_tiles_to_codes.argtypes = [vp, i64, i64, i32, i64, vp, i64, vp]
         L.qg_tiles_to_codes.restype = ctypes.c_int
+        L.qg_tiled_epoch.argtypes = [ctypes.POINTER(TiledArgs), ctypes.c_int32, vp, vp]
+        L.qg_tiled_epoch.restype = ctypes.c_int
         _SIGS_DONE = True
     return L
 
@@ -270,6 +278,19 @@ class SegTable:
         self.n = n
 
 
+def sm_count() -> int:
+    return torch.cuda.get_device_properties(N.device()).multi_processor_count
+
+
+def choose_bn_fused(npad: int, row_blocks_total: int, cap: int) -> int:
+    """Persistent epoch kernel: at most ``cap`` (= SMs) tiles per stage, so every CTA
+    owns <= 1 tile per stage; the smallest N tile that keeps that maximises parallelism."""
+    bn = min(256, npad)
+    while bn > 32 and row_blocks_total * (npad // (bn // 2)) <= cap:
+        bn //= 2
+    return bn
+
+
 def choose_bn(npad: int, row_blocks_total: int) -> int:
     bn = min(256, npad)
     while bn > 32 and row_blocks_total * (npad // bn) < 148:
@@ -281,7 +302,7 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
            keep: list, work: float = 0.0):
     """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m)."""
     rbs = [-(-s.m // TILE) for s in segs]
-    bn = choose_bn(b_npad, sum(rbs))
+    bn = choose_bn(b_npad, sum(rbs)) if EPOCH is None else choose_bn_fused(b_npad, sum(rbs), sm_count())
     n_tiles = b_npad // bn
     begin = 0
     for s, r in zip(segs, rbs):
@@ -296,6 +317,11 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     if epi_struct is not None:
         args.epi = ctypes.pointer(epi_struct)
     if not begin:
+        return
+    if EPOCH is not None:
+        # deferred: flush_epoch() launches every recorded stage in ONE persistent kernel
+        EPOCH.append((args, work, table))
+        keep.append(args)
         return
     from . import bitgemm
     if bitgemm.PHASE_HOOK is not None:
@@ -392,9 +418,34 @@ def entry_tiles(stacks, side: str, want_row_sums: bool, keep: list):
         begin += units if rows * cols else 0
         segs.append(seg)
         outs.append((tiles, pitch, rs))
+        keep.extend([tiles, rs])          # read later by a deferred (fused-epoch) launch
     if begin:
         table = SegTable(segs, EntrySeg)
         keep.append(table)
         N.check(N.lib().qg_entry_tiles(table.dev.data_ptr(), len(segs), stacks[0].bits, int(right), begin,
                                        N.stream()), "qg_entry_tiles")
     return outs
+
+
+def flush_epoch(stages: list, keep: list) -> None:
+    """Launch recorded stages as persistent epoch kernels (<= MAX_EPOCH_STAGES per launch):
+    one cooperative grid, a grid barrier between stages (include/qgtc_b200.h qg_tiled_epoch)."""
+    from . import bitgemm
+    for i in range(0, len(stages), MAX_EPOCH_STAGES):
+        chunk = stages[i:i + MAX_EPOCH_STAGES]
+        arr = (TiledArgs * len(chunk))(*[c[0] for c in chunk])
+        bar = N.alloc(1 + MAX_EPOCH_STAGES, torch.int32, "empty")   # zeroed by the call (memset node)
+        keep.extend([arr, bar])
+        if bitgemm.PHASE_HOOK is not None:
+            for a, (_, work, _) in zip(arr, chunk):
+                stamps = torch.zeros((a.total_ctas, 8), dtype=torch.int64, device=N.device())
+                a.phase_ns = stamps.data_ptr()
+                bitgemm.PHASE_HOOK.append((stamps, work))
+        if os.environ.get("QG_DEBUG_EPOCH"):
+            for a, (_, _, table) in zip(arr, chunk):
+                raw = table.dev.cpu().numpy().tobytes()
+                segs = (TSeg * a.nsegs).from_buffer_copy(raw)
+                print("  py stage segs=%x nsegs=%d total=%d bn=%d | seg0 a=%x b=%x m=%d r128=%d cta_begin=%d k=%d"
+                      % (a.segs, a.nsegs, a.total_ctas, a.bn, segs[0].a or 0, segs[0].b or 0, segs[0].m, segs[0].r128,
+                         segs[0].cta_begin, segs[0].k_tiles), flush=True)
+        N.check(_lib().qg_tiled_epoch(arr, len(chunk), bar.data_ptr(), N.stream()), "qg_tiled_epoch")

@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+QG_DEBUG_EPOCH=1 timeout 300 python tools/cold_step.py C2 4 > gpurun_out/cold.log 2>&1
+timeout 300 python tools/phase_tiled.py C2 4 > gpurun_out/phase_c2.log 2>&1
+timeout 300 python tools/run_config.py C3 > gpurun_out/c3.log 2>&1

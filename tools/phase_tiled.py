@@ -23,6 +23,7 @@ bitgemm.PHASE_HOOK = rec
 engine.model_forward_group(batches, model)
 torch.cuda.synchronize()
 bitgemm.PHASE_HOOK = None
+prev_end = None
 for i, (st, _) in enumerate(rec):
     s = st.cpu().numpy().astype(np.float64)
     s = s[s[:, 0] > 0]
@@ -31,4 +32,6 @@ for i, (st, _) in enumerate(rec):
     print(f"launch {i}: ctas={len(s)} span={(s[:, 5].max() - t0) / 1e3:.2f}us  last-start={(s[:, 0].max() - t0) / 1e3:.2f}us"
           f"  per-CTA mean(max) us: setup {d[:, 0].mean():.2f}({d[:, 0].max():.2f})"
           f"  first-tile {d[:, 1].mean():.2f}({d[:, 1].max():.2f})  mainloop {d[:, 2].mean():.2f}({d[:, 2].max():.2f})"
-          f"  epilogue {d[:, 3].mean():.2f}({d[:, 3].max():.2f})  teardown {d[:, 4].mean():.2f}({d[:, 4].max():.2f})")
+          f"  epilogue {d[:, 3].mean():.2f}({d[:, 3].max():.2f})  teardown {d[:, 4].mean():.2f}({d[:, 4].max():.2f})"
+          + (f"  gap-from-prev {(t0 - prev_end) / 1e3:.2f}us" if prev_end is not None else ""))
+    prev_end = s[:, 5].max()
