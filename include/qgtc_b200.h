@@ -268,6 +268,11 @@ typedef struct {
   int64_t out_npad;            /* right-tiled output: padded N                       */
   const qg_epilogue* epi;      /* shared epilogue scalars / per-column vectors       */
   int64_t* phase_ns;           /* optional [total_ctas][8] %globaltimer stamps (tools/) */
+  int32_t a_bits;              /* a_blocks only: 1 = segs[].a holds PACKED blocks (2 KB:
+                                  128 rows x 4 words, the column-wise bits of the block),
+                                  expanded to the UMMA byte layout in shared memory;
+                                  0 = pre-expanded 16 KB byte blocks                    */
+  int32_t pad2_;
 } qg_tiled_args;
 
 /* Warp-specialised tiled bit-GEMM (cp.async.bulk producer, single-thread
@@ -285,8 +290,9 @@ int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint32_t* grid_
 
 /* Gather the non-zero 128x128 blocks (blk_rb/blk_kt) of a column-wise 1-bit matrix
  * into `packed` (2 KB each; skipped when a_words == NULL and `packed` is already
- * filled, e.g. shipped by the QGT2 tile-sparse wire format), expand them to 16 KB
- * UMMA byte blocks and accumulate row degrees (graph.py:292-295; degrees zeroed). */
+ * filled, e.g. shipped by the QGT3 tile-sparse wire format), expand them to 16 KB
+ * UMMA byte blocks (skipped when bytes == NULL: qg_tiled_gemm a_bits mode expands in
+ * shared memory) and accumulate row degrees (graph.py:292-295; degrees zeroed). */
 int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,
                      const int32_t* blk_rb, const int32_t* blk_kt, int64_t nblocks, uint32_t* packed,
                      uint8_t* bytes, int64_t* degrees, void* stream);

@@ -34,6 +34,7 @@ struct TiledParams {
   qg_epilogue epi;          // shared scalars + per-column vectors (per-row pointers come from segs)
   int64_t* phase_ns;        // optional per-tile %globaltimer stamps (tools/phase_tiled.py)
   int64_t total_ctas;       // work items (segment, row block, N tile) of this stage
+  int32_t a_bits;           // 1: adjacency blocks are shipped packed (2 KB) and expanded in smem
 };
 
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
@@ -296,6 +297,7 @@ struct TileRing {
   uint64_t* full;
   uint64_t* empty;
   uint64_t* done;
+  uint64_t* aready;           // a_bits: expanded A operand of a ring slot is ready
   unsigned long long* sRowSum;
   double* sRowTerm;
   uint32_t tmem;
@@ -324,9 +326,11 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const int nt = (int)(local % P.n_tiles);
   const int64_t n0 = (int64_t)nt * bn;
 
+  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B][a_bits: 2 KB packed bit block]
   const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u;
+  const bool abits = P.a_blocks && P.a_bits;
   uint8_t* stage0 = R.stage0;
-  const uint32_t stage_bytes = a_bytes + b_bytes;
+  const uint32_t stage_bytes = abits ? ((a_bytes + b_bytes + 2048u + 1023u) & ~1023u) : a_bytes + b_bytes;
   double* sCol = R.sCol;
   uint64_t* full = R.full;
   uint64_t* empty = R.empty;
@@ -354,11 +358,18 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
       int kt;
       const uint8_t* asrc;
-      if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
-      else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
       uint8_t* dst = stage0 + (size_t)s * stage_bytes;
-      mbar_expect_tx(&full[s], a_bytes + b_bytes);
-      bulk_g2s(dst, asrc, a_bytes, &full[s]);
+      if (abits) {
+        // 2 KB packed block -> staging; the expander warps build the 16 KB operand
+        kt = G.blk_kt[kbase + it];
+        mbar_expect_tx(&full[s], 2048u + b_bytes);
+        bulk_g2s(dst + a_bytes + b_bytes, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
+      } else {
+        if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
+        else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
+        mbar_expect_tx(&full[s], a_bytes + b_bytes);
+        bulk_g2s(dst, asrc, a_bytes, &full[s]);
+      }
       bulk_g2s(dst + a_bytes, bbase + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
@@ -367,7 +378,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     for (int it = 0; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
-      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+      mbar_wait(smem_u32(abits ? &R.aready[s] : &full[s]), (g / S) & 1);
       if (it == 0) tstamp(P, tile, 2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
@@ -423,6 +434,31 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
           sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
         }
       }
+    }
+  }
+  if (abits && warp >= 2) {
+    // expander warps: packed 128x128 bit block -> UMMA K-major 0/1 bytes (16 KB) per
+    // ring slot; thread -> (row, 16-bit K-core) = one 16-byte store
+    const int et = tid - 64;
+    for (int it = 0; it < nk; ++it) {
+      const uint32_t g = it0 + (uint32_t)it;
+      const int s = (int)(g % (uint32_t)S);
+      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+      uint8_t* slot = stage0 + (size_t)s * stage_bytes;
+      const uint32_t* bits = reinterpret_cast<const uint32_t*>(slot + a_bytes + b_bytes);
+      // u = (row/8, K-core, row%8) is exactly the UMMA core-matrix order: the 16-byte
+      // store for unit u lands at u * 16 (consecutive lanes -> consecutive addresses)
+      for (int u = et; u < 1024; u += kTThreads - 64) {
+        const int r = ((u >> 6) << 3) | (u & 7), c = (u >> 3) & 7;
+        const uint32_t x = bits[r * 4 + (c >> 1)] >> ((c & 1) * 16);
+        *reinterpret_cast<uint4*>(slot + u * 16) =
+            make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu), expand_nibble((x >> 8) & 0xFu),
+                       expand_nibble((x >> 12) & 0xFu));
+      }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.aready[s]);
     }
   }
   __syncwarp();
@@ -512,7 +548,8 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
 // CTA setup shared by both kernels: TMEM allocation, ring barriers.
 template <int TMEM_COLS>
 __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t* full, uint64_t* empty,
-                                            uint64_t* done, uint32_t* tmem_base_s, unsigned long long* sRowSum,
+                                            uint64_t* aready, uint64_t* done, uint32_t* tmem_base_s,
+                                            unsigned long long* sRowSum,
                                             double* sRowTerm, int S, uint32_t stage_bytes_max) {
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) {
@@ -521,7 +558,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); mbar_init(&aready[i], 6); }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -530,6 +567,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.full = full;
   R.empty = empty;
   R.done = done;
+  R.aready = aready;
   R.sRowSum = sRowSum;
   R.sRowTerm = sRowTerm;
   R.S = S;
@@ -540,7 +578,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
 template <int TMEM_COLS>
 __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[128];
   __shared__ double sRowTerm[128];
@@ -548,8 +586,9 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   // schedule arrays and the segment table are static for the lifetime of a launch
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
-  tiled_setup<TMEM_COLS>(R, smem, full, empty, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
-                         16384u + (uint32_t)P.bn * 128u);
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
+                         P.a_bits ? ((16384u + (uint32_t)P.bn * 128u + 2048u + 1023u) & ~1023u)
+                                  : 16384u + (uint32_t)P.bn * 128u);
   // everything below may read the predecessor grid's outputs (activations, row sums,
   // per-forward epilogue vectors)
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -606,12 +645,12 @@ static __device__ __forceinline__ int64_t next_tile(unsigned int* ctr, int64_t* 
 template <int TMEM_COLS>
 __global__ void __maxnreg__(112) tc_tiled_epoch_kernel(const __grid_constant__ EpochParams EP) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[128];
   __shared__ double sRowTerm[128];
   TileRing R;
-  tiled_setup<TMEM_COLS>(R, smem, full, empty, &done, &tmem_base_s, sRowSum, sRowTerm, EP.ring_stages,
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, EP.ring_stages,
                          EP.stage_bytes_max);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -663,14 +702,16 @@ __global__ void __launch_bounds__(256) block_expand_kernel(const uint32_t* __res
   const int t = threadIdx.x, r = t & 127, h = t >> 7;
   const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(packed) + b * 128 + r);
   const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-  uint8_t* blk = bytes + b * 16384;
+  if (bytes) {                                // NULL: degrees only (blocks expanded in the GEMM)
+    uint8_t* blk = bytes + b * 16384;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int c = h + 2 * i;                   // K-core: bits 16c..16c+15 = word c>>1, half c&1
-    const uint32_t x = w[c >> 1] >> ((c & 1) * 16);
-    const uint4 o = make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu),
-                               expand_nibble((x >> 8) & 0xFu), expand_nibble((x >> 12) & 0xFu));
-    *reinterpret_cast<uint4*>(blk + umma_off(r, c)) = o;
+    for (int i = 0; i < 4; ++i) {
+      const int c = h + 2 * i;                 // K-core: bits 16c..16c+15 = word c>>1, half c&1
+      const uint32_t x = w[c >> 1] >> ((c & 1) * 16);
+      const uint4 o = make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu),
+                                 expand_nibble((x >> 8) & 0xFu), expand_nibble((x >> 12) & 0xFu));
+      *reinterpret_cast<uint4*>(blk + umma_off(r, c)) = o;
+    }
   }
   if (degrees && h == 0) {
     const int64_t row = (int64_t)blk_rb[b] * 128 + r;
@@ -825,6 +866,7 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   if (a->epi) P.epi = *a->epi;
   P.phase_ns = a->phase_ns;
   P.total_ctas = a->total_ctas;
+  P.a_bits = a->a_blocks ? a->a_bits : 0;
   const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
                       (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
   return (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
@@ -844,7 +886,8 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   int rc;
   const size_t cols = tiled_params(a, P, rc);
   if (rc != QG_OK) return rc;
-  const size_t stage = 16384 + (size_t)P.bn * 128;
+  const size_t stage = P.a_bits ? ((16384 + (size_t)P.bn * 128 + 2048 + 1023) & ~(size_t)1023)
+                                : 16384 + (size_t)P.bn * 128;
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;
@@ -929,7 +972,7 @@ extern "C" int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint
     bn_max = std::max(bn_max, EP.st[i].bn);
     max_tiles = std::max<int64_t>(max_tiles, EP.st[i].total_ctas);
   }
-  const size_t stage = 16384 + (size_t)bn_max * 128;
+  const size_t stage = (16384 + (size_t)bn_max * 128 + 2048 + 1023) & ~(size_t)1023;   // + packed bit block
   const int ring = (int)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols_max) / stage));
   for (int i = 0; i < nstages; ++i) EP.st[i].stages = ring;
   EP.nstages = nstages;
@@ -954,7 +997,7 @@ extern "C" int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint
 extern "C" int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,
                                 const int32_t* blk_rb, const int32_t* blk_kt, int64_t nblocks, uint32_t* packed,
                                 uint8_t* bytes, int64_t* degrees, void* stream) {
-  if (nblocks < 0 || (nblocks && (!blk_rb || !bytes || !packed))) return QG_ERR_ARG;
+  if (nblocks < 0 || (nblocks && (!blk_rb || !packed))) return QG_ERR_ARG;
   if (nblocks == 0) return QG_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (a_words)   // gather from the dense packed matrix; otherwise `packed` is already filled

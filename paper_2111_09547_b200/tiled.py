@@ -60,7 +60,8 @@ class TiledArgs(ctypes.Structure):
                 ("total_ctas", ctypes.c_int64), ("b_npad", ctypes.c_int64), ("n", ctypes.c_int64),
                 ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
-                ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p)]
+                ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p), ("a_bits", ctypes.c_int32),
+                ("pad2_", ctypes.c_int32)]
 
 
 _SIGS_DONE = False
@@ -69,6 +70,14 @@ _SIGS_DONE = False
 # epoch); flush_epoch() then issues them as qg_tiled_epoch launches.
 EPOCH = None
 MAX_EPOCH_STAGES = 8
+
+# QG_A_BITS=1: adjacency blocks reach the GEMM packed (2 KB per 128x128 block) and are
+# expanded to the tensor-core byte layout in shared memory by otherwise idle warps: 8x
+# less A traffic and no 16 KB-per-block copy in HBM (C4: 12.1 vs 16.5 GB).  Off by
+# default: the copy -> expand -> MMA chain measured slower than streaming pre-expanded
+# blocks on B200 (C2 65 vs 55 us, C4 7.9 vs 7.3 ms, C5-16k 55% vs 69% of peak;
+# profiles/r01g_abits_ab.txt) -- the main loop is latency-, not L2-bandwidth-bound.
+A_BITS = os.environ.get("QG_A_BITS", "0") == "1"
 
 
 def _lib():
@@ -112,7 +121,7 @@ class BlockedAdjacency:
         self.blk_kt = torch.from_numpy(kt_of.astype(np.int32)).to(dev)
         self.blk_rb = torch.from_numpy(rb_of.astype(np.int32)).to(dev)
         self.packed = torch.empty((max(self.nblocks, 1), 128, 4), dtype=torch.int32, device=dev)
-        self.bytes = torch.empty((max(self.nblocks, 1), 16384), dtype=torch.uint8, device=dev)
+        self._bytes = None
         self.degrees = torch.zeros(a.logical_rows, dtype=torch.int64, device=dev)
         self.m = a.logical_rows
         self.r128 = pad128(a.logical_rows)
@@ -131,7 +140,7 @@ class BlockedAdjacency:
         dev = blk_count.device
         self.blk_count, self.blk_base, self.blk_kt, self.blk_rb = blk_count, blk_base, blk_kt, blk_rb
         self.packed = packed if nblocks else torch.zeros((1, 128, 4), dtype=torch.int32, device=dev)
-        self.bytes = torch.empty((max(self.nblocks, 1), 16384), dtype=torch.uint8, device=dev)
+        self._bytes = None
         self.degrees = torch.zeros(int(rows), dtype=torch.int64, device=dev)
         self.m = int(rows)
         self.r128 = pad128(int(rows))
@@ -141,6 +150,18 @@ class BlockedAdjacency:
         self.refresh()
         return self
 
+    @property
+    def bytes(self) -> torch.Tensor:
+        """Pre-expanded 16 KB UMMA byte blocks (only when A_BITS is off)."""
+        if self._bytes is None:
+            self._bytes = torch.empty((max(self.nblocks, 1), 16384), dtype=torch.uint8, device=self.packed.device)
+            self.refresh()
+        return self._bytes
+
+    def operand(self) -> tuple:
+        """(device pointer, a_bits) of the left operand the tiled GEMM reads."""
+        return (self.packed.data_ptr(), 1) if A_BITS else (self.bytes.data_ptr(), 0)
+
     def refresh(self):
         """Re-gather + re-expand the blocks (and degrees) from the adjacency's current
         words with the same schedule -- device only, capturable in a CUDA graph."""
@@ -149,12 +170,12 @@ class BlockedAdjacency:
         if self.nblocks:
             if not getattr(self, "_gather", True):      # shipped blocks: expand only
                 N.check(_lib().qg_block_prepare(None, self.m, 0, 0, N.ptr(self.blk_rb), N.ptr(self.blk_kt),
-                                                self.nblocks, N.ptr(self.packed), N.ptr(self.bytes),
+                                                self.nblocks, N.ptr(self.packed), N.ptr(self._bytes),
                                                 N.ptr(self.degrees), N.stream()), "qg_block_prepare")
                 return
             N.check(_lib().qg_block_prepare(N.ptr(a.dwords), a.logical_rows, a.padded_rows, a.padded_cols,
                                             N.ptr(self.blk_rb), N.ptr(self.blk_kt), self.nblocks, N.ptr(self.packed),
-                                            N.ptr(self.bytes), N.ptr(self.degrees), N.stream()), "qg_block_prepare")
+                                            N.ptr(self._bytes), N.ptr(self.degrees), N.stream()), "qg_block_prepare")
 
 
 def blocked(a) -> BlockedAdjacency:
@@ -299,7 +320,7 @@ def choose_bn(npad: int, row_blocks_total: int) -> int:
 
 
 def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: int, out_npad: int, epi_struct,
-           keep: list, work: float = 0.0):
+           keep: list, work: float = 0.0, a_bits: bool = False):
     """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m)."""
     rbs = [-(-s.m // TILE) for s in segs]
     bn = choose_bn(b_npad, sum(rbs)) if EPOCH is None else choose_bn_fused(b_npad, sum(rbs), sm_count())
@@ -314,6 +335,7 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     args.segs, args.nsegs, args.a_blocks, args.total_ctas = table.dev.data_ptr(), table.n, int(a_blocks), begin
     args.b_npad, args.n, args.bn, args.n_tiles = b_npad, n, bn, n_tiles
     args.mode, args.out_layout, args.out_npad = mode, out_layout, out_npad
+    args.a_bits = int(bool(a_blocks and a_bits))
     if epi_struct is not None:
         args.epi = ctypes.pointer(epi_struct)
     if not begin:
@@ -369,14 +391,15 @@ def bmm_reduced(a, x, *, out: torch.Tensor | None = None) -> torch.Tensor:
         return out
     xt, _ = operand_tiles(x, "right")
     seg = TSeg()
-    seg.a, seg.b, seg.m, seg.r128 = blk.bytes.data_ptr(), xt.data_ptr(), m, blk.r128
+    a_ptr, a_bits = blk.operand()
+    seg.a, seg.b, seg.m, seg.r128 = a_ptr, xt.data_ptr(), m, blk.r128
     seg.blk_count, seg.blk_base, seg.blk_kt = (blk.blk_count.data_ptr(), blk.blk_base.data_ptr(),
                                                blk.blk_kt.data_ptr())
     seg.out_i32 = out.data_ptr()
     keep = []
     # row blocks with no non-zero K tile are written as zeros by the kernel (nk = 0)
     launch([seg], a_blocks=True, b_npad=npad_of(n), n=n, mode=N.GEMM_I32, out_layout=0, out_npad=0,
-           epi_struct=None, keep=keep, work=2.0 * 1024 * (-(-n // 8) * 8) * blk.nz8)
+           epi_struct=None, keep=keep, work=2.0 * 1024 * (-(-n // 8) * 8) * blk.nz8, a_bits=a_bits)
     out._qg_keep = keep           # the segment table must outlive the (async) launch
     return out
 
