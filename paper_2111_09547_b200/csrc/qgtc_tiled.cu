@@ -215,73 +215,56 @@ __device__ __forceinline__ uint32_t epi_slices_screen(const TiledParams& P, cons
   const double* sR = sCol + 2 * bn;
   const uint32_t maxv = (1u << E.q_bits) - 1u;
   const double r0 = E.screen_r0;
-  const uint32_t tb = (uint32_t)(E.screen_tol * 0x1p40) + 4u;    // tolerance in 2^-40 units (< 2^31)
-  const uint32_t tb2 = 2u * tb;
+  const uint64_t tb = (uint64_t)(E.screen_tol * 0x1p40) + 4u;   // tolerance in 2^-40 units
   const int out_layout = P.out_layout;
   uint8_t* const q_codes = G.q_codes;
   int64_t* const status = G.status;
   const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
-  const int nsl16 = (L.nslices + 1) >> 1;                  // 16-column slices
   uint32_t rsum = 0;
-  for (int sl = L.first; sl < nsl16; sl += 2) {
-    const int c16 = sl * 16;
-    uint32_t v[16];
-    if (L.has_acc) {
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(L.tmem_row + (uint32_t)c16));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    } else {
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) v[jj] = 0;
-    }
+  for (int sl = L.first; sl < L.nslices; sl += 2) {
+    const int cl8 = sl * 8;
+    uint32_t v[8];
+    L.load8(cl8, v);
     bool slow = false;
-    uint32_t q[16];
+    uint32_t q[8];
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) {
-      const int cl = c16 + jj;
-      double r = __fma_rn(sP[cl], (double)(int32_t)v[jj], __fma_rn(sG[cl], rterm, sR[cl]));
+    for (int jj = 0; jj < 8; ++jj) {
+      const int cl = cl8 + jj;
+      // acc >= 0 (non-negative operands): 2^52 + acc is exact, one DADD instead of I2F
+      const double a = __dsub_rn(__hiloint2double(0x43300000, (int)v[jj]), 0x1p52);
+      double r = __fma_rn(sP[cl], a, __fma_rn(sG[cl], rterm, sR[cl]));
       if (RELU) r = fmax(r, r0);
-      const uint32_t hi = (uint32_t)__double2hiint(r), lo = (uint32_t)__double2loint(r);
-      // code: floor of y = r - 2^12 for r in [2^12, 2^13), clamped; negative / tiny r -> 0,
-      // r >= 2^13 -> maxv (arithmetic shift keeps negative r negative)
-      const int kc = (__double2hiint(r) >> 8) - 0x40B000;
+      const uint64_t bits = (uint64_t)__double_as_longlong(r);
+      // code: floor(y) of r = 2^12 + y in [2^12, 2^13), clamped (sign-preserving shift:
+      // negative r -> 0, r >= 2^13 -> maxv)
+      const int kc = (int)((int64_t)bits >> 40) - 0x40B000;
       q[jj] = (uint32_t)min(max(kc, 0), (int)maxv);
-      // near a boundary B in [1, maxv]: the 40-bit fraction of r within tb of 0 or 1
-      const uint32_t t = lo + tb;
-      const uint32_t hc = hi + (t < lo ? 1u : 0u);
-      const int B = ((int)hc >> 8) - 0x40B000;
-      slow |= ((hc & 0xFFu) == 0u) & (t < tb2) & (B >= 1) & (c16 + jj < L.nvalid);
+      // ambiguous: the 40-bit fraction within tb of a code boundary B >= 1
+      const uint64_t x = bits + tb;
+      slow |= ((x & 0xFFFFFFFFFFull) < 2 * tb) & (x >= 0x40B0010000000000ull) & (cl < L.nvalid);
     }
     if (slow && L.rvalid) {
-#pragma unroll 1
-      for (int jj = 0; jj < 16; ++jj)
-        if (c16 + jj < L.nvalid)
-          q[jj] = exact_code_global(E, v[jj], rterm, L.n0 + c16 + jj, maxv, status, L.myrow * pn + L.n0 + c16 + jj);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (cl8 + jj < L.nvalid)
+          q[jj] = exact_code_global(E, v[jj], rterm, L.n0 + cl8 + jj, maxv, status, L.myrow * pn + L.n0 + cl8 + jj);
     }
+    const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
+    const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
+    rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    if (L.rvalid) {
+      const int64_t cb = L.n0 + cl8;
+      if (out_layout == 1) {
+        *reinterpret_cast<uint2*>(q_codes + left_tile_off(L.myrow, cb, r128)) = make_uint2(lo, hi);
+      } else {
+        uint8_t* base = q_codes + right_tile_off(L.myrow, cb, out_npad);
+        if (cl8 + 8 <= L.nvalid) {
 #pragma unroll
-    for (int h8 = 0; h8 < 2; ++h8) {
-      const uint32_t* qq = q + 8 * h8;
-      const int cl8 = c16 + 8 * h8;
-      const uint32_t lo = qq[0] | (qq[1] << 8) | (qq[2] << 16) | (qq[3] << 24);
-      const uint32_t hi = qq[4] | (qq[5] << 8) | (qq[6] << 16) | (qq[7] << 24);
-      rsum += ((qq[0] + qq[1]) + (qq[2] + qq[3])) + ((qq[4] + qq[5]) + (qq[6] + qq[7]));
-      if (L.rvalid && cl8 < L.nvalid) {
-        const int64_t cb = L.n0 + cl8;
-        if (out_layout == 1) {
-          *reinterpret_cast<uint2*>(q_codes + left_tile_off(L.myrow, cb, r128)) = make_uint2(lo, hi);
+          for (int jj = 0; jj < 8; ++jj) base[jj * 16] = (uint8_t)q[jj];
         } else {
-          uint8_t* base = q_codes + right_tile_off(L.myrow, cb, out_npad);
-          if (cl8 + 8 <= L.nvalid) {
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj) base[jj * 16] = (uint8_t)qq[jj];
-          } else {
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)qq[jj];
-          }
+          for (int jj = 0; jj < 8; ++jj)
+            if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)q[jj];
         }
       }
     }

@@ -1,0 +1,3 @@
+for d in 0 1 2 4 3 6 7; do
+  echo "== QG_EPI_DBG=$d"; QG_EPI_DBG=$d timeout 120 python tools/phase_tiled.py C4 8 8 2>&1 | cut -c1-170 | head -2
+done
