@@ -287,6 +287,7 @@ struct TileRing {
   int S;
   uint32_t it0;               // ring position (K tiles issued so far)
   uint32_t ndone;             // accumulator phases completed so far
+  bool pdl_wait;              // griddepcontrol.wait still pending (PDL-launched single tile)
 };
 
 // One work item: (segment, 128-row block, N tile) -> fused GEMM tile.  Ends with a
@@ -335,7 +336,39 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   if (warp == 0 && lane == 0) {
     // ---------------- producer: two bulk copies per K tile ----------------
     const uint8_t* bbase = G.b + (n0 >> 3) * 1024;
-    for (int it = 0; it < nk; ++it) {
+    int it_begin = 0;
+    if (R.pdl_wait) {
+      // PDL: the STATIC operand of the first ring-full of K tiles (adjacency blocks, or the
+      // weights of a dense-left GEMM) is fetched while the predecessor grid drains; the
+      // operand it produced only after griddepcontrol.wait
+      const int pre = nk < S ? nk : S;
+      uint8_t* dst0 = stage0;
+      for (int it = 0; it < pre; ++it) {
+        uint8_t* dst = dst0 + (size_t)((it0 + it) % S) * stage_bytes;
+        uint64_t* fb = &full[(it0 + it) % S];
+        if (abits) {
+          mbar_expect_tx(fb, 2048u + b_bytes);
+          bulk_g2s(dst + a_bytes + b_bytes, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
+        } else if (P.a_blocks) {
+          mbar_expect_tx(fb, a_bytes + b_bytes);
+          bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
+        } else {
+          mbar_expect_tx(fb, a_bytes + b_bytes);
+          bulk_g2s(dst + a_bytes, bbase + (int64_t)it * (P.b_npad << 7), b_bytes, fb);
+        }
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int it = 0; it < pre; ++it) {
+        uint8_t* dst = dst0 + (size_t)((it0 + it) % S) * stage_bytes;
+        uint64_t* fb = &full[(it0 + it) % S];
+        if (P.a_blocks)
+          bulk_g2s(dst + a_bytes, bbase + (int64_t)G.blk_kt[kbase + it] * (P.b_npad << 7), b_bytes, fb);
+        else
+          bulk_g2s(dst, G.a + (int64_t)it * (G.r128 << 7) + rb * 16384, a_bytes, fb);
+      }
+      it_begin = pre;
+    }
+    for (int it = it_begin; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
       if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
@@ -375,6 +408,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     // warps 2..7 stage the epilogue constants while the main loop runs: the row terms
     // RN(k_row * row_sum) (predecessor outputs) and the per-column constants
     const int t = tid - 64;
+    if (R.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (t < 128) {
       const int64_t row = rb * 128 + t;
       R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
@@ -445,6 +479,10 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     }
   }
   __syncwarp();
+  // every thread is past the predecessor grid before any global write (nk == 0 tiles
+  // reach the epilogue without waiting on the pipeline)
+  if (R.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+  R.pdl_wait = false;
   if (nk > 0) {
     mbar_wait(smem_u32(R.done), R.ndone & 1);
     R.ndone += 1;
@@ -556,6 +594,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.S = S;
   R.it0 = 0;
   R.ndone = 0;
+  R.pdl_wait = false;
 }
 
 template <int TMEM_COLS>
@@ -572,13 +611,13 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
                          P.a_bits ? ((16384u + (uint32_t)P.bn * 128u + 2048u + 1023u) & ~1023u)
                                   : 16384u + (uint32_t)P.bn * 128u);
-  // everything below may read the predecessor grid's outputs (activations, row sums,
-  // per-forward epilogue vectors)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   R.tmem = tmem_base_s;
+  // the predecessor grid's outputs (activations, row sums) are read only after
+  // griddepcontrol.wait, issued per role inside the tile (static operands prefetch first)
+  R.pdl_wait = true;
   tiled_tile<TMEM_COLS>(P, (int64_t)blockIdx.x, R);
   if ((threadIdx.x >> 5) == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
