@@ -297,6 +297,19 @@ int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows,
                      const int32_t* blk_rb, const int32_t* blk_kt, int64_t nblocks, uint32_t* packed,
                      uint8_t* bytes, int64_t* degrees, void* stream);
 
+/* qg_block_prepare over many batches in ONE launch (shipped blocks, no gather): the
+ * per-epoch block expansion + degrees of the multi-batch end-to-end path. */
+typedef struct {
+  const uint32_t* packed;      /* [nblocks][128][4] packed blocks                     */
+  const int32_t* blk_rb;       /* row block of each block                            */
+  uint8_t* bytes;              /* 16 KB UMMA byte blocks out, or NULL (degrees only)  */
+  int64_t* degrees;            /* [rows] ACCUMULATED (caller zeroes), or NULL         */
+  int64_t rows;
+  int64_t block_begin;         /* first global block index of this batch             */
+} qg_block_seg;
+
+int qg_block_prepare_grouped(const qg_block_seg* segs, int32_t nsegs, int64_t total_blocks, void* stream);
+
 /* Plain row-major u8 codes [rows][ld] <-> left (right = 0, pitch = pad128(rows)) or
  * right (right = 1, pitch = npad) tiled layout. */
 int qg_codes_to_tiles(const uint8_t* codes, int64_t rows, int64_t cols, int64_t ld, int right, int64_t pitch,

@@ -33,7 +33,8 @@ EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes"
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
            "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes",
            "qg_test_requant", "qg_tiled_gemm", "qg_block_prepare", "qg_codes_to_tiles",
-           "qg_tiles_to_codes", "qg_entry_tiles", "qg_tiled_epoch")
+           "qg_tiles_to_codes", "qg_entry_tiles", "qg_tiled_epoch",
+           "qg_block_prepare_grouped")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -103,6 +104,7 @@ def lib() -> ctypes.CDLL:
             "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp],
                                    ctypes.c_int),
             "qg_entry_tiles": ([_vp, _i32, _i32, _i32, _i64, _vp], ctypes.c_int),
+            "qg_block_prepare_grouped": ([_vp, _i32, _i64, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)

@@ -798,4 +798,4 @@ extern "C" int qg_test_requant(const double* x, int64_t n, double amin, double s
   return launch_status_g();
 }
 
-extern "C" int qg_version(void) { return 22; }  // == number of exported entry points
+extern "C" int qg_version(void) { return 23; }  // == number of exported entry points

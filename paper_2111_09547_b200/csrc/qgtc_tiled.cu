@@ -742,6 +742,40 @@ __global__ void __launch_bounds__(256) block_expand_kernel(const uint32_t* __res
   }
 }
 
+// Grouped variant over many batches (one launch per epoch on the e2e path): block ->
+// segment by binary search on block_begin, then the same expansion + degrees.
+__global__ void __launch_bounds__(256) block_expand_grouped_kernel(const qg_block_seg* __restrict__ segs, int nsegs,
+                                                                   int64_t total_blocks) {
+  const int64_t gb = blockIdx.x;
+  if (gb >= total_blocks) return;
+  int lo = 0, hi = nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].block_begin <= gb) lo = mid; else hi = mid - 1;
+  }
+  const qg_block_seg& S = segs[lo];
+  const int64_t b = gb - S.block_begin;
+  const int t = threadIdx.x, r = t & 127, h = t >> 7;
+  const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(S.packed) + b * 128 + r);
+  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+  if (S.bytes) {
+    uint8_t* blk = S.bytes + b * 16384;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = h + 2 * i;
+      const uint32_t x = w[c >> 1] >> ((c & 1) * 16);
+      *reinterpret_cast<uint4*>(blk + umma_off(r, c)) =
+          make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu), expand_nibble((x >> 8) & 0xFu),
+                     expand_nibble((x >> 12) & 0xFu));
+    }
+  }
+  if (S.degrees && h == 0) {
+    const int64_t row = (int64_t)S.blk_rb[b] * 128 + r;
+    const int d = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+    if (row < S.rows && d) atomicAdd(reinterpret_cast<unsigned long long*>(S.degrees + row), (unsigned long long)d);
+  }
+}
+
 // Plain code matrix (row-major [rows][ld]) -> left- or right-tiled layout.
 __global__ void codes_to_tiles_kernel(const uint8_t* __restrict__ codes, int64_t rows, int64_t cols, int64_t ld,
                                       int right, int64_t pitch, uint8_t* __restrict__ tiles) {
@@ -1026,6 +1060,14 @@ extern "C" int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t p
     block_gather_kernel<<<(unsigned)((nblocks * 32 + 255) / 256), 256, 0, st>>>(a_words, padded_rows, padded_cols,
                                                                                 blk_rb, blk_kt, nblocks, packed);
   block_expand_kernel<<<(unsigned)nblocks, 256, 0, st>>>(packed, nblocks, blk_rb, bytes, degrees, rows);
+  return tstatus();
+}
+
+extern "C" int qg_block_prepare_grouped(const qg_block_seg* segs, int32_t nsegs, int64_t total_blocks,
+                                        void* stream) {
+  if (!segs || nsegs < 1 || total_blocks < 0) return QG_ERR_ARG;
+  if (total_blocks == 0) return QG_OK;
+  block_expand_grouped_kernel<<<(unsigned)total_blocks, 256, 0, (cudaStream_t)stream>>>(segs, nsegs, total_blocks);
   return tstatus();
 }
 

@@ -46,9 +46,16 @@ class EpochRunner:
 
     def _forward_all(self, verify: bool):
         if self.rescan:
-            from .tiled import blocked
-            for b in self.batches:            # new words each step: re-gather + re-expand the blocks
-                blocked(b.adjacency).refresh()
+            from .tiled import GroupedRefresh, blocked
+            blks = [blocked(b.adjacency) for b in self.batches]
+            if all(not getattr(k, "_gather", True) for k in blks):
+                # shipped blocks (QGT3 views): one grouped expansion + degrees launch
+                if getattr(self, "_grouped", None) is None:
+                    self._grouped = GroupedRefresh(blks)
+                self._grouped.run()
+            else:
+                for k in blks:                # new words each step: re-gather + re-expand the blocks
+                    k.refresh()
         return model_forward_group(self.batches, self.model, jump=self.jump, reuse=self.reuse, verify=verify)
 
     def capture(self, pre=None, post=None, stamps: bool = False):
@@ -117,7 +124,11 @@ class EpochRunner:
         stages = 2 * len(self.model.layers)
         per_epoch = 1 + (-(-stages // MAX_EPOCH_STAGES) if engine.FUSED_EPOCH else stages)
         if self.rescan:
-            per_epoch += sum(2 if getattr(blocked(b.adjacency), "_gather", True) else 1 for b in self.batches)
+            blks = [blocked(b.adjacency) for b in self.batches]
+            if all(not getattr(k, "_gather", True) for k in blks):
+                per_epoch += 1                                      # grouped expansion
+            else:
+                per_epoch += 2 * len(blks)
         return per_epoch
 
 
@@ -148,6 +159,14 @@ class HostEpochRunner:
         self.device.copy_(self.host, non_blocking=True)
 
     def _d2h(self, outs):
+        # the engine writes every batch's logits into one allocation (row-contiguous, batch
+        # order): one strided view over it -> ONE D2H for the epoch
+        contiguous = bool(outs) and all(o.is_contiguous() for o in outs) and all(
+            b.data_ptr() == a.data_ptr() + a.numel() * a.element_size() for a, b in zip(outs, outs[1:]))
+        if contiguous and sum(o.shape[0] for o in outs) == self.out_host.shape[0]:
+            whole = outs[0].as_strided(tuple(self.out_host.shape), (self.out_host.shape[1], 1))
+            self.out_host.copy_(whole, non_blocking=True)
+            return
         r = 0
         for o in outs:
             self.out_host[r:r + o.shape[0]].copy_(o, non_blocking=True)

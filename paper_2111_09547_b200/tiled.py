@@ -472,3 +472,52 @@ def flush_epoch(stages: list, keep: list) -> None:
                       % (a.segs, a.nsegs, a.total_ctas, a.bn, segs[0].a or 0, segs[0].b or 0, segs[0].m, segs[0].r128,
                          segs[0].cta_begin, segs[0].k_tiles), flush=True)
         N.check(_lib().qg_tiled_epoch(arr, len(chunk), bar.data_ptr(), N.stream()), "qg_tiled_epoch")
+
+
+# ------------------------------------------------- grouped block expansion
+class BlockSeg(ctypes.Structure):
+    """Mirror of ``qg_block_seg``."""
+
+    _fields_ = [("packed", ctypes.c_void_p), ("blk_rb", ctypes.c_void_p), ("bytes", ctypes.c_void_p),
+                ("degrees", ctypes.c_void_p), ("rows", ctypes.c_int64), ("block_begin", ctypes.c_int64)]
+
+
+class GroupedRefresh:
+    """Per-step block expansion + degrees of many shipped-block batches (QGT3 views) in
+    ONE memset + ONE launch, instead of a memset and a launch per batch.  The batches'
+    degrees are re-pointed to views of one joint buffer so a single memset zeroes them."""
+
+    def __init__(self, blks: list):
+        self.blks = [b for b in blks if b.nblocks]
+        dev = N.device()
+        total_rows = sum(b.m for b in blks)
+        self.degrees = torch.zeros(max(total_rows, 1), dtype=torch.int64, device=dev)
+        off = 0
+        for b in blks:                              # every batch's degrees -> a view of the joint buffer
+            b.degrees = self.degrees[off:off + b.m]
+            off += b.m
+        segs, begin = [], 0
+        for b in self.blks:
+            seg = BlockSeg()
+            seg.packed, seg.blk_rb = b.packed.data_ptr(), b.blk_rb.data_ptr()
+            seg.bytes = None if A_BITS else b.bytes.data_ptr()
+            seg.degrees, seg.rows, seg.block_begin = b.degrees.data_ptr(), b.m, begin
+            begin += b.nblocks
+            segs.append(seg)
+        self.total = begin
+        self.keep = []
+        if segs:
+            n = len(segs)
+            host = torch.zeros(n * ctypes.sizeof(BlockSeg), dtype=torch.uint8).pin_memory()
+            arr = (BlockSeg * n).from_address(host.data_ptr())
+            for i, sg in enumerate(segs):
+                arr[i] = sg
+            self.table = host.to(dev)                 # static for the runner's lifetime
+            self.keep.append(host)
+        self.nsegs = len(segs)
+
+    def run(self):
+        self.degrees.zero_()
+        if self.nsegs:
+            N.check(N.lib().qg_block_prepare_grouped(self.table.data_ptr(), self.nsegs, self.total, N.stream()),
+                    "qg_block_prepare_grouped")
