@@ -92,6 +92,9 @@ class EpochRunner:
                     self.logits = self._forward_all(verify=False)
                     if post is not None:
                         post(self.logits)
+            except BaseException:
+                N.STATIC_COPIES.clear()         # tables of a failed capture must never be copied later
+                raise
             finally:
                 N.ALLOC = N.TorchAlloc()
                 bitgemm.PHASE_HOOK = None
@@ -214,6 +217,9 @@ class CapturedCall:
                 with torch.cuda.graph(self.graph, stream=self.stream):
                     self.slabs.reset()
                     self.result = fn()
+            except BaseException:
+                N.STATIC_COPIES.clear()
+                raise
             finally:
                 N.ALLOC = N.TorchAlloc()
             N.flush_static_copies()

@@ -84,3 +84,29 @@ def test_logit_gather_world2_gloo(world):
         assert p.exitcode == 0
     want = np.arange(sum(rows), dtype=np.float64)[:, None] * 1000 + np.arange(classes)[None, :]
     np.testing.assert_array_equal(full, want)
+
+
+@pytest.mark.gpu
+def test_sharded_epoch_assembles_like_the_whole_epoch():
+    """Single-process check of the sharded bench path: every rank's LPT share runs as its
+    own epoch graph; reassembling the shares in global batch order (LogitGather.assemble,
+    what rank 0 does after the all_gather) equals the whole epoch on one GPU, bit for bit."""
+    from paper_2111_09547_b200.runtime import EpochRunner
+    cfg = synth.with_bits(synth.CONFIGS["C3"], 4)
+    ids = list(range(6))
+    sizes = synth.batch_part_sizes(cfg)[:6]
+    batches, feats, _ = synth.planted_batches(cfg, seed=0, batch_ids=ids)
+    model = synth.calibrated_model(cfg, batches[0], feats[0])
+    whole = torch.cat([o.cpu() for o in EpochRunner(model, batches, rescan=False).capture().run()])
+    world = 2
+    plan = shard.assign_lpt([shard.batch_cost(s, cfg.in_dim, cfg.bits) for s in sizes], world)
+    rows = [b.total_nodes for b in batches]
+    g = shard.LogitGather(plan, rows, model.layers[-1].out_dim, device="cpu")
+    recv = torch.zeros_like(g.recv)
+    for rank in range(world):
+        r = EpochRunner(model, [batches[i] for i in plan[rank]], rescan=False).capture()
+        outs = r.run()
+        torch.cuda.synchronize()
+        flat = torch.cat([o.cpu() for o in outs]) if outs else torch.zeros((0, g.classes), dtype=torch.float64)
+        recv[rank * g.pad: rank * g.pad + flat.shape[0]] = flat
+    assert torch.equal(g.assemble(recv), whole)
