@@ -312,8 +312,11 @@ def choose_bn_fused(npad: int, row_blocks_total: int, cap: int) -> int:
     return bn
 
 
+BN_MAX = int(os.environ.get("QG_BN_MAX", "256"))      # tuning experiments
+
+
 def choose_bn(npad: int, row_blocks_total: int) -> int:
-    bn = min(256, npad)
+    bn = min(BN_MAX, npad)
     while bn > 32 and row_blocks_total * (npad // bn) < 148:
         bn //= 2
     return bn
