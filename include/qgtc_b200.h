@@ -371,6 +371,37 @@ int qg_test_requant(const double* x, int64_t n, double alpha_min, double scale, 
 /* popcount32 (bitgemm.py:58-60) on the device. */
 int qg_popcount32(const uint32_t* in, int64_t n, int32_t* out, void* stream);
 
+/* ---- reference-shaped entry points (SURVEY.md 8(b) export table) ---------------
+ * qg_bmm_1xs: bmm_1bit_by_nbit (bitgemm.py:306-371) -- qg_bitgemm with lbits == 1
+ *   (QG_ERR_BITS otherwise); mode PER_PLANE (the reference's per-plane list), I32
+ *   (reduce_bitplanes fused) or EPILOGUE.
+ * qg_gemm_sxt: gemm_sbit_by_tbit (bitgemm.py:374-475) -- qg_bitgemm, mode I32 or
+ *   EPILOGUE (QG_ERR_ARG for PER_PLANE).
+ * qg_batch_h2d: the single H2D of a packed compound buffer (pack_batch /
+ *   unpack_batch, graph.py:374-431; QGT2/QGT3 images) from PINNED host memory,
+ *   stream-ordered (capturable in a CUDA graph). */
+int qg_bmm_1xs(const qg_gemm_args* args, void* stream);
+int qg_gemm_sxt(const qg_gemm_args* args, void* stream);
+int qg_batch_h2d(const void* pinned_src, int64_t nbytes, void* device_dst, void* stream);
+
+/* OpCounters closed forms (bitgemm.py:72-100, 335-370, 409-461), host-only:
+ *   bmm:  rt x ct 8x128 tiles of A, `zero_tiles` of them all-zero, s planes of X,
+ *         n_chunks = padded N / 8;
+ *   gemm: per plane i < s of X its zero tiles plane_zero_tiles[i], t planes of W.
+ * jump = 0 counts every tile; cross_tile = 0 is the cross-bit reuse mode. */
+typedef struct {
+  int64_t tile_mma_count;
+  int64_t tile_fetch_count;
+  int64_t tiles_skipped;
+  int64_t word_and_popcount_count;
+  int64_t tiles_total;
+} qg_counters;
+
+int qg_bmm_counters(int64_t rt, int64_t ct, int64_t zero_tiles, int32_t s, int64_t n_chunks, int32_t jump,
+                    int32_t cross_tile, qg_counters* out);
+int qg_gemm_counters(int64_t rt, int64_t ct, const int64_t* plane_zero_tiles, int32_t s, int32_t t,
+                     int64_t n_chunks, int32_t jump, int32_t cross_tile, qg_counters* out);
+
 #ifdef __cplusplus
 }
 #endif

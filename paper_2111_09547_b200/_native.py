@@ -34,7 +34,8 @@ EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes"
            "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes",
            "qg_test_requant", "qg_tiled_gemm", "qg_block_prepare", "qg_codes_to_tiles",
            "qg_tiles_to_codes", "qg_entry_tiles", "qg_tiled_epoch",
-           "qg_block_prepare_grouped")
+           "qg_block_prepare_grouped", "qg_bmm_1xs", "qg_gemm_sxt", "qg_batch_h2d", "qg_bmm_counters",
+           "qg_gemm_counters")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -96,6 +97,8 @@ def lib() -> ctypes.CDLL:
             "qg_plane_zero_tiles": ([_vp, _i64, _i64, _i64, _vp, _vp], ctypes.c_int),
             "qg_epilogue_apply": ([_vp, _i64, _i64, ctypes.POINTER(Epilogue), _vp], ctypes.c_int),
             "qg_bitgemm": ([ctypes.POINTER(GemmArgs), _vp], ctypes.c_int),
+            "qg_bmm_1xs": ([ctypes.POINTER(GemmArgs), _vp], ctypes.c_int),
+            "qg_gemm_sxt": ([ctypes.POINTER(GemmArgs), _vp], ctypes.c_int),
             "qg_reduce_planes": ([_vp, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
             "qg_popcount32": ([_vp, _i64, _vp, _vp], ctypes.c_int),
             "qg_edges_to_bits": ([_vp, _vp, _i64, _i64, _vp, _i64, _i64, _vp], ctypes.c_int),
@@ -105,6 +108,9 @@ def lib() -> ctypes.CDLL:
                                    ctypes.c_int),
             "qg_entry_tiles": ([_vp, _i32, _i32, _i32, _i64, _vp], ctypes.c_int),
             "qg_block_prepare_grouped": ([_vp, _i32, _i64, _vp], ctypes.c_int),
+            "qg_batch_h2d": ([_vp, _i64, _vp, _vp], ctypes.c_int),
+            "qg_bmm_counters": ([_i64, _i64, _i64, _i32, _i64, _i32, _i32, _vp], ctypes.c_int),
+            "qg_gemm_counters": ([_i64, _i64, _vp, _i32, _i32, _i64, _i32, _i32, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)

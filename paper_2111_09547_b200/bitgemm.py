@@ -358,7 +358,7 @@ def _launch_work(mp, kp, np_, rbits, mode, schedule):
 
 def gemm_device(lhs_dwords, lbits, m, mp, k, kp, rhs_dwords, rbits, n, np_, *, mode, schedule=None,
                 out=None, epi_struct=None, algo="auto", cross_bit=False, overflow=None, scratch=None,
-                lhs_codes=None, rhs_codes=None):
+                lhs_codes=None, rhs_codes=None, entry: str = "qg_bitgemm"):
     """Launch qg_bitgemm on device tensors (no syncs).  ``lhs_codes``/``rhs_codes``
     are optional (u8 tensor, ld) code caches used instead of the plane words."""
     args = N.GemmArgs()
@@ -389,11 +389,11 @@ def gemm_device(lhs_dwords, lbits, m, mp, k, kp, rhs_dwords, rbits, n, np_, *, m
     if PROFILE_HOOK is not None:
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s_ev.record()
-        N.check(N.lib().qg_bitgemm(args, N.stream()), "qg_bitgemm")
+        N.check(getattr(N.lib(), entry)(args, N.stream()), entry)
         e_ev.record()
         PROFILE_HOOK.append((s_ev, e_ev, _launch_work(mp, kp, np_, rbits, mode, schedule)))
         return
-    N.check(N.lib().qg_bitgemm(args, N.stream()), "qg_bitgemm")
+    N.check(getattr(N.lib(), entry)(args, N.stream()), entry)
 
 
 def ctypes_pointer(struct):
@@ -411,15 +411,21 @@ def _check_reuse(reuse: str):
         raise ValueError(f"reuse must be {CROSS_BIT!r} or {CROSS_TILE!r}")
 
 
+def _c_counters(fn: str, *args) -> OpCounters:
+    """OpCounters from the C-ABI closed forms (qg_bmm_counters / qg_gemm_counters)."""
+    import ctypes
+    out = (ctypes.c_int64 * 5)()
+    N.check(getattr(N.lib(), fn)(*args, ctypes.byref(out)), fn)
+    return OpCounters(*(int(v) for v in out))
+
+
 def _bmm_counters(a: PackedBitMatrix, s: int, n_chunks: int, jump: bool, reuse: str):
+    """Counters of bmm_1bit_by_nbit (bitgemm.py:335-370); resolved lazily (needs the scan)."""
     def resolve():
         sch = _schedule(a)
-        total = sch.rt * sch.ct
-        zeros = sch.zeros if (jump and total) else 0
-        nz = total - zeros
-        mma = s * nz * n_chunks
-        return OpCounters(tile_mma_count=mma, tile_fetch_count=nz if reuse == CROSS_TILE else s * nz,
-                          tiles_skipped=zeros, word_and_popcount_count=mma * 256, tiles_total=total)
+        zeros = sch.zeros if (jump and sch.rt * sch.ct) else 0
+        return _c_counters("qg_bmm_counters", sch.rt, sch.ct, zeros, s, n_chunks, int(jump),
+                           int(reuse == CROSS_TILE))
     return resolve
 
 
@@ -447,7 +453,7 @@ def bmm_planes_device(a: PackedBitMatrix, x: BitPlaneStack, *, jump=True, reuse=
     if m and n and a.padded_cols:
         gemm_device(a.dwords, 1, m, a.padded_rows, a.logical_cols, a.padded_cols, x.dwords, s, n,
                     x.padded_cols, mode=N.GEMM_PER_PLANE, schedule=sch, out=out, algo=algo,
-                    cross_bit=(reuse == CROSS_BIT))
+                    cross_bit=(reuse == CROSS_BIT), entry="qg_bmm_1xs")
     _set_counters(_bmm_counters(a, s, x.padded_cols // TILE_COLS, jump, reuse))
     return out
 
@@ -482,15 +488,11 @@ def reduce_bitplanes(plane_accs) -> np.ndarray:
 
 def _gemm_counters(x: BitPlaneStack, t: int, n_chunks: int, jump: bool, reuse: str):
     def resolve():
+        import ctypes
         rt, ct = x.padded_rows // TILE_ROWS, x.padded_cols // TILE_K_BITS
-        per_plane_total = rt * ct
-        zeros = _plane_zero_tiles(x) if (jump and per_plane_total) else [0] * x.bits
-        nzs = [per_plane_total - z for z in zeros]
-        mma = t * sum(nzs) * n_chunks
-        return OpCounters(tile_mma_count=mma,
-                          tile_fetch_count=sum(nzs) if reuse == CROSS_TILE else t * sum(nzs),
-                          tiles_skipped=sum(zeros), word_and_popcount_count=256 * mma,
-                          tiles_total=x.bits * per_plane_total)
+        zeros = _plane_zero_tiles(x) if (jump and rt * ct) else [0] * x.bits
+        return _c_counters("qg_gemm_counters", rt, ct, (ctypes.c_int64 * x.bits)(*zeros), x.bits, t, n_chunks,
+                           int(jump), int(reuse == CROSS_TILE))
     return resolve
 
 
@@ -533,7 +535,7 @@ def gemm_sbit_by_tbit(x: BitPlaneStack, w: BitPlaneStack, out: str = "int32",
         acc = torch.zeros((m, n), dtype=torch.int32, device=dev)
         if m and n:
             gemm_device(x.dwords, x.bits, m, x.padded_rows, k, x.padded_cols, w.dwords, w.bits, n, w.padded_cols,
-                        mode=N.GEMM_I32, out=acc, overflow=overflow)
+                        mode=N.GEMM_I32, out=acc, overflow=overflow, entry="qg_gemm_sxt")
         _set_counters(_gemm_counters(x, w.bits, w.padded_cols // TILE_COLS, jump, reuse))
         if exact:
             N.raise_overflow(overflow, lambda: _peak(x, w))
@@ -542,7 +544,8 @@ def gemm_sbit_by_tbit(x: BitPlaneStack, w: BitPlaneStack, out: str = "int32",
     scratch = torch.empty((m, n), dtype=torch.int32, device=dev) if exact else None
     if m and n:
         gemm_device(x.dwords, x.bits, m, x.padded_rows, k, x.padded_cols, w.dwords, w.bits, n, w.padded_cols,
-                    mode=N.GEMM_EPILOGUE, epi_struct=plan.struct, overflow=overflow, scratch=scratch)
+                    mode=N.GEMM_EPILOGUE, epi_struct=plan.struct, overflow=overflow, scratch=scratch,
+                    entry="qg_gemm_sxt")
     _set_counters(_gemm_counters(x, w.bits, w.padded_cols // TILE_COLS, jump, reuse))
     if exact:
         N.raise_overflow(overflow, lambda: _peak(x, w))

@@ -798,4 +798,60 @@ extern "C" int qg_test_requant(const double* x, int64_t n, double amin, double s
   return launch_status_g();
 }
 
-extern "C" int qg_version(void) { return 23; }  // == number of exported entry points
+extern "C" int qg_version(void) { return 28; }  // == number of exported entry points
+
+// ---------------------------------------------------------------------------
+// Reference-shaped entry points over qg_bitgemm / cudaMemcpyAsync,
+// and the OpCounters closed forms (host-only).
+extern "C" int qg_bmm_1xs(const qg_gemm_args* a, void* stream) {
+  if (!a) return QG_ERR_ARG;
+  if (a->lbits != 1) return QG_ERR_BITS;
+  return qg_bitgemm(a, stream);
+}
+
+extern "C" int qg_gemm_sxt(const qg_gemm_args* a, void* stream) {
+  if (!a) return QG_ERR_ARG;
+  if (a->mode != QG_GEMM_I32 && a->mode != QG_GEMM_EPILOGUE) return QG_ERR_ARG;
+  return qg_bitgemm(a, stream);
+}
+
+extern "C" int qg_batch_h2d(const void* pinned_src, int64_t nbytes, void* device_dst, void* stream) {
+  if (nbytes < 0 || (nbytes && (!pinned_src || !device_dst))) return QG_ERR_ARG;
+  if (nbytes == 0) return QG_OK;
+  const cudaError_t e = cudaMemcpyAsync(device_dst, pinned_src, (size_t)nbytes, cudaMemcpyHostToDevice,
+                                        (cudaStream_t)stream);
+  return e == cudaSuccess ? QG_OK : QG_ERR_CUDA;
+}
+
+extern "C" int qg_bmm_counters(int64_t rt, int64_t ct, int64_t zero_tiles, int32_t s, int64_t n_chunks, int32_t jump,
+                               int32_t cross_tile, qg_counters* out) {
+  if (!out || rt < 0 || ct < 0 || n_chunks < 0 || s < 1 || s > 8 || zero_tiles < 0 || zero_tiles > rt * ct)
+    return QG_ERR_ARG;
+  const int64_t total = rt * ct;
+  const int64_t nz = jump ? total - zero_tiles : total;
+  out->tile_mma_count = (int64_t)s * nz * n_chunks;
+  out->tile_fetch_count = cross_tile ? nz : (int64_t)s * nz;
+  out->tiles_skipped = jump ? zero_tiles : 0;
+  out->word_and_popcount_count = 256 * out->tile_mma_count;
+  out->tiles_total = total;
+  return QG_OK;
+}
+
+extern "C" int qg_gemm_counters(int64_t rt, int64_t ct, const int64_t* plane_zero_tiles, int32_t s, int32_t t,
+                                int64_t n_chunks, int32_t jump, int32_t cross_tile, qg_counters* out) {
+  if (!out || !plane_zero_tiles || rt < 0 || ct < 0 || n_chunks < 0 || s < 1 || s > 8 || t < 1 || t > 8)
+    return QG_ERR_ARG;
+  const int64_t per_plane = rt * ct;
+  int64_t nz = 0, zeros = 0;
+  for (int i = 0; i < s; ++i) {
+    if (plane_zero_tiles[i] < 0 || plane_zero_tiles[i] > per_plane) return QG_ERR_ARG;
+    nz += jump ? per_plane - plane_zero_tiles[i] : per_plane;
+    zeros += plane_zero_tiles[i];
+  }
+  out->tile_mma_count = (int64_t)t * nz * n_chunks;
+  out->tile_fetch_count = cross_tile ? nz : (int64_t)t * nz;
+  out->tiles_skipped = jump ? zeros : 0;
+  out->word_and_popcount_count = 256 * out->tile_mma_count;
+  out->tiles_total = (int64_t)s * per_plane;
+  return QG_OK;
+}

@@ -44,3 +44,34 @@ def test_host_side_argument_errors_need_no_gpu():
         N.check(N.QG_ERR_SHAPE, "x")
     assert N.lib().qg_quantize_pack(None, 0, 4, 4, 4, 0.0, 1.0, 9, 0, 8, None, None, None, None, None, None) \
         in (N.QG_ERR_ARG, N.QG_ERR_BITS)
+
+
+def test_counter_closed_forms_match_the_oracle():
+    """qg_bmm_counters / qg_gemm_counters (host-only C-ABI) == the oracle's closed forms of
+    the reference counters (bitgemm.py:335-370, 409-461) on random flag maps."""
+    import ctypes
+
+    import numpy as np
+
+    from oracle import qgtc_oracle as O
+    from paper_2111_09547_b200 import _native as N
+    lib = N.lib()
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        rt, ct, s, t, n_chunks = (int(v) for v in rng.integers(1, 9, 5))
+        jump, cross = bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
+        flags = rng.uniform(0, 1, (rt, ct)) < rng.uniform(0, 1)
+        out = (ctypes.c_int64 * 5)()
+        assert lib.qg_bmm_counters(rt, ct, int(flags.sum()), s, n_chunks, int(jump), int(cross), ctypes.byref(out)) == 0
+        want = O.counters_bmm(flags, s, n_chunks, jump=jump, cross_tile=cross)
+        assert list(out) == [want[k] for k in ("tile_mma_count", "tile_fetch_count", "tiles_skipped",
+                                               "word_and_popcount_count", "tiles_total")]
+        planes = [rng.uniform(0, 1, (rt, ct)) < rng.uniform(0, 1) for _ in range(s)]
+        zeros = (ctypes.c_int64 * s)(*[int(f.sum()) for f in planes])
+        assert lib.qg_gemm_counters(rt, ct, zeros, s, t, n_chunks, int(jump), int(cross), ctypes.byref(out)) == 0
+        want = O.counters_gemm(planes, t, n_chunks, jump=jump, cross_tile=cross)
+        assert list(out) == [want[k] for k in ("tile_mma_count", "tile_fetch_count", "tiles_skipped",
+                                               "word_and_popcount_count", "tiles_total")]
+    # argument errors are host-side status codes, no GPU involved
+    assert lib.qg_bmm_counters(2, 2, 5, 1, 1, 1, 1, ctypes.byref(out)) == N.QG_ERR_ARG
+    assert lib.qg_batch_h2d(None, 16, None, None) == N.QG_ERR_ARG
