@@ -253,7 +253,18 @@ typedef struct {
   int64_t cta_begin;           /* first CTA of this segment                          */
   int32_t k_tiles;             /* dense left: K tiles                                */
   int32_t pad_;
+  int64_t pad2_;
+  /* pair mode (qg_tiled_args.pair): 2-D TMA descriptors (CUtensorMap, 128 B, 64-B
+   * aligned; qg_encode_linear_map) of the A source and the B source viewed as rows of
+   * 128 bytes -- the pair's copies signal the leader CTA's mbarrier (cta_group::2) */
+  uint8_t tmap_a[128];
+  uint8_t tmap_b[128];
 } qg_tseg;
+
+/* Encode a 2-D TMA descriptor over a linear device buffer of `bytes` (multiple of 128)
+ * viewed as rows of 128 bytes, box = box_rows rows (a contiguous box_rows*128-byte
+ * copy).  Host-only; out = 128 bytes. */
+int qg_encode_linear_map(const void* base, int64_t bytes, int32_t box_rows, void* out);
 
 typedef struct {
   const qg_tseg* segs;         /* DEVICE array of segments (sorted by cta_begin)     */
@@ -272,7 +283,9 @@ typedef struct {
                                   128 rows x 4 words, the column-wise bits of the block),
                                   expanded to the UMMA byte layout in shared memory;
                                   0 = pre-expanded 16 KB byte blocks                    */
-  int32_t pad2_;
+  int32_t pair;                /* 1: CTA pairs (cluster of 2) with cta_group::2 MMAs, M = 256;
+                                  segs[].cta_begin then counts PAIRS, total_ctas = 2 x pairs,
+                                  bn >= 64 (each CTA stages bn/2 columns of B)             */
 } qg_tiled_args;
 
 /* Warp-specialised tiled bit-GEMM (cp.async.bulk producer, single-thread

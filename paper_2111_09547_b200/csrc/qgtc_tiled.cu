@@ -17,11 +17,13 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <cuda.h>
 #include "qgtc_common.cuh"
 
 namespace qg {
 
 struct TiledParams {
+  alignas(64) CUtensorMap zero_map;   // pair mode: 16 KB zero block (rows of 128 B)
   const qg_tseg* segs;
   int32_t nsegs;
   int32_t a_blocks;         // 1: left operand = adjacency blocks (schedule), 0: dense left slabs
@@ -35,6 +37,7 @@ struct TiledParams {
   int64_t* phase_ns;        // optional per-tile %globaltimer stamps (tools/phase_tiled.py)
   int64_t total_ctas;       // work items (segment, row block, N tile) of this stage
   int32_t a_bits;           // 1: adjacency blocks are shipped packed (2 KB) and expanded in smem
+  int32_t pair;             // 1: CTA pairs (cluster of 2) run cta_group::2 MMAs, M = 256
 };
 
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
@@ -42,6 +45,11 @@ static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     P.phase_ns[tile * 8 + k] = (int64_t)t;
+    if (k == 0) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      P.phase_ns[tile * 8 + 6] = (int64_t)smid;
+    }
   }
 }
 
@@ -290,6 +298,80 @@ struct TileRing {
   bool pdl_wait;              // griddepcontrol.wait still pending (PDL-launched single tile)
 };
 
+// Epilogue of one 128-row x bn tile held in this CTA's TMEM: 8-column slices over all
+// 8 warps, fused dequant/BN/act/requant (or fp64 / int32 output); the lane's code row
+// sum is accumulated into R.sRowSum (flushed to global by the caller).
+__device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tseg& G, TileRing& R, int64_t tile,
+                                              int64_t rb, int64_t n0, int nk, uint32_t tmem, const double* sCol,
+                                              bool fused, bool screen) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bn = P.bn;
+  const qg_epilogue& E = P.epi;
+  // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
+  const int quad = warp & 3, half = warp >> 2;
+  const int64_t r0 = rb * 128 + quad * 32;
+  const int64_t myrow = r0 + lane;
+  const bool rvalid = myrow < G.m;
+  const int64_t rem_cols = P.n - n0;
+  const int ncols_cta = rem_cols <= 0 ? 0 : (rem_cols < bn ? (int)rem_cols : bn);
+  const int nslices = (ncols_cta + 7) >> 3;
+  const bool packed = fused && E.out_kind == QG_OUT_PLANES;
+  EpiLane L;
+  L.tmem_row = tmem + ((uint32_t)(quad * 32) << 16);
+  L.has_acc = nk > 0;
+  L.first = half;
+  L.nslices = nslices;
+  L.nvalid = (int)(P.n - n0);
+  L.rvalid = myrow < G.m;
+  L.myrow = myrow;
+  L.n0 = n0;
+  uint32_t rsum = 0;
+  if (!fused) {
+    const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
+    for (int sl = half; sl < nslices; sl += 2) {
+      uint32_t v[8];
+      L.load8(sl * 8, v);
+      if (rvalid) {
+        int32_t* dst = G.out_i32 + myrow * P.n + n0 + sl * 8;
+        if (vec_ok && sl * 8 + 8 <= L.nvalid) {
+          // 8 consecutive columns of this row: two 16-byte stores (n % 4 == 0 keeps them aligned)
+          reinterpret_cast<int4*>(dst)[0] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+          reinterpret_cast<int4*>(dst)[1] = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (sl * 8 + jj < L.nvalid) dst[jj] = (int32_t)v[jj];
+        }
+      }
+    }
+  } else {
+    // one uniform dispatch per tile: the slice loop below is straight-line per variant
+    const double rterm = rvalid ? R.sRowTerm[quad * 32 + lane] : 0.0;
+    const bool row_only = !E.use_col && !E.use_const && !E.bias;
+    if (screen) {
+      rsum = E.act == QG_ACT_RELU ? epi_slices_screen<true>(P, G, L, sCol, rterm)
+                                  : epi_slices_screen<false>(P, G, L, sCol, rterm);
+    } else switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
+#define QG_EPI_CASE(i, A, B, Rw) \
+  case i: rsum = epi_slices<A, B, Rw>(P, G, L, sCol, rterm); break;
+      QG_EPI_CASE(0, QG_ACT_NONE, false, false)
+      QG_EPI_CASE(1, QG_ACT_NONE, false, true)
+      QG_EPI_CASE(2, QG_ACT_NONE, true, false)
+      QG_EPI_CASE(3, QG_ACT_NONE, true, true)
+      QG_EPI_CASE(4, QG_ACT_RELU, false, false)
+      QG_EPI_CASE(5, QG_ACT_RELU, false, true)
+      QG_EPI_CASE(6, QG_ACT_RELU, true, false)
+      QG_EPI_CASE(7, QG_ACT_RELU, true, true)
+      QG_EPI_CASE(8, QG_ACT_TANH, false, false)
+      QG_EPI_CASE(9, QG_ACT_TANH, false, true)
+      QG_EPI_CASE(10, QG_ACT_TANH, true, false)
+      default: rsum = epi_slices<QG_ACT_TANH, true, true>(P, G, L, sCol, rterm); break;
+#undef QG_EPI_CASE
+    }
+  }
+  if (packed && G.q_row_sums && rsum) atomicAdd(&R.sRowSum[quad * 32 + lane], (unsigned long long)rsum);
+}
+
 // One work item: (segment, 128-row block, N tile) -> fused GEMM tile.  Ends with a
 // CTA barrier so the next tile may overwrite TMEM / shared staging.
 template <int TMEM_COLS>
@@ -491,71 +573,9 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   __syncthreads();   // sCol / row terms / zeroed row sums visible to all epilogue warps
   if (tid == 0) tstamp(P, tile, 3);
 
-  // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
-  const int quad = warp & 3, half = warp >> 2;
-  const int64_t r0 = rb * 128 + quad * 32;
-  const int64_t myrow = r0 + lane;
-  const bool rvalid = myrow < G.m;
-  const int64_t rem_cols = P.n - n0;
-  const int ncols_cta = rem_cols <= 0 ? 0 : (rem_cols < bn ? (int)rem_cols : bn);
-  const int nslices = (ncols_cta + 7) >> 3;
-  const bool packed = fused && E.out_kind == QG_OUT_PLANES;
-  EpiLane L;
-  L.tmem_row = tmem + ((uint32_t)(quad * 32) << 16);
-  L.has_acc = nk > 0;
-  L.first = half;
-  L.nslices = nslices;
-  L.nvalid = (int)(P.n - n0);
-  L.rvalid = myrow < G.m;
-  L.myrow = myrow;
-  L.n0 = n0;
-  uint32_t rsum = 0;
-  if (!fused) {
-    const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
-    for (int sl = half; sl < nslices; sl += 2) {
-      uint32_t v[8];
-      L.load8(sl * 8, v);
-      if (rvalid) {
-        int32_t* dst = G.out_i32 + myrow * P.n + n0 + sl * 8;
-        if (vec_ok && sl * 8 + 8 <= L.nvalid) {
-          // 8 consecutive columns of this row: two 16-byte stores (n % 4 == 0 keeps them aligned)
-          reinterpret_cast<int4*>(dst)[0] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
-          reinterpret_cast<int4*>(dst)[1] = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            if (sl * 8 + jj < L.nvalid) dst[jj] = (int32_t)v[jj];
-        }
-      }
-    }
-  } else {
-    // one uniform dispatch per tile: the slice loop below is straight-line per variant
-    const double rterm = rvalid ? R.sRowTerm[quad * 32 + lane] : 0.0;
-    const bool row_only = !E.use_col && !E.use_const && !E.bias;
-    if (screen) {
-      rsum = E.act == QG_ACT_RELU ? epi_slices_screen<true>(P, G, L, sCol, rterm)
-                                  : epi_slices_screen<false>(P, G, L, sCol, rterm);
-    } else switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
-#define QG_EPI_CASE(i, A, B, Rw) \
-  case i: rsum = epi_slices<A, B, Rw>(P, G, L, sCol, rterm); break;
-      QG_EPI_CASE(0, QG_ACT_NONE, false, false)
-      QG_EPI_CASE(1, QG_ACT_NONE, false, true)
-      QG_EPI_CASE(2, QG_ACT_NONE, true, false)
-      QG_EPI_CASE(3, QG_ACT_NONE, true, true)
-      QG_EPI_CASE(4, QG_ACT_RELU, false, false)
-      QG_EPI_CASE(5, QG_ACT_RELU, false, true)
-      QG_EPI_CASE(6, QG_ACT_RELU, true, false)
-      QG_EPI_CASE(7, QG_ACT_RELU, true, true)
-      QG_EPI_CASE(8, QG_ACT_TANH, false, false)
-      QG_EPI_CASE(9, QG_ACT_TANH, false, true)
-      QG_EPI_CASE(10, QG_ACT_TANH, true, false)
-      default: rsum = epi_slices<QG_ACT_TANH, true, true>(P, G, L, sCol, rterm); break;
-#undef QG_EPI_CASE
-    }
-  }
+  tile_epilogue(P, G, R, tile, rb, n0, nk, tmem, sCol, fused, screen);
   if (tid == 0) tstamp(P, tile, 4);
-  if (packed && G.q_row_sums) {
-    if (rsum) atomicAdd(&R.sRowSum[quad * 32 + lane], (unsigned long long)rsum);
+  if (P.mode == QG_GEMM_EPILOGUE && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
     __syncthreads();
     if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[tid])
       atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
@@ -621,6 +641,256 @@ __global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_consta
   tiled_tile<TMEM_COLS>(P, (int64_t)blockIdx.x, R);
   if ((threadIdx.x >> 5) == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
+}
+
+
+// ------------------------------------------------ 2-SM (CTA pair) variant
+// A cluster of 2 CTAs computes a 256-row x bn tile with cta_group::2 MMAs (M = 256):
+// each CTA stages its OWN 128-row A block and HALF of the B tile (bn/2 columns), so a
+// K tile costs 16 KB + bn*64 B of shared memory / L2 traffic per CTA instead of
+// 16 KB + bn*128 B.  The leader (rank 0) issues the MMAs once both CTAs' stages have
+// landed (the peer relays its stage completion to the leader with a remote mbarrier
+// arrive) and commits to the empty / done barriers of both CTAs (multicast).  Adjacency
+// row blocks of a pair generally have different non-zero K lists: the pair walks their
+// UNION, and a CTA whose row block has no block at that K tile stages a zero block.
+__device__ __align__(1024) uint8_t g_zero_block[16384];
+
+__device__ __forceinline__ uint32_t mapa_cluster(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_2d_pair(void* dst, const void* tmap, int32_t x, int32_t y, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2 [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+__device__ __forceinline__ void umma_i8_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+               ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+
+// Union of two ascending K lists: the i-th K tile of the pair, and whether each row
+// block has a block there (advancing the cursors).
+struct UnionCursor {
+  const int32_t* l0;
+  const int32_t* l1;
+  int n0, n1, i0, i1;
+  __device__ __forceinline__ int next(bool& has0, bool& has1) {
+    const int k0 = i0 < n0 ? l0[i0] : 0x7fffffff, k1 = i1 < n1 ? l1[i1] : 0x7fffffff;
+    const int kt = k0 < k1 ? k0 : k1;
+    has0 = k0 == kt;
+    has1 = k1 == kt;
+    i0 += has0;
+    i1 += has1;
+    return kt;
+  }
+};
+
+template <int TMEM_COLS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
+    tc_pair_kernel(const __grid_constant__ TiledParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ unsigned long long sRowSum[128];
+  __shared__ double sRowTerm[128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int bn = P.bn, S = P.stages, bh = bn >> 1;
+  const int64_t pair = (int64_t)(blockIdx.x >> 1);
+  if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 0);
+
+  // ---- work item of the pair: (segment, row-block pair, N tile); cta_begin counts PAIRS
+  int lo = 0, hi = P.nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.segs[mid].cta_begin <= pair) lo = mid; else hi = mid - 1;
+  }
+  const qg_tseg& G = P.segs[lo];
+  const int64_t local = pair - G.cta_begin;
+  const int64_t rbp = local / P.n_tiles;
+  const int nt = (int)(local % P.n_tiles);
+  const int64_t n0 = (int64_t)nt * bn;
+  const int64_t nrb = G.r128 >> 7;
+  const int64_t rb = rbp * 2 + rank;                     // this CTA's row block (may be past the end)
+  const int64_t rb_other = rbp * 2 + (rank ^ 1);
+  const bool rb_ok = rb < nrb, other_ok = rb_other < nrb;
+
+  // K schedule of the pair (identical in both CTAs)
+  UnionCursor U{};
+  int nk = 0, kbase_me = 0;
+  if (P.a_blocks) {
+    const int64_t rb0 = rbp * 2, rb1 = rbp * 2 + 1;
+    U.l0 = G.blk_kt + G.blk_base[rb0];
+    U.n0 = G.blk_count[rb0];
+    U.l1 = rb1 < nrb ? G.blk_kt + G.blk_base[rb1] : nullptr;
+    U.n1 = rb1 < nrb ? G.blk_count[rb1] : 0;
+    kbase_me = rb_ok ? G.blk_base[rb] : 0;
+    UnionCursor c = U;
+    bool h0, h1;
+    while (c.i0 < c.n0 || c.i1 < c.n1) { c.next(h0, h1); ++nk; }
+  } else {
+    nk = G.k_tiles;
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  const uint32_t a_bytes = 16384u, bh_bytes = (uint32_t)bh * 128u;
+  const uint32_t stage_bytes = a_bytes + bh_bytes;
+  uint8_t* stage0 = smem;
+  double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  const bool fused = P.mode == QG_GEMM_EPILOGUE;
+  const qg_epilogue& E = P.epi;
+  const bool screen = fused && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
+                      (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
+  if (tid < 128) sRowSum[tid] = 0ull;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();                                    // barriers of both CTAs initialised
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+  TileRing R;
+  R.stage0 = stage0; R.sCol = sCol; R.full = full; R.empty = empty; R.done = &done; R.aready = nullptr;
+  R.sRowSum = sRowSum; R.sRowTerm = sRowTerm; R.S = S; R.it0 = 0; R.ndone = 0; R.pdl_wait = false; R.tmem = tmem;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer (both CTAs): own A block + own half of B ----------------
+    // TMA copies (cta_group::2) complete on the LEADER's full[s]; the leader arms it with
+    // the bytes of both CTAs (a peer's bytes may land first: the tx count runs ahead)
+    const uint32_t leader_full = mapa_cluster(smem_u32(&full[0]), 0);
+    const int64_t b_row0 = ((n0 + (int64_t)rank * bh) >> 3) * 8;      // 128-byte rows
+    UnionCursor c = U;
+    int i_me = 0;
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % S;
+      if (it >= S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
+      const void* amap;
+      int64_t arow;
+      int kt;
+      if (P.a_blocks) {
+        bool h0, h1;
+        kt = c.next(h0, h1);
+        const bool mine = rank == 0 ? h0 : h1;
+        const bool real = rb_ok && mine;
+        amap = real ? (const void*)G.tmap_a : (const void*)&P.zero_map;
+        arow = real ? (int64_t)(kbase_me + i_me) * 128 : 0;
+        i_me += mine;
+      } else {
+        kt = it;
+        amap = rb_ok ? (const void*)G.tmap_a : (const void*)&P.zero_map;
+        arow = rb_ok ? (((int64_t)kt * (G.r128 << 7) + rb * 16384) >> 7) : 0;
+      }
+      uint8_t* dst = stage0 + (size_t)s * stage_bytes;
+      if (rank == 0) mbar_expect_tx(&full[s], 2u * (a_bytes + bh_bytes));
+      const uint32_t bar = leader_full + (uint32_t)s * 8u;
+      tma_2d_pair(dst, amap, 0, (int32_t)arow, bar);
+      tma_2d_pair(dst + a_bytes, G.tmap_b, 0, (int32_t)(((int64_t)kt * (P.b_npad << 7) >> 7) + b_row0), bar);
+    }
+  } else if (warp == 1 && lane == 0) {
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader): both CTAs' stages, M = 256 ----------------
+      const uint32_t idesc = (2u << 4) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      for (int it = 0; it < nk; ++it) {
+        const int s = it % S;
+        mbar_wait(smem_u32(&full[s]), (it / S) & 1);
+        if (it == 0) tstamp(P, (int64_t)blockIdx.x, 2);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_i8_pair(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc,
+                       (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit_pair(&empty[s]);
+      }
+      if (nk > 0) umma_commit_pair(&done);
+    }
+  } else if (warp >= 2 && fused) {
+    const int t = tid - 64;
+    if (t < 128) {
+      const int64_t row = rb * 128 + t;
+      sRowTerm[t] = (E.use_row && rb_ok && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
+    }
+    if (screen) {
+      for (int i = t; i < bn; i += kTThreads - 64) {
+        const int64_t cc = n0 + i;
+        double pc = 0.0, gc = 0.0, rc = 0x1p12;
+        if (cc < P.n) {
+          const double inv = E.q_inv_scale;
+          const double sC = E.use_col ? E.k_col * (double)E.col_sums[cc] : 0.0;
+          const double base = (sC + (E.use_const ? E.k_const : 0.0)) + (E.bias ? E.bias[cc] : 0.0);
+          double g = 1.0, center = base;
+          if (E.bn_mean) {
+            g = E.bn_gamma[cc] / E.bn_denom[cc];
+            center = (base - E.bn_mean[cc]) * g + E.bn_beta[cc];
+          }
+          gc = g * inv;
+          pc = E.k_acc * gc;
+          rc = 0x1p12 + (center - E.q_amin) * inv;
+        }
+        sCol[i] = pc;
+        sCol[bn + i] = gc;
+        sCol[2 * bn + i] = rc;
+      }
+    } else {
+      for (int i = t; i < bn; i += kTThreads - 64) {
+        const int64_t cc = n0 + i;
+        const bool ok = cc < P.n;
+        sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[cc]) : 0.0;
+        sCol[1 * bn + i] = (ok && E.bias) ? E.bias[cc] : 0.0;
+        if (E.bn_mean) {
+          sCol[2 * bn + i] = ok ? E.bn_mean[cc] : 0.0;
+          sCol[3 * bn + i] = ok ? E.bn_denom[cc] : 1.0;
+          sCol[4 * bn + i] = ok ? E.bn_gamma[cc] : 0.0;
+          sCol[5 * bn + i] = ok ? E.bn_beta[cc] : 0.0;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (nk > 0) {
+    mbar_wait(smem_u32(&done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  __syncthreads();
+  if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 3);
+  if (rb_ok) {
+    tile_epilogue(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused, screen);
+    if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
+    if (fused && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
+      __syncthreads();
+      if (tid < 128 && rb * 128 + tid < G.m && sRowSum[tid])
+        atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[tid]);
+    }
+  }
+  (void)other_ok;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();                                    // both CTAs done with TMEM and the ring
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 5);
 }
 
 // ------------------------------------------------ persistent epoch kernel
@@ -923,6 +1193,7 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.phase_ns = a->phase_ns;
   P.total_ctas = a->total_ctas;
   P.a_bits = a->a_blocks ? a->a_bits : 0;
+  P.pair = a->pair;
   const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
                       (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
   return (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
@@ -937,11 +1208,84 @@ static size_t smem_budget() {
   return budget;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+extern "C" int qg_encode_linear_map(const void* base, int64_t bytes, int32_t box_rows, void* out) {
+  if (!base || !out || bytes <= 0 || (bytes & 127) || box_rows < 1 || box_rows > 256 ||
+      (reinterpret_cast<uintptr_t>(base) & 15))
+    return QG_ERR_ARG;
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return QG_ERR_UNSUPPORTED;
+  const cuuint64_t dims[2] = {128, (cuuint64_t)(bytes >> 7)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base),
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? QG_OK : QG_ERR_ARG;
+}
+
+template <int COLS>
+static void launch_pair(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
+  static size_t attr_done = 0;
+  if (smem > attr_done) {
+    cudaFuncSetAttribute(tc_pair_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tc_pair_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    attr_done = smem;
+  }
+  static const bool pdl = getenv("QG_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, tc_pair_kernel<COLS>, P);
+}
+
 extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   TiledParams P;
   int rc;
   const size_t cols = tiled_params(a, P, rc);
   if (rc != QG_OK) return rc;
+  if (P.pair) {
+    // total_ctas = 2 x pairs; a stage holds the own A block + half of the B tile
+    if (P.a_bits || (a->total_ctas & 1) || P.bn < 64) return QG_ERR_UNSUPPORTED;
+    void* zero = nullptr;
+    cudaGetSymbolAddress(&zero, g_zero_block);
+    if (qg_encode_linear_map(zero, 16384, 128, &P.zero_map) != QG_OK) return QG_ERR_UNSUPPORTED;
+    const size_t stage = 16384 + (size_t)P.bn * 64;
+    P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
+    const size_t smem = (size_t)P.stages * stage + cols;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = (unsigned)a->total_ctas;
+    switch (P.bn) {
+      case 64: launch_pair<64>(P, grid, smem, st); break;
+      case 128: launch_pair<128>(P, grid, smem, st); break;
+      default: launch_pair<256>(P, grid, smem, st); break;
+    }
+    return tstatus();
+  }
   const size_t stage = P.a_bits ? ((16384 + (size_t)P.bn * 128 + 2048 + 1023) & ~(size_t)1023)
                                 : 16384 + (size_t)P.bn * 128;
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));

@@ -50,7 +50,8 @@ class TSeg(ctypes.Structure):
                 ("q_codes", ctypes.c_void_p), ("q_row_sums", ctypes.c_void_p), ("out_real", ctypes.c_void_p),
                 ("out_i32", ctypes.c_void_p), ("status", ctypes.c_void_p), ("m", ctypes.c_int64),
                 ("r128", ctypes.c_int64), ("cta_begin", ctypes.c_int64), ("k_tiles", ctypes.c_int32),
-                ("pad_", ctypes.c_int32)]
+                ("pad_", ctypes.c_int32), ("pad2_", ctypes.c_int64), ("tmap_a", ctypes.c_uint8 * 128),
+                ("tmap_b", ctypes.c_uint8 * 128)]
 
 
 class TiledArgs(ctypes.Structure):
@@ -61,7 +62,7 @@ class TiledArgs(ctypes.Structure):
                 ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
                 ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p), ("a_bits", ctypes.c_int32),
-                ("pad2_", ctypes.c_int32)]
+                ("pair", ctypes.c_int32)]
 
 
 _SIGS_DONE = False
@@ -79,6 +80,9 @@ MAX_EPOCH_STAGES = 8
 # profiles/r01g_abits_ab.txt) -- the main loop is latency-, not L2-bandwidth-bound.
 A_BITS = os.environ.get("QG_A_BITS", "0") == "1"
 
+# 2-SM CTA pairs for large GEMM stages (QG_PAIR=0 disables)
+PAIR = os.environ.get("QG_PAIR", "1") != "0"
+
 
 def _lib():
     global _SIGS_DONE
@@ -95,6 +99,8 @@ def _lib():
         L.qg_tiles_to_codes.restype = ctypes.c_int
         L.qg_tiled_epoch.argtypes = [ctypes.POINTER(TiledArgs), ctypes.c_int32, vp, vp]
         L.qg_tiled_epoch.restype = ctypes.c_int
+        L.qg_encode_linear_map.argtypes = [vp, i64, i32, vp]
+        L.qg_encode_linear_map.restype = ctypes.c_int
         _SIGS_DONE = True
     return L
 
@@ -322,16 +328,37 @@ def choose_bn(npad: int, row_blocks_total: int) -> int:
     return bn
 
 
+def use_pair(b_npad: int, row_blocks_total: int, sizes, mode: int) -> bool:
+    """2-SM CTA pairs (cta_group::2) for large int32-output stages (the C5 bit-GEMM): each
+    CTA stages half of the B tile (needs the operand buffer sizes for the TMA
+    descriptors).  The fused-epilogue engine stages stay on single-CTA tiles: measured
+    slower in pairs (C4 8.3 vs 7.4 ms/epoch, C3 0.34 vs 0.29 ms; the pair's tile is
+    epilogue-bound and 2 CTAs/SM already overlap epilogue with main loop)."""
+    return (PAIR and mode == N.GEMM_I32 and sizes is not None and EPOCH is None and b_npad >= 64
+            and row_blocks_total * max(1, b_npad // 256) >= 2 * sm_count())
+
+
 def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: int, out_npad: int, epi_struct,
-           keep: list, work: float = 0.0, a_bits: bool = False):
-    """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m)."""
+           keep: list, work: float = 0.0, a_bits: bool = False, sizes=None):
+    """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m).
+    ``sizes``: per segment (A source bytes, B source bytes), enabling the 2-SM pair path."""
     rbs = [-(-s.m // TILE) for s in segs]
-    bn = choose_bn(b_npad, sum(rbs)) if EPOCH is None else choose_bn_fused(b_npad, sum(rbs), sm_count())
+    pair = use_pair(b_npad, sum(rbs), sizes, mode) and not a_bits
+    if pair:
+        bn = max(64, min(256, b_npad))
+    else:
+        bn = choose_bn(b_npad, sum(rbs)) if EPOCH is None else choose_bn_fused(b_npad, sum(rbs), sm_count())
     n_tiles = b_npad // bn
     begin = 0
     for s, r in zip(segs, rbs):
         s.cta_begin = begin
-        begin += r * n_tiles
+        begin += (-(-r // 2) if pair else r) * n_tiles
+    if pair:
+        begin *= 2                                   # CTAs = 2 x pairs; cta_begin counts pairs
+        bh = bn // 2
+        for sg, (abytes, bbytes) in zip(segs, sizes):
+            N.check(_lib().qg_encode_linear_map(sg.a, abytes, 128, ctypes.byref(sg.tmap_a)), "qg_encode_linear_map")
+            N.check(_lib().qg_encode_linear_map(sg.b, bbytes, bh, ctypes.byref(sg.tmap_b)), "qg_encode_linear_map")
     table = SegTable(segs)
     keep.append(table)
     args = TiledArgs()
@@ -339,6 +366,7 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     args.b_npad, args.n, args.bn, args.n_tiles = b_npad, n, bn, n_tiles
     args.mode, args.out_layout, args.out_npad = mode, out_layout, out_npad
     args.a_bits = int(bool(a_blocks and a_bits))
+    args.pair = int(pair)
     if epi_struct is not None:
         args.epi = ctypes.pointer(epi_struct)
     if not begin:
@@ -401,8 +429,9 @@ def bmm_reduced(a, x, *, out: torch.Tensor | None = None) -> torch.Tensor:
     seg.out_i32 = out.data_ptr()
     keep = []
     # row blocks with no non-zero K tile are written as zeros by the kernel (nk = 0)
+    sizes = None if a_bits else [(blk.nblocks * 16384, xt.numel())]
     launch([seg], a_blocks=True, b_npad=npad_of(n), n=n, mode=N.GEMM_I32, out_layout=0, out_npad=0,
-           epi_struct=None, keep=keep, work=2.0 * 1024 * (-(-n // 8) * 8) * blk.nz8, a_bits=a_bits)
+           epi_struct=None, keep=keep, work=2.0 * 1024 * (-(-n // 8) * 8) * blk.nz8, a_bits=a_bits, sizes=sizes)
     out._qg_keep = keep           # the segment table must outlive the (async) launch
     return out
 

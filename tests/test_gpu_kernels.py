@@ -250,3 +250,29 @@ def test_requant_screen_is_bit_identical_on_configs(name, bits):
     off = _forward_screen(batches, model, False)
     for x, y in zip(on, off):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("pair", [True, False])
+def test_bmm_reduced_pair_path_large(pair):
+    """The 2-SM (cta_group::2, TMA-signalled) pair path of bmm_reduced at a size that
+    selects it: block-sparse A with empty row blocks (union schedule + zero blocks) and
+    an odd number of row blocks; result == dense product, and == the single-CTA path."""
+    from paper_2111_09547_b200 import tiled
+    g = torch.Generator(device="cuda").manual_seed(3)
+    m, k, n, bits = 4000, 2500, 4096, 5
+    dense = (torch.rand((m, k), generator=g, device="cuda") < 0.02).to(torch.uint8)
+    dense[:1000, 1200:] = 0
+    dense[2600:3000] = 0                                  # empty row blocks
+    dense[3000:, :600] = 0
+    codes = torch.randint(0, 1 << bits, (k, n), generator=g, device="cuda", dtype=torch.uint8)
+    a = bg.pack_colwise(dense)
+    tiles, pitch = tiled.tiles_from_codes(codes, k, n, n, "right")
+    x = tiled.TiledCodeStack(bg.ROW_WISE, k, n, bits, tiles, "right", pitch)
+    old = tiled.PAIR
+    tiled.PAIR = pair
+    try:
+        got = tiled.bmm_reduced(a, x)
+    finally:
+        tiled.PAIR = old
+    want = (dense.double() @ codes.double()).to(torch.int64)
+    assert torch.equal(got.to(torch.int64), want)
