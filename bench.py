@@ -425,8 +425,9 @@ def ours(args, world, rank):
         from c5_sweep import run_point
         c5 = run_point(args.c5_n, 0.1, args.bits, reps=10, int8_peak=peak)
         c5.update({"bound": "tensor", "peak": peak, "unit": "TOPS",
+                   "kernel": "tc_pair_kernel (2-SM cluster, tcgen05.mma.cta_group::2.kind::i8 M=256, TMA)",
                    "config": "C5: A Bernoulli(0.1) 1-bit x X uniform codes, reduce_bitplanes(bmm_1bit_by_nbit) "
-                             "in one tc_tiled_kernel launch, CUDA-graph replays timed with CUDA events"})
+                             "in one launch, CUDA-graph replays timed with CUDA events"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
