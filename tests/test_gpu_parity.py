@@ -265,3 +265,24 @@ def test_bindings_match_golden():
     ha.release()
     with pytest.raises(ValueError, match="released"):
         bb.to_val(ha)
+
+
+@pytest.mark.parametrize("variant", ["fused_epoch", "a_bits", "screen", "default"])
+@pytest.mark.parametrize("i", [0, 3, 5])
+def test_opt_in_kernel_variants_match_golden(variant, i):
+    """The opt-in engine variants (persistent fused epoch, in-smem adjacency expansion,
+    affine requant screen) stay bit-exact against the reference logits."""
+    from paper_2111_09547_b200 import engine, tiled
+    c = model_case(load("model"), i)
+    batch, _ = _batch_from_case(c)
+    model = _model_from_case(c)
+    saved = (engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN)
+    try:
+        engine.FUSED_EPOCH = variant == "fused_epoch"
+        tiled.A_BITS = variant == "a_bits"
+        engine.SCREEN = variant == "screen"
+        if variant == "a_bits":
+            batch.adjacency._blocked = None          # rebuild the blocks for the packed-operand path
+        np.testing.assert_array_equal(bg.model_forward(batch, model), c.logits)
+    finally:
+        engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN = saved
