@@ -617,8 +617,8 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.pdl_wait = false;
 }
 
-template <int TMEM_COLS>
-__global__ void __launch_bounds__(kTThreads) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
+template <int TMEM_COLS, int MINB>
+__global__ void __launch_bounds__(kTThreads, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
   __shared__ uint32_t tmem_base_s;
@@ -1144,12 +1144,12 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
 
 static inline int tstatus() { return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA; }
 
-template <int COLS>
+template <int COLS, int MINB>
 static void tiled_attr(size_t bytes) {
   static size_t done = 0;
   if (bytes > done) {
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     done = bytes;
   }
@@ -1159,8 +1159,9 @@ static void tiled_attr(size_t bytes) {
 // still running; the kernel's griddepcontrol.wait (after its prologue) orders every
 // read of predecessor outputs, so launch latency + TMEM/barrier setup overlap the
 // previous layer's tail.  Captured into CUDA graphs as programmatic edges.
-template <int COLS>
+template <int COLS, int MINB>
 static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
+  tiled_attr<COLS, MINB>(smem);
   static const bool pdl = getenv("QG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1172,7 +1173,7 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS>, P);
+  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB>, P);
 }
 
 // qg_tiled_args -> kernel parameters; returns the per-column constant bytes the
@@ -1288,15 +1289,36 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   }
   const size_t stage = P.a_bits ? ((16384 + (size_t)P.bn * 128 + 2048 + 1023) & ~(size_t)1023)
                                 : 16384 + (size_t)P.bn * 128;
-  P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
+  // Occupancy: 2 CTAs/SM by default (one CTA's fp64 epilogue overlaps the other's main
+  // loop).  Stages with N tiles <= 128 and >= 3 CTAs per SM of work run 3 CTAs/SM
+  // (80-register variant, 72 KB ring, 3 x <= 128 TMEM columns): more warps hide the
+  // epilogue's latency (C3: 0.29 -> 0.25 ms/epoch).
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const bool env_budget = getenv("QG_TILED_SMEM_KB") != nullptr;
+  const bool three = !env_budget && P.bn <= 128 && a->total_ctas >= 3 * (int64_t)sms;
+  const size_t budget = three ? 72 * 1024 : smem_budget();
+  P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = (unsigned)a->total_ctas;
-  switch (P.bn) {
-    case 32: tiled_attr<32>(smem); launch_tiled<32>(P, grid, smem, st); break;
-    case 64: tiled_attr<64>(smem); launch_tiled<64>(P, grid, smem, st); break;
-    case 128: tiled_attr<128>(smem); launch_tiled<128>(P, grid, smem, st); break;
-    default: tiled_attr<256>(smem); launch_tiled<256>(P, grid, smem, st); break;
+  if (three) {
+    switch (P.bn) {
+      case 32: launch_tiled<32, 3>(P, grid, smem, st); break;
+      case 64: launch_tiled<64, 3>(P, grid, smem, st); break;
+      default: launch_tiled<128, 3>(P, grid, smem, st); break;
+    }
+  } else {
+    switch (P.bn) {
+      case 32: launch_tiled<32, 2>(P, grid, smem, st); break;
+      case 64: launch_tiled<64, 2>(P, grid, smem, st); break;
+      case 128: launch_tiled<128, 2>(P, grid, smem, st); break;
+      default: launch_tiled<256, 2>(P, grid, smem, st); break;
+    }
   }
   return tstatus();
 }
@@ -1326,11 +1348,11 @@ static int launch_epoch(EpochParams& EP, size_t smem, int64_t max_tiles, cudaStr
     cudaFuncGetAttributes(&fa, tc_tiled_epoch_kernel<COLS>);
     int per_sm_single = 0;
     cudaFuncAttributes fb{};
-    cudaFuncGetAttributes(&fb, tc_tiled_kernel<COLS>);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncGetAttributes(&fb, tc_tiled_kernel<COLS, 2>);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_single, tc_tiled_kernel<COLS>, kTThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_single, tc_tiled_kernel<COLS, 2>, kTThreads, smem);
     int smem_sm = 0, smem_blk = 0, p2 = 0, p3 = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
