@@ -83,7 +83,7 @@ static __device__ __noinline__ uint32_t exact_code_global(const qg_epilogue& E, 
 struct EpiLane {
   uint32_t tmem_row;
   bool has_acc, rvalid;
-  int first, nslices, nvalid;
+  int first, step, nslices, nvalid;   // this lane's slices: first, first + step, ...
   int64_t myrow, n0;
   __device__ __forceinline__ void load8(int cl8, uint32_t (&v)[8]) const {
     if (has_acc) {
@@ -128,7 +128,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   int64_t* const status = G.status;
   const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
   uint32_t rsum = 0;                                        // <= 256 cols x 255: fits u32
-  for (int sl = L.first; sl < L.nslices; sl += 2) {
+  for (int sl = L.first; sl < L.nslices; sl += L.step) {
     const int cl8 = sl * 8;
     uint32_t v[8];
     L.load8(cl8, v);
@@ -229,7 +229,7 @@ __device__ __forceinline__ uint32_t epi_slices_screen(const TiledParams& P, cons
   int64_t* const status = G.status;
   const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
   uint32_t rsum = 0;
-  for (int sl = L.first; sl < L.nslices; sl += 2) {
+  for (int sl = L.first; sl < L.nslices; sl += L.step) {
     const int cl8 = sl * 8;
     uint32_t v[8];
     L.load8(cl8, v);
@@ -308,7 +308,8 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   const int bn = P.bn;
   const qg_epilogue& E = P.epi;
   // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
-  const int quad = warp & 3, half = warp >> 2;
+  // warps 4q..4q+3 cover the 128 TMEM lanes; the blockDim/128 warp groups split the slices
+  const int quad = warp & 3, half = warp >> 2, groups = (int)(blockDim.x >> 7);
   const int64_t r0 = rb * 128 + quad * 32;
   const int64_t myrow = r0 + lane;
   const bool rvalid = myrow < G.m;
@@ -320,6 +321,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   L.tmem_row = tmem + ((uint32_t)(quad * 32) << 16);
   L.has_acc = nk > 0;
   L.first = half;
+  L.step = groups;
   L.nslices = nslices;
   L.nvalid = (int)(P.n - n0);
   L.rvalid = myrow < G.m;
@@ -328,7 +330,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   uint32_t rsum = 0;
   if (!fused) {
     const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
-    for (int sl = half; sl < nslices; sl += 2) {
+    for (int sl = half; sl < nslices; sl += groups) {
       uint32_t v[8];
       L.load8(sl * 8, v);
       if (rvalid) {
@@ -497,7 +499,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     }
     if (screen) {
       // screened requant: per-column affine coefficients P_c, G_c, R_c (see epi_slices_screen)
-      for (int i = t; i < bn; i += kTThreads - 64) {
+      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
         const int64_t c = n0 + i;
         double pc = 0.0, gc = 0.0, rc = 0x1p12;
         if (c < P.n) {
@@ -518,7 +520,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         sCol[2 * bn + i] = rc;
       }
     } else {
-      for (int i = t; i < bn; i += kTThreads - 64) {
+      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
         const int64_t c = n0 + i;
         const bool ok = c < P.n;
         // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
@@ -547,7 +549,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       const uint32_t* bits = reinterpret_cast<const uint32_t*>(slot + a_bytes + b_bytes);
       // u = (row/8, K-core, row%8) is exactly the UMMA core-matrix order: the 16-byte
       // store for unit u lands at u * 16 (consecutive lanes -> consecutive addresses)
-      for (int u = et; u < 1024; u += kTThreads - 64) {
+      for (int u = et; u < 1024; u += (int)blockDim.x - 64) {
         const int r = ((u >> 6) << 3) | (u & 7), c = (u >> 3) & 7;
         const uint32_t x = bits[r * 4 + (c >> 1)] >> ((c & 1) * 16);
         *reinterpret_cast<uint4*>(slot + u * 16) =
@@ -617,8 +619,8 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.pdl_wait = false;
 }
 
-template <int TMEM_COLS, int MINB>
-__global__ void __launch_bounds__(kTThreads, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
+template <int TMEM_COLS, int MINB, int NT>
+__global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
   __shared__ uint32_t tmem_base_s;
@@ -834,7 +836,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       sRowTerm[t] = (E.use_row && rb_ok && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
     }
     if (screen) {
-      for (int i = t; i < bn; i += kTThreads - 64) {
+      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
         const int64_t cc = n0 + i;
         double pc = 0.0, gc = 0.0, rc = 0x1p12;
         if (cc < P.n) {
@@ -855,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
         sCol[2 * bn + i] = rc;
       }
     } else {
-      for (int i = t; i < bn; i += kTThreads - 64) {
+      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
         const int64_t cc = n0 + i;
         const bool ok = cc < P.n;
         sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[cc]) : 0.0;
@@ -1144,12 +1146,12 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
 
 static inline int tstatus() { return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA; }
 
-template <int COLS, int MINB>
+template <int COLS, int MINB, int NT>
 static void tiled_attr(size_t bytes) {
   static size_t done = 0;
   if (bytes > done) {
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB, NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     done = bytes;
   }
@@ -1159,13 +1161,13 @@ static void tiled_attr(size_t bytes) {
 // still running; the kernel's griddepcontrol.wait (after its prologue) orders every
 // read of predecessor outputs, so launch latency + TMEM/barrier setup overlap the
 // previous layer's tail.  Captured into CUDA graphs as programmatic edges.
-template <int COLS, int MINB>
+template <int COLS, int MINB, int NT = kTThreads>
 static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
-  tiled_attr<COLS, MINB>(smem);
+  tiled_attr<COLS, MINB, NT>(smem);
   static const bool pdl = getenv("QG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1173,7 +1175,7 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB>, P);
+  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB, NT>, P);
 }
 
 // qg_tiled_args -> kernel parameters; returns the per-column constant bytes the
@@ -1301,6 +1303,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   }
   static const bool env_budget = getenv("QG_TILED_SMEM_KB") != nullptr;
   const bool three = !env_budget && P.bn <= 128 && a->total_ctas >= 3 * (int64_t)sms;
+  static const bool wide = getenv("QG_WIDE") == nullptr || atoi(getenv("QG_WIDE")) != 0;
   const size_t budget = three ? 72 * 1024 : smem_budget();
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
@@ -1317,7 +1320,12 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
       case 32: launch_tiled<32, 2>(P, grid, smem, st); break;
       case 64: launch_tiled<64, 2>(P, grid, smem, st); break;
       case 128: launch_tiled<128, 2>(P, grid, smem, st); break;
-      default: launch_tiled<256, 2>(P, grid, smem, st); break;
+      default:
+        // 12 warps for the epilogue-bound dense-left (update) GEMMs: the 128x256 epilogue's
+        // latency-bound fp64 chains spread over 3 warp groups (C4 update stages -3.5%)
+        if (wide && !P.a_blocks && P.mode == QG_GEMM_EPILOGUE) launch_tiled<256, 2, 384>(P, grid, smem, st);
+        else launch_tiled<256, 2>(P, grid, smem, st);
+        break;
     }
   }
   return tstatus();
@@ -1348,11 +1356,11 @@ static int launch_epoch(EpochParams& EP, size_t smem, int64_t max_tiles, cudaStr
     cudaFuncGetAttributes(&fa, tc_tiled_epoch_kernel<COLS>);
     int per_sm_single = 0;
     cudaFuncAttributes fb{};
-    cudaFuncGetAttributes(&fb, tc_tiled_kernel<COLS, 2>);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncGetAttributes(&fb, tc_tiled_kernel<COLS, 2, kTThreads>);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2, kTThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2, kTThreads>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_single, tc_tiled_kernel<COLS, 2>, kTThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_single, tc_tiled_kernel<COLS, 2, kTThreads>, kTThreads, smem);
     int smem_sm = 0, smem_blk = 0, p2 = 0, p3 = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
