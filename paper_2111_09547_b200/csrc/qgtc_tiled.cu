@@ -1018,6 +1018,7 @@ __global__ void __launch_bounds__(256) block_expand_kernel(const uint32_t* __res
 // segment by binary search on block_begin, then the same expansion + degrees.
 __global__ void __launch_bounds__(256) block_expand_grouped_kernel(const qg_block_seg* __restrict__ segs, int nsegs,
                                                                    int64_t total_blocks) {
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t gb = blockIdx.x;
   if (gb >= total_blocks) return;
   int lo = 0, hi = nsegs - 1;
@@ -1078,6 +1079,9 @@ __global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t
 // sums reduce over the unit's 128 columns before one atomic per row.
 __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
                                                           int nplanes, int right) {
+  // the first GEMM (PDL-launched) may start its prologue + static-operand prefetch now;
+  // it reads this kernel's output only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ __align__(16) uint8_t tile[32][128 + 16];
   int lo = 0, hi = nsegs - 1;
   while (lo < hi) {
