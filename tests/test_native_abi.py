@@ -5,6 +5,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 from paper_2111_09547_b200 import _native as N
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -75,3 +77,39 @@ def test_counter_closed_forms_match_the_oracle():
     # argument errors are host-side status codes, no GPU involved
     assert lib.qg_bmm_counters(2, 2, 5, 1, 1, 1, 1, ctypes.byref(out)) == N.QG_ERR_ARG
     assert lib.qg_batch_h2d(None, 16, None, None) == N.QG_ERR_ARG
+
+
+def _build_capi_demo(tmp_path):
+    import shutil
+    import subprocess
+
+    from paper_2111_09547_b200 import _native as N
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(N.LIB_PATH)
+    exe = str(tmp_path / "capi_demo")
+    cmd = ["gcc", "-O2", "-I", os.path.join(root, "include"), os.path.join(root, "examples", "capi_demo.c"),
+           "-L", lib_dir, "-lqgtc_b200", "-L/usr/local/cuda/lib64", "-lcudart", "-lm",
+           f"-Wl,-rpath,{lib_dir}", "-Wl,-rpath,/usr/local/cuda/lib64", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_plain_c_consumer_builds_and_runs_host_only(tmp_path):
+    """A plain-C host (examples/capi_demo.c) compiles against include/qgtc_b200.h, links the
+    library and gets the reference counter closed forms through the C-ABI."""
+    import subprocess
+    exe = _build_capi_demo(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "host-only checks OK" in out.stdout
+
+
+@pytest.mark.gpu
+def test_plain_c_consumer_device_bit_qnt(tmp_path):
+    import subprocess
+    exe = _build_capi_demo(tmp_path)
+    out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "device bit_qnt: OK" in out.stdout
