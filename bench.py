@@ -466,7 +466,10 @@ def ours(args, world, rank):
         "e2e": {"value": round(e2e_ms, 5), "unit": "ms/epoch", "h2d_bytes_per_step": host.h2d_bytes,
                 "d2h_bytes_per_step": host.d2h_bytes, "wall_ms_per_step": round(e2e_wall / args.steps, 5),
                 "parity_vs_device_path": "bit-exact" if e2e_parity else "MISMATCH",
-                "path": "ONE CUDA graph per step: pinned QGT3 images (schedule + non-zero 128x128 adjacency blocks + feature planes) -> 1 H2D -> block expansion + epoch -> fp64 logits -> 1 D2H"},
+                "path": ("ONE CUDA graph per step: pinned QGT3 images (schedule + non-zero 128x128 adjacency "
+                         "blocks + feature planes) -> H2D -> block expansion + epoch -> fp64 logits -> D2H"
+                         + (f"; {host.chunks} batch chunks pipelined (H2D / compute / D2H overlapped on "
+                            "two copy engines)" if host.chunks > 1 else "; one H2D and one D2H"))},
         "gpu_launches": launches,
         "clocks": clocks,
     }

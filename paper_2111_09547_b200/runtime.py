@@ -142,7 +142,7 @@ class HostEpochRunner:
     QGT3 (graph.pack_batch_v3) ships only the non-zero 128x128 adjacency blocks,
     so the H2D carries the zero-tile-jumping schedule instead of the dense bits."""
 
-    def __init__(self, model: ModelConfig, batches: list, **kw):
+    def __init__(self, model: ModelConfig, batches: list, chunks: int | None = None, **kw):
         self.model = model
         images = [pack_batch_v3(b) for b in batches]
         self.offsets = np.cumsum([0] + [len(im) for im in images])
@@ -156,7 +156,79 @@ class HostEpochRunner:
         self.out_host = torch.empty((rows, self.classes), dtype=torch.float64).pin_memory()
         self.h2d_bytes = int(self.offsets[-1])
         self.d2h_bytes = rows * self.classes * 8
-        self.inner = EpochRunner(model, views, rescan=True, **kw).capture(pre=self._h2d, post=self._d2h)
+        # multi-batch epochs: pipeline the H2D (copy engine 1), the compute and the D2H (copy
+        # engine 2) over chunks of batches -- PCIe is full duplex, so the input and output
+        # transfers of different chunks overlap each other and the compute
+        auto = 1 if len(views) < 8 else (4 if len(views) < 64 else 8)
+        k = chunks if chunks is not None else auto
+        self.chunks = max(1, min(k, len(views)))
+        if self.chunks > 1:
+            self._capture_pipelined(views)
+        else:
+            self.inner = EpochRunner(model, views, rescan=True, **kw).capture(pre=self._h2d, post=self._d2h)
+
+    def _capture_pipelined(self, views):
+        from .engine import _prepared, model_forward_group
+        from .tiled import GroupedRefresh, blocked, weight_tiles
+        groups = [list(g) for g in np.array_split(np.arange(len(views)), self.chunks)]
+        _prepared(self.model)
+        for ly, prep in zip(self.model.layers, _prepared(self.model)):
+            weight_tiles(ly, prep)
+        refresh = [GroupedRefresh([blocked(views[i].adjacency) for i in g]) for g in groups]
+        row0 = np.cumsum([0] + [v.total_nodes for v in views])
+        self._stream = torch.cuda.Stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def forward(capturing: bool):
+            outs_all = []
+            ev_in = [torch.cuda.Event() for _ in groups]
+            if capturing:
+                with torch.cuda.stream(s_in):
+                    s_in.wait_stream(self._stream)
+                    for gi, g in enumerate(groups):
+                        a, b = int(self.offsets[g[0]]), int(self.offsets[g[-1] + 1])
+                        self.device[a:b].copy_(self.host[a:b], non_blocking=True)
+                        ev_in[gi].record(s_in)
+            for gi, g in enumerate(groups):
+                if capturing:
+                    self._stream.wait_event(ev_in[gi])
+                refresh[gi].run()
+                outs = model_forward_group([views[i] for i in g], self.model, verify=not capturing)
+                outs_all += outs
+                if capturing:
+                    done = torch.cuda.Event()
+                    done.record(self._stream)
+                    with torch.cuda.stream(s_out):
+                        s_out.wait_event(done)
+                        self._copy_rows(outs, int(row0[g[0]]))
+            if capturing:
+                self._stream.wait_stream(s_in)
+                self._stream.wait_stream(s_out)
+            return outs_all
+
+        with torch.cuda.stream(self._stream):
+            plan = N.SlabPlan()
+            N.ALLOC = plan
+            try:
+                forward(False)
+            finally:
+                N.ALLOC = N.TorchAlloc()
+            torch.cuda.synchronize()
+            self._slabs = N.SlabAlloc(plan)
+            self._graph = torch.cuda.CUDAGraph()
+            N.ALLOC = self._slabs
+            try:
+                with torch.cuda.graph(self._graph, stream=self._stream):
+                    self._slabs.reset()
+                    self._logits = forward(True)
+            except BaseException:
+                N.STATIC_COPIES.clear()
+                raise
+            finally:
+                N.ALLOC = N.TorchAlloc()
+            N.flush_static_copies()
+        self.inner = None
+        self._keep = (refresh, s_in, s_out)
 
     def _h2d(self):
         # the step's single H2D through the C-ABI (qg_batch_h2d; a memcpy node in the graph)
@@ -164,22 +236,27 @@ class HostEpochRunner:
                 "qg_batch_h2d")
 
     def _d2h(self, outs):
-        # the engine writes every batch's logits into one allocation (row-contiguous, batch
-        # order): one strided view over it -> ONE D2H for the epoch
+        self._copy_rows(outs, 0)
+
+    def _copy_rows(self, outs, row0: int):
+        """D2H of consecutive batches' logits into out_host[row0:]: the engine writes a
+        launch's logits into one allocation (row-contiguous, batch order), so one strided
+        view over it -> ONE copy."""
+        rows = sum(o.shape[0] for o in outs)
         contiguous = bool(outs) and all(o.is_contiguous() for o in outs) and all(
             b.data_ptr() == a.data_ptr() + a.numel() * a.element_size() for a, b in zip(outs, outs[1:]))
-        if contiguous and sum(o.shape[0] for o in outs) == self.out_host.shape[0]:
-            whole = outs[0].as_strided(tuple(self.out_host.shape), (self.out_host.shape[1], 1))
-            self.out_host.copy_(whole, non_blocking=True)
+        if contiguous:
+            whole = outs[0].as_strided((rows, self.out_host.shape[1]), (self.out_host.shape[1], 1))
+            self.out_host[row0:row0 + rows].copy_(whole, non_blocking=True)
             return
-        r = 0
+        r = row0
         for o in outs:
             self.out_host[r:r + o.shape[0]].copy_(o, non_blocking=True)
             r += o.shape[0]
 
     @property
     def stream(self):
-        return self.inner.stream
+        return self.inner.stream if self.inner is not None else self._stream
 
     def load(self, images) -> None:
         """Place a step's QGT3 images into the pinned staging area (host memcpy)."""
@@ -190,7 +267,10 @@ class HostEpochRunner:
         """H2D + epoch + D2H: one graph launch on the runner's stream; returns the pinned logits
         (valid after the stream synchronises)."""
         with torch.cuda.stream(self.stream):
-            self.inner.run()
+            if self.inner is not None:
+                self.inner.run()
+            else:
+                self._graph.replay()
         return self.out_host
 
 

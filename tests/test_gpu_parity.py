@@ -286,3 +286,26 @@ def test_opt_in_kernel_variants_match_golden(variant, i):
         np.testing.assert_array_equal(bg.model_forward(batch, model), c.logits)
     finally:
         engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN = saved
+
+
+def test_pipelined_e2e_runner_equals_single_graph():
+    """The chunked e2e runner (H2D / compute / D2H of batch chunks overlapped on two copy
+    engines) returns the same fp64 logits as the single-transfer runner, bit for bit."""
+    import torch
+
+    from paper_2111_09547_b200 import synth
+    from paper_2111_09547_b200.runtime import HostEpochRunner
+    cfg = synth.with_bits(synth.CONFIGS["C3"], 4)
+    batches, feats, _ = synth.planted_batches(cfg, seed=2, batch_ids=range(10))
+    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=2)
+    one = HostEpochRunner(model, batches, chunks=1)
+    piped = HostEpochRunner(model, batches, chunks=3)
+    assert piped.chunks == 3
+    a = one.run_host()
+    one.stream.synchronize()
+    for _ in range(2):
+        b = piped.run_host()
+        piped.stream.synchronize()
+        assert torch.equal(a, b)
+    dev = torch.cat([o.cpu() for o in bg.engine.model_forward_group(batches, model)])
+    assert torch.equal(a, dev)
