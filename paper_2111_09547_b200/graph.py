@@ -416,6 +416,13 @@ def pack_batch_v3(b: SubgraphBatch) -> bytes:
     return bytes(out)
 
 
+def v3_feature_offset(image: bytes) -> int:
+    """Byte offset of the feature-plane section inside a QGT3 image (the last section)."""
+    (_m, _v, _f, ns, total, fbits, _x, _r, _a, _b, _apr, _apc, fpr, fpc, _d, nrb, nb,
+     _nz) = _V3_HEADER.unpack_from(image)
+    return _v3_layout(ns, total, nrb, nb, fbits * fpr * fpc // 32)[7]
+
+
 class BlockSparseAdjacency(PackedBitMatrix):
     """Column-wise 1-bit adjacency known only by its non-zero 128x128 blocks (QGT3).
 

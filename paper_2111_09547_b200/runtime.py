@@ -30,7 +30,7 @@ class EpochRunner:
     """Graph-captured epoch of ``model_forward`` over ``batches``."""
 
     def __init__(self, model: ModelConfig, batches: list, *, jump: bool = True, reuse: str = "cross-tile",
-                 stream: torch.cuda.Stream | None = None, rescan: bool = True):
+                 stream: torch.cuda.Stream | None = None, rescan: bool = True, external_refresh: bool = False):
         self.model = model
         self.batches = list(batches)
         self.jump, self.reuse = jump, reuse
@@ -39,13 +39,14 @@ class EpochRunner:
         # rescan=True re-gathers and re-expands the adjacency blocks from the current
         # words inside every epoch (new data each step, e2e path).
         self.rescan = rescan
+        self.external_refresh = external_refresh   # the caller's pre() re-expands the blocks
         self.stream = stream or torch.cuda.Stream()
         self.graph = None
         self.logits = None
         self._keep = []
 
     def _forward_all(self, verify: bool):
-        if self.rescan:
+        if self.rescan and not self.external_refresh:
             from .tiled import GroupedRefresh, blocked
             blks = [blocked(b.adjacency) for b in self.batches]
             if all(not getattr(k, "_gather", True) for k in blks):
@@ -162,10 +163,25 @@ class HostEpochRunner:
         auto = 1 if len(views) < 8 else (4 if len(views) < 64 else 8)
         k = chunks if chunks is not None else auto
         self.chunks = max(1, min(k, len(views)))
+        from .engine import UPDATE_THEN_AGGREGATE
         if self.chunks > 1:
             self._capture_pipelined(views)
-        else:
+        elif model.layers[0].order != UPDATE_THEN_AGGREGATE:
+            # aggregate-first (GCN): the first GEMM needs the blocks -> nothing to overlap
             self.inner = EpochRunner(model, views, rescan=True, **kw).capture(pre=self._h2d, post=self._d2h)
+        else:
+            # split H2D: the feature sections first on the compute stream (entry conversion
+            # and a GIN layer's update GEMM need only them); the schedule + adjacency blocks
+            # on a side stream (second copy engine) with the block expansion behind them --
+            # the first aggregation GEMM joins it (tiled.PENDING_JOIN)
+            from .graph import v3_feature_offset
+            from .tiled import GroupedRefresh, blocked
+            self._feat_off = [int(o) + v3_feature_offset(im) for im, o in zip(images, self.offsets)]
+            self._grouped = GroupedRefresh([blocked(v.adjacency) for v in views])
+            self._grouped.run()                       # degrees valid for the eager recording pass
+            self._s_in = torch.cuda.Stream()
+            self.inner = EpochRunner(model, views, rescan=True, external_refresh=True, **kw).capture(
+                pre=self._h2d_split, post=self._d2h_join)
 
     def _capture_pipelined(self, views):
         from .engine import _prepared, model_forward_group
@@ -234,6 +250,29 @@ class HostEpochRunner:
         # the step's single H2D through the C-ABI (qg_batch_h2d; a memcpy node in the graph)
         N.check(N.lib().qg_batch_h2d(self.host.data_ptr(), self.host.numel(), self.device.data_ptr(), N.stream()),
                 "qg_batch_h2d")
+
+    def _h2d_split(self):
+        from . import tiled
+        main = torch.cuda.current_stream()
+        self._s_in.wait_stream(main)
+        for i, f0 in enumerate(self._feat_off):
+            end = int(self.offsets[i + 1])
+            if end > f0:
+                self.device[f0:end].copy_(self.host[f0:end], non_blocking=True)
+        with torch.cuda.stream(self._s_in):
+            for i, f0 in enumerate(self._feat_off):
+                a = int(self.offsets[i])
+                self.device[a:f0].copy_(self.host[a:f0], non_blocking=True)
+            self._grouped.run()
+            ev = torch.cuda.Event()
+            ev.record(self._s_in)
+        tiled.PENDING_JOIN = ev
+
+    def _d2h_join(self, outs):
+        from . import tiled
+        tiled.PENDING_JOIN = None
+        torch.cuda.current_stream().wait_stream(self._s_in)      # side stream rejoins (no-op if joined)
+        self._copy_rows(outs, 0)
 
     def _d2h(self, outs):
         self._copy_rows(outs, 0)

@@ -70,6 +70,10 @@ _SIGS_DONE = False
 # When a list, launch() records stage arguments instead of launching (engine's fused
 # epoch); flush_epoch() then issues them as qg_tiled_epoch launches.
 EPOCH = None
+
+# An event the first adjacency-block launch must wait on (the e2e runner's side-stream
+# H2D of the schedule + blocks and their expansion); cleared once joined.
+PENDING_JOIN = None
 MAX_EPOCH_STAGES = 8
 
 # QG_A_BITS=1: adjacency blocks reach the GEMM packed (2 KB per 128x128 block) and are
@@ -371,6 +375,10 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
         args.epi = ctypes.pointer(epi_struct)
     if not begin:
         return
+    global PENDING_JOIN
+    if a_blocks and PENDING_JOIN is not None:
+        torch.cuda.current_stream().wait_event(PENDING_JOIN)
+        PENDING_JOIN = None
     if EPOCH is not None:
         # deferred: flush_epoch() launches every recorded stage in ONE persistent kernel
         EPOCH.append((args, work, table))
