@@ -41,7 +41,7 @@ INT8_PEAK_FILE = os.path.join(ROOT, "profiles", "int8_peak.json")
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--steps", type=int, default=1000)
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--config", default="C2")
     p.add_argument("--bits", type=int, default=4)
@@ -90,7 +90,7 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index=0, period=0.002):
+    def __init__(self, index=0, period=0.0005):
         self.samples, self.reasons, self.period = [], set(), period
         self.ok = False
         try:
