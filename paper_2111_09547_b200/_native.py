@@ -233,7 +233,10 @@ class SlabAlloc:
         """Per-forward re-initialisation (inside the captured graph)."""
         self.i = 0
         self.slabs["volatile"].zero_()
-        self.slabs["status"].view(torch.int64).fill_(STATUS_CLEAR)
+        # a fill KERNEL, not a memset node: measured 2-3 us faster per C2 epoch (the next
+        # node is a kernel)
+        st = self.slabs["status"]
+        check(lib().qg_status_reset(st.data_ptr(), st.numel() // 8, stream()), "qg_status_reset")
 
     def take(self, shape, dtype, kind):
         if self.i >= len(self.seq) or self.seq[self.i][0] != shape or self.seq[self.i][1] != dtype:
