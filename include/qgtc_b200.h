@@ -69,6 +69,10 @@ int qg_version(void);
 /* Reset `n` int64 status cells to "no error" (0x7f7f.. > any index). */
 int qg_status_reset(int64_t* status, int64_t n, void* stream);
 
+/* Per-forward reset of a runtime's slabs in one kernel: `zero` (nzero int64 words,
+ * the atomic accumulators) := 0, `status` (nstatus cells) := the clear pattern. */
+int qg_slab_reset(int64_t* zero, int64_t nzero, int64_t* status, int64_t nstatus, void* stream);
+
 /*
  * Fused Eq.2 quantization + bit decomposition + packing (bit_qnt).
  * Replaces quantize_matrix (quantize.py:93-105) + bit_decompose

@@ -361,6 +361,24 @@ static inline int launch_status() {
 static inline bool bad_pad(int pad) { return pad != 8 && pad != 128; }
 static inline int64_t pad_up(int64_t n, int64_t m) { return (n + m - 1) / m * m; }
 
+// Per-epoch slab reset in ONE kernel: zero the accumulator slab, clear the status slab.
+__global__ void slab_reset_kernel(int64_t* zero, int64_t nz, int64_t* status, int64_t ns) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz + ns; i += stride) {
+    if (i < nz) zero[i] = 0;
+    else status[i - nz] = 0x7f7f7f7f7f7f7f7fLL;
+  }
+}
+
+extern "C" int qg_slab_reset(int64_t* zero, int64_t nzero, int64_t* status, int64_t nstatus, void* stream) {
+  if (nzero < 0 || nstatus < 0 || (nzero && !zero) || (nstatus && !status)) return QG_ERR_ARG;
+  const int64_t n = nzero + nstatus;
+  if (n == 0) return QG_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 1184);
+  slab_reset_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(zero, nzero, status, nstatus);
+  return launch_status();
+}
+
 extern "C" int qg_status_reset(int64_t* status, int64_t n, void* stream) {
   if (!status || n < 0) return QG_ERR_ARG;
   if (n == 0) return QG_OK;
