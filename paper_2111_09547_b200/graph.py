@@ -22,7 +22,7 @@ import torch
 
 from . import _native as N
 from .bitpack import (COLUMN_WISE, ROW_WISE, BitPlaneStack, PackedBitMatrix, _HEADER as _STACK_HEADER,
-                      deserialize, pad8, pad128, serialize)
+                      pad8, pad128, serialize)
 from .errors import FormatError
 from .quantize import QuantParams, quantize_pack_device
 
