@@ -290,7 +290,25 @@ typedef struct {
   int32_t pair;                /* 1: CTA pairs (cluster of 2) with cta_group::2 MMAs, M = 256;
                                   segs[].cta_begin then counts PAIRS, total_ctas = 2 x pairs,
                                   bn >= 64 (each CTA stages bn/2 columns of B)             */
+  const struct qg_chain* chain; /* optional: fuse a dense stage-2 GEMM behind this stage   */
 } qg_tiled_args;
+
+/* Chained stage 2 of a tiled GEMM (qg_tiled_args.chain): the GIN aggregate -> update
+ * pair (engine.py:282-334, layer order AGGREGATE_THEN_UPDATE) in one launch.  Stage 1
+ * (n_tiles == 1, EPILOGUE mode, packed output) requantizes its 128-row tile into u8
+ * codes that stay in shared memory as the LEFT operand of stage 2, whose right operand
+ * is `w` (right-tiled, K = stage-1 n); stage 2's epilogue uses the code row sums of
+ * that tile.  segs[].q_codes / q_row_sums / out_real / status are then stage 2's
+ * outputs; stage 1's codes are never written to HBM. */
+typedef struct qg_chain {
+  const uint8_t* w;            /* right-tiled stage-2 operand (slab pitch w_npad * 128)  */
+  int64_t w_npad;              /* padded N of w: power of two 32..256                    */
+  int64_t n;                   /* stage-2 logical output columns (<= w_npad)             */
+  int32_t out_layout;          /* 0 fp64 row-major, 2 right-tiled codes                  */
+  int32_t pad_;
+  int64_t out_npad;            /* right-tiled output: padded N                           */
+  const qg_epilogue* epi;      /* stage-2 epilogue                                       */
+} qg_chain;
 
 /* Warp-specialised tiled bit-GEMM (cp.async.bulk producer, single-thread
  * tcgen05.mma kind::i8 issuer, 8-warp fused epilogue).  Same arithmetic as

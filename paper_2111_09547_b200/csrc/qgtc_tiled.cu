@@ -38,6 +38,13 @@ struct TiledParams {
   int64_t total_ctas;       // work items (segment, row block, N tile) of this stage
   int32_t a_bits;           // 1: adjacency blocks are shipped packed (2 KB) and expanded in smem
   int32_t pair;             // 1: CTA pairs (cluster of 2) run cta_group::2 MMAs, M = 256
+  int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
+  // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
+  // codes, which never leave shared memory (needs n_tiles == 1)
+  int32_t chain, bn2, k2, out_layout2;
+  int64_t n2, out_npad2, w2_npad;
+  const uint8_t* w2;
+  qg_epilogue epi2;
 };
 
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
@@ -49,6 +56,7 @@ static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       P.phase_ns[tile * 8 + 6] = (int64_t)smid;
+      P.phase_ns[tile * 8 + 7] = 0;             // chained launches overwrite it (stage-2 accumulator ready)
     }
   }
 }
@@ -104,11 +112,14 @@ struct EpiLane {
 // Dequant: ((((k_acc*acc) + rows) + cols) + const) + bias -- the reference's
 // grouping (bitgemm.py:156-160); absent terms are +0.0 (exact, see sCol fill).
 // Returns this lane's requantized code sum (packed output) for the row sums.
-template <int ACT, bool HAS_BN, bool ROW_ONLY>
+// ST: 0 = this stage to global memory; 1 = chained stage 1, codes into the shared
+// memory operand of stage 2 (mid[k tile]); 2 = chained stage 2 (P.epi2, bn2, n2).
+template <int ACT, bool HAS_BN, bool ROW_ONLY, int ST>
 __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
-                                               const double* __restrict__ sCol, double rterm) {
-  const qg_epilogue& E = P.epi;
-  const int bn = P.bn;
+                                               const double* __restrict__ sCol, double rterm, uint8_t* mid0,
+                                               uint8_t* mid1) {
+  const qg_epilogue& E = ST == 2 ? P.epi2 : P.epi;
+  const int bn = ST == 2 ? P.bn2 : P.bn;
   const double* sC = sCol;
   const double* sB = sCol + bn;
   const double* sMean = sCol + 2 * bn;
@@ -120,13 +131,14 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   const bool packed = E.out_kind == QG_OUT_PLANES;
   const uint32_t maxv = packed ? (1u << E.q_bits) - 1u : 0u;
   const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
-  const int out_layout = P.out_layout;
+  const int out_layout = ST == 2 ? P.out_layout2 : P.out_layout;
   // segment fields in registers (G lives in global memory; the code stores below
   // could alias it, so the compiler would otherwise reload every slice)
   uint8_t* const q_codes = G.q_codes;
   double* const out_real = G.out_real;
   int64_t* const status = G.status;
-  const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
+  const int64_t r128 = G.r128, out_npad = ST == 2 ? P.out_npad2 : P.out_npad, pn = ST == 2 ? P.n2 : P.n;
+  const int lrow = (int)(L.myrow & 127);
   uint32_t rsum = 0;                                        // <= 256 cols x 255: fits u32
   for (int sl = L.first; sl < L.nslices; sl += L.step) {
     const int cl8 = sl * 8;
@@ -184,6 +196,14 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
     const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
     rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    if (ST == 1) {
+      // stage 2's LEFT operand in shared memory (UMMA K-major core matrices, one 16 KB
+      // slot per 128 K columns); rows past m hold zeros (their stage-2 rows are not stored)
+      uint8_t* slab = (cl8 >> 7) ? mid1 : mid0;
+      *reinterpret_cast<uint2*>(slab + (lrow >> 3) * 1024 + ((cl8 & 127) >> 4) * 128 + (lrow & 7) * 16 +
+                                (cl8 & 15)) = make_uint2(lo, hi);
+      continue;
+    }
     if (L.rvalid) {
       const int64_t cb = L.n0 + cl8;
       if (out_layout == 1) {
@@ -300,20 +320,24 @@ struct TileRing {
 
 // Epilogue of one 128-row x bn tile held in this CTA's TMEM: 8-column slices over all
 // 8 warps, fused dequant/BN/act/requant (or fp64 / int32 output); the lane's code row
-// sum is accumulated into R.sRowSum (flushed to global by the caller).
+// sum is accumulated into R.sRowSum (flushed to global by the caller).  ST as in
+// epi_slices (1: chained stage 1 into mid0/mid1; 2: chained stage 2).
+template <int ST>
 __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tseg& G, TileRing& R, int64_t tile,
                                               int64_t rb, int64_t n0, int nk, uint32_t tmem, const double* sCol,
-                                              bool fused, bool screen) {
+                                              bool fused, bool screen, uint8_t* mid0 = nullptr,
+                                              uint8_t* mid1 = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bn = P.bn;
-  const qg_epilogue& E = P.epi;
+  const int bn = ST == 2 ? P.bn2 : P.bn;
+  const int64_t pn = ST == 2 ? P.n2 : P.n;
+  const qg_epilogue& E = ST == 2 ? P.epi2 : P.epi;
   // ---------------- epilogue: 8-column TMEM slices over all 8 warps ----------------
   // warps 4q..4q+3 cover the 128 TMEM lanes; the blockDim/128 warp groups split the slices
   const int quad = warp & 3, half = warp >> 2, groups = (int)(blockDim.x >> 7);
   const int64_t r0 = rb * 128 + quad * 32;
   const int64_t myrow = r0 + lane;
   const bool rvalid = myrow < G.m;
-  const int64_t rem_cols = P.n - n0;
+  const int64_t rem_cols = pn - n0;
   const int ncols_cta = rem_cols <= 0 ? 0 : (rem_cols < bn ? (int)rem_cols : bn);
   const int nslices = (ncols_cta + 7) >> 3;
   const bool packed = fused && E.out_kind == QG_OUT_PLANES;
@@ -323,12 +347,12 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   L.first = half;
   L.step = groups;
   L.nslices = nslices;
-  L.nvalid = (int)(P.n - n0);
+  L.nvalid = (int)(pn - n0);
   L.rvalid = myrow < G.m;
   L.myrow = myrow;
   L.n0 = n0;
   uint32_t rsum = 0;
-  if (!fused) {
+  if (ST == 0 && !fused) {
     const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
     for (int sl = half; sl < nslices; sl += groups) {
       uint32_t v[8];
@@ -350,12 +374,12 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
     // one uniform dispatch per tile: the slice loop below is straight-line per variant
     const double rterm = rvalid ? R.sRowTerm[quad * 32 + lane] : 0.0;
     const bool row_only = !E.use_col && !E.use_const && !E.bias;
-    if (screen) {
+    if (ST == 0 && screen) {
       rsum = E.act == QG_ACT_RELU ? epi_slices_screen<true>(P, G, L, sCol, rterm)
                                   : epi_slices_screen<false>(P, G, L, sCol, rterm);
     } else switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
 #define QG_EPI_CASE(i, A, B, Rw) \
-  case i: rsum = epi_slices<A, B, Rw>(P, G, L, sCol, rterm); break;
+  case i: rsum = epi_slices<A, B, Rw, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
       QG_EPI_CASE(0, QG_ACT_NONE, false, false)
       QG_EPI_CASE(1, QG_ACT_NONE, false, true)
       QG_EPI_CASE(2, QG_ACT_NONE, true, false)
@@ -367,16 +391,17 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
       QG_EPI_CASE(8, QG_ACT_TANH, false, false)
       QG_EPI_CASE(9, QG_ACT_TANH, false, true)
       QG_EPI_CASE(10, QG_ACT_TANH, true, false)
-      default: rsum = epi_slices<QG_ACT_TANH, true, true>(P, G, L, sCol, rterm); break;
+      default: rsum = epi_slices<QG_ACT_TANH, true, true, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
 #undef QG_EPI_CASE
     }
   }
-  if (packed && G.q_row_sums && rsum) atomicAdd(&R.sRowSum[quad * 32 + lane], (unsigned long long)rsum);
+  if (packed && (ST == 1 || G.q_row_sums) && rsum)
+    atomicAdd(&R.sRowSum[quad * 32 + lane], (unsigned long long)rsum);
 }
 
 // One work item: (segment, 128-row block, N tile) -> fused GEMM tile.  Ends with a
 // CTA barrier so the next tile may overwrite TMEM / shared staging.
-template <int TMEM_COLS>
+template <int TMEM_COLS, bool CHAIN>
 __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, TileRing& R) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bn = P.bn, S = R.S;
@@ -395,10 +420,10 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const int64_t n0 = (int64_t)nt * bn;
 
   // stage = [A: 16 KB UMMA bytes][B: bn x 128 B][a_bits: 2 KB packed bit block]
-  const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u;
+  const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u, slot_b = (uint32_t)P.slot_bn * 128u;
   const bool abits = P.a_blocks && P.a_bits;
   uint8_t* stage0 = R.stage0;
-  const uint32_t stage_bytes = abits ? ((a_bytes + b_bytes + 2048u + 1023u) & ~1023u) : a_bytes + b_bytes;
+  const uint32_t stage_bytes = abits ? ((a_bytes + slot_b + 2048u + 1023u) & ~1023u) : a_bytes + slot_b;
   double* sCol = R.sCol;
   uint64_t* full = R.full;
   uint64_t* empty = R.empty;
@@ -412,8 +437,10 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
 
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
-  const bool screen = fused && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
+  const bool screen = fused && !CHAIN && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
                       (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
+  // chained stage 2: per-column constants after stage 1's (screen is off when chained)
+  double* sCol2 = sCol + (E.bn_mean ? 6 : 2) * bn;
   if (tid < 128) R.sRowSum[tid] = 0ull;
   if (tid == 0) tstamp(P, tile, 1);
 
@@ -432,7 +459,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         uint64_t* fb = &full[(it0 + it) % S];
         if (abits) {
           mbar_expect_tx(fb, 2048u + b_bytes);
-          bulk_g2s(dst + a_bytes + b_bytes, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
+          bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
         } else if (P.a_blocks) {
           mbar_expect_tx(fb, a_bytes + b_bytes);
           bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
@@ -463,7 +490,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         // 2 KB packed block -> staging; the expander warps build the 16 KB operand
         kt = G.blk_kt[kbase + it];
         mbar_expect_tx(&full[s], 2048u + b_bytes);
-        bulk_g2s(dst + a_bytes + b_bytes, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
+        bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
       } else {
         if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
         else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
@@ -471,6 +498,18 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         bulk_g2s(dst, asrc, a_bytes, &full[s]);
       }
       bulk_g2s(dst + a_bytes, bbase + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
+    }
+    if (CHAIN) {
+      // stage 2's (static) right operand, one K tile per ring position after stage 1's;
+      // its left operand is written into the same slots by the stage-1 epilogue
+      const uint32_t wb = (uint32_t)P.bn2 * 128u;
+      for (int j = 0; j < P.k2; ++j) {
+        const uint32_t g = it0 + (uint32_t)nk + (uint32_t)j;
+        const int s = (int)(g % (uint32_t)S);
+        if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
+        mbar_expect_tx(&full[s], wb);
+        bulk_g2s(stage0 + (size_t)s * stage_bytes + a_bytes, P.w2 + (int64_t)j * (P.w2_npad << 7), wb, &full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
@@ -536,6 +575,21 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         }
       }
     }
+    if (CHAIN) {
+      const qg_epilogue& E2 = P.epi2;
+      const int bn2 = P.bn2;
+      for (int i = t; i < bn2; i += (int)blockDim.x - 64) {
+        const bool ok = i < P.n2;
+        sCol2[0 * bn2 + i] = (ok && E2.use_col) ? __dmul_rn(E2.k_col, (double)E2.col_sums[i]) : 0.0;
+        sCol2[1 * bn2 + i] = (ok && E2.bias) ? E2.bias[i] : 0.0;
+        if (E2.bn_mean) {
+          sCol2[2 * bn2 + i] = ok ? E2.bn_mean[i] : 0.0;
+          sCol2[3 * bn2 + i] = ok ? E2.bn_denom[i] : 1.0;
+          sCol2[4 * bn2 + i] = ok ? E2.bn_gamma[i] : 0.0;
+          sCol2[5 * bn2 + i] = ok ? E2.bn_beta[i] : 0.0;
+        }
+      }
+    }
   }
   if (abits && warp >= 2) {
     // expander warps: packed 128x128 bit block -> UMMA K-major 0/1 bytes (16 KB) per
@@ -546,7 +600,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       const int s = (int)(g % (uint32_t)S);
       mbar_wait(smem_u32(&full[s]), (g / S) & 1);
       uint8_t* slot = stage0 + (size_t)s * stage_bytes;
-      const uint32_t* bits = reinterpret_cast<const uint32_t*>(slot + a_bytes + b_bytes);
+      const uint32_t* bits = reinterpret_cast<const uint32_t*>(slot + a_bytes + slot_b);
       // u = (row/8, K-core, row%8) is exactly the UMMA core-matrix order: the 16-byte
       // store for unit u lands at u * 16 (consecutive lanes -> consecutive addresses)
       for (int u = et; u < 1024; u += (int)blockDim.x - 64) {
@@ -575,12 +629,60 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   __syncthreads();   // sCol / row terms / zeroed row sums visible to all epilogue warps
   if (tid == 0) tstamp(P, tile, 3);
 
-  tile_epilogue(P, G, R, tile, rb, n0, nk, tmem, sCol, fused, screen);
-  if (tid == 0) tstamp(P, tile, 4);
-  if (P.mode == QG_GEMM_EPILOGUE && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
+  if (CHAIN) {
+    // ---- chained stage 2: stage 1's codes -> shared memory -> dense GEMM -> epilogue 2
+    const uint32_t itc = R.it0;                          // ring position of stage-2 K tile 0
+    R.it0 += (uint32_t)P.k2;
+    uint8_t* mid0 = stage0 + (size_t)(itc % (uint32_t)S) * stage_bytes;
+    uint8_t* mid1 = stage0 + (size_t)((itc + 1) % (uint32_t)S) * stage_bytes;
+    tile_epilogue<1>(P, G, R, tile, rb, 0, nk, tmem, sCol, true, false, mid0, mid1);
+    // generic-proxy code stores -> visible to the tensor core; TMEM reads retired
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[tid])
-      atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const qg_epilogue& E2 = P.epi2;
+    if (tid < 128) {
+      // stage 2's row terms: RN(k_row * code row sum), the sums of the codes just written
+      const int64_t row = rb * 128 + tid;
+      R.sRowTerm[tid] = (E2.use_row && row < G.m) ? __dmul_rn(E2.k_row, (double)R.sRowSum[tid]) : 0.0;
+      R.sRowSum[tid] = 0ull;
+    }
+    if (warp == 1 && lane == 0) {
+      const uint32_t idesc2 = idesc_u8(P.bn2);
+      for (int j = 0; j < P.k2; ++j) {
+        const uint32_t g = itc + (uint32_t)j;
+        const int s = (int)(g % (uint32_t)S);
+        mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_i8(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc2, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(R.done);
+    }
+    mbar_wait(smem_u32(R.done), R.ndone & 1);
+    R.ndone += 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    __syncthreads();                                     // stage-2 row terms visible
+    if (tid == 0) tstamp(P, tile, 7);
+    tile_epilogue<2>(P, G, R, tile, rb, 0, P.k2, tmem, sCol2, true, false);
+    if (tid == 0) tstamp(P, tile, 4);
+    if (E2.out_kind == QG_OUT_PLANES && G.q_row_sums) {
+      __syncthreads();
+      if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[tid])
+        atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
+    }
+  } else {
+    tile_epilogue<0>(P, G, R, tile, rb, n0, nk, tmem, sCol, fused, screen);
+    if (tid == 0) tstamp(P, tile, 4);
+    if (P.mode == QG_GEMM_EPILOGUE && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
+      __syncthreads();
+      if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[tid])
+        atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -619,7 +721,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.pdl_wait = false;
 }
 
-template <int TMEM_COLS, int MINB, int NT>
+template <int TMEM_COLS, int MINB, int NT, bool CHAIN = false>
 __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
@@ -631,8 +733,8 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
   tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
-                         P.a_bits ? ((16384u + (uint32_t)P.bn * 128u + 2048u + 1023u) & ~1023u)
-                                  : 16384u + (uint32_t)P.bn * 128u);
+                         P.a_bits ? ((16384u + (uint32_t)P.slot_bn * 128u + 2048u + 1023u) & ~1023u)
+                                  : 16384u + (uint32_t)P.slot_bn * 128u);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -640,7 +742,7 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   // the predecessor grid's outputs (activations, row sums) are read only after
   // griddepcontrol.wait, issued per role inside the tile (static operands prefetch first)
   R.pdl_wait = true;
-  tiled_tile<TMEM_COLS>(P, (int64_t)blockIdx.x, R);
+  tiled_tile<TMEM_COLS, CHAIN>(P, (int64_t)blockIdx.x, R);
   if ((threadIdx.x >> 5) == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
 }
@@ -879,7 +981,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   __syncthreads();
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 3);
   if (rb_ok) {
-    tile_epilogue(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused, screen);
+    tile_epilogue<0>(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused, screen);
     if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
     if (fused && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
       __syncthreads();
@@ -958,7 +1060,7 @@ __global__ void __maxnreg__(112) tc_tiled_epoch_kernel(const __grid_constant__ E
     // first tile static (every CTA has one while tiles last), the rest claimed dynamically
     for (int64_t tile = blockIdx.x; tile < P.total_ctas;
          tile = (int64_t)gridDim.x + next_tile(EP.grid_bar + 1 + st, &s_tile))
-      tiled_tile<TMEM_COLS>(P, tile, R);
+      tiled_tile<TMEM_COLS, false>(P, tile, R);
     if (st + 1 < EP.nstages) grid_sync(EP.grid_bar, gridDim.x, gen);
   }
   if ((threadIdx.x >> 5) == 0)
@@ -1150,12 +1252,12 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
 
 static inline int tstatus() { return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA; }
 
-template <int COLS, int MINB, int NT>
+template <int COLS, int MINB, int NT, bool CHAIN>
 static void tiled_attr(size_t bytes) {
   static size_t done = 0;
   if (bytes > done) {
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB, NT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB, NT, CHAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(tc_tiled_kernel<COLS, MINB, NT, CHAIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     done = bytes;
   }
@@ -1165,9 +1267,9 @@ static void tiled_attr(size_t bytes) {
 // still running; the kernel's griddepcontrol.wait (after its prologue) orders every
 // read of predecessor outputs, so launch latency + TMEM/barrier setup overlap the
 // previous layer's tail.  Captured into CUDA graphs as programmatic edges.
-template <int COLS, int MINB, int NT = kTThreads>
+template <int COLS, int MINB, int NT = kTThreads, bool CHAIN = false>
 static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
-  tiled_attr<COLS, MINB, NT>(smem);
+  tiled_attr<COLS, MINB, NT, CHAIN>(smem);
   static const bool pdl = getenv("QG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1179,7 +1281,7 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB, NT>, P);
+  cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB, NT, CHAIN>, P);
 }
 
 // qg_tiled_args -> kernel parameters; returns the per-column constant bytes the
@@ -1201,9 +1303,33 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.total_ctas = a->total_ctas;
   P.a_bits = a->a_blocks ? a->a_bits : 0;
   P.pair = a->pair;
+  P.slot_bn = P.bn;
   const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
                       (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
-  return (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
+  size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
+  if (a->chain) {
+    const qg_chain* c = a->chain;
+    // stage 1: one N tile covering all its columns, packed codes, no screen, byte blocks
+    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != 1 || a->n > a->bn || a->pair || P.a_bits || screen ||
+        a->epi->out_kind != QG_OUT_PLANES)
+      { rc = QG_ERR_UNSUPPORTED; return 0; }
+    if (!c->w || !c->epi || c->w_npad < 32 || c->w_npad > 256 || (c->w_npad & (c->w_npad - 1)) || c->n < 1 ||
+        c->n > c->w_npad || (c->out_layout != 0 && c->out_layout != 2) ||
+        (c->out_layout == 0) != (c->epi->out_kind == QG_OUT_REAL))
+      { rc = QG_ERR_ARG; return 0; }
+    P.chain = 1;
+    P.bn2 = (int32_t)c->w_npad;
+    P.k2 = (int32_t)((a->n + 127) / 128);
+    P.n2 = c->n;
+    P.out_layout2 = c->out_layout;
+    P.out_npad2 = c->out_npad;
+    P.w2 = c->w;
+    P.w2_npad = c->w_npad;
+    P.epi2 = *c->epi;
+    P.slot_bn = std::max(P.bn, P.bn2);
+    cols += (c->epi->bn_mean ? 6 : 2) * (size_t)P.bn2 * 8;
+  }
+  return cols;
 }
 
 // the kernel is epilogue-heavy: size the ring so TWO CTAs fit per SM (one CTA's fp64
@@ -1293,8 +1419,8 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     }
     return tstatus();
   }
-  const size_t stage = P.a_bits ? ((16384 + (size_t)P.bn * 128 + 2048 + 1023) & ~(size_t)1023)
-                                : 16384 + (size_t)P.bn * 128;
+  const size_t stage = P.a_bits ? ((16384 + (size_t)P.slot_bn * 128 + 2048 + 1023) & ~(size_t)1023)
+                                : 16384 + (size_t)P.slot_bn * 128;
   // Occupancy: 2 CTAs/SM by default (one CTA's fp64 epilogue overlaps the other's main
   // loop).  Stages with N tiles <= 128 and >= 3 CTAs per SM of work run 3 CTAs/SM
   // (80-register variant, 72 KB ring, 3 x <= 128 TMEM columns): more warps hide the
@@ -1306,28 +1432,51 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   static const bool env_budget = getenv("QG_TILED_SMEM_KB") != nullptr;
-  const bool three = !env_budget && P.bn <= 128 && a->total_ctas >= 3 * (int64_t)sms;
+  // TMEM columns: the widest accumulator (stage 1 or the chained stage 2)
+  const int tcols = P.slot_bn;
+  const bool three = !env_budget && !P.chain && tcols <= 128 && a->total_ctas >= 3 * (int64_t)sms;
   static const bool wide = getenv("QG_WIDE") == nullptr || atoi(getenv("QG_WIDE")) != 0;
   const size_t budget = three ? 72 * 1024 : smem_budget();
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = (unsigned)a->total_ctas;
-  if (three) {
-    switch (P.bn) {
+  if (P.chain) {
+    // chained aggregate -> update: one tile per CTA.  A chained stage has half the CTAs of
+    // the split-N stages it replaces and two epilogues per tile: with fewer tiles than
+    // SMs, 16 warps (1 CTA/SM) split the epilogue slices 4 ways
+    static const int chain_nt = getenv("QG_CHAIN_NT") ? atoi(getenv("QG_CHAIN_NT")) : 0;
+    const bool wide16 = chain_nt == 512 || (chain_nt == 0 && a->total_ctas <= (int64_t)sms);
+    if (wide16) {
+      switch (tcols) {
+        case 32: launch_tiled<32, 1, 512, true>(P, grid, smem, st); break;
+        case 64: launch_tiled<64, 1, 512, true>(P, grid, smem, st); break;
+        case 128: launch_tiled<128, 1, 512, true>(P, grid, smem, st); break;
+        default: launch_tiled<256, 1, 512, true>(P, grid, smem, st); break;
+      }
+    } else {
+      switch (tcols) {
+        case 32: launch_tiled<32, 2, kTThreads, true>(P, grid, smem, st); break;
+        case 64: launch_tiled<64, 2, kTThreads, true>(P, grid, smem, st); break;
+        case 128: launch_tiled<128, 2, kTThreads, true>(P, grid, smem, st); break;
+        default: launch_tiled<256, 2, kTThreads, true>(P, grid, smem, st); break;
+      }
+    }
+  } else if (three) {
+    switch (tcols) {
       case 32: launch_tiled<32, 3>(P, grid, smem, st); break;
       case 64: launch_tiled<64, 3>(P, grid, smem, st); break;
       default: launch_tiled<128, 3>(P, grid, smem, st); break;
     }
   } else {
-    switch (P.bn) {
+    switch (tcols) {
       case 32: launch_tiled<32, 2>(P, grid, smem, st); break;
       case 64: launch_tiled<64, 2>(P, grid, smem, st); break;
       case 128: launch_tiled<128, 2>(P, grid, smem, st); break;
       default:
         // 12 warps for the epilogue-bound dense-left (update) GEMMs: the 128x256 epilogue's
         // latency-bound fp64 chains spread over 3 warp groups (C4 update stages -3.5%)
-        if (wide && !P.a_blocks && P.mode == QG_GEMM_EPILOGUE) launch_tiled<256, 2, 384>(P, grid, smem, st);
+        if (wide && !P.a_blocks && !P.chain && P.mode == QG_GEMM_EPILOGUE) launch_tiled<256, 2, 384>(P, grid, smem, st);
         else launch_tiled<256, 2>(P, grid, smem, st);
         break;
     }
@@ -1400,6 +1549,7 @@ extern "C" int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint
   int64_t max_tiles = 1;
   for (int i = 0; i < nstages; ++i) {
     int rc;
+    if (stages[i].chain) return QG_ERR_UNSUPPORTED;
     const size_t cols = tiled_params(&stages[i], EP.st[i], rc);
     if (rc != QG_OK) return rc;
     cols_max = std::max(cols_max, cols);

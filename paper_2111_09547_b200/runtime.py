@@ -86,13 +86,16 @@ class EpochRunner:
                 self.stamps = []
                 if stamps:
                     bitgemm.PHASE_HOOK = self.stamps
+                from . import tiled
+                n0 = tiled.LAUNCHES
                 with torch.cuda.graph(self.graph, stream=self.stream):
                     if pre is not None:
                         pre()
-                    self.slabs.reset()              # 1 memset + 1 fill per epoch
+                    self.slabs.reset()              # one slab-reset kernel per epoch
                     self.logits = self._forward_all(verify=False)
                     if post is not None:
                         post(self.logits)
+                self.gemm_launches = tiled.LAUNCHES - n0
             except BaseException:
                 N.STATIC_COPIES.clear()         # tables of a failed capture must never be copied later
                 raise
@@ -120,13 +123,20 @@ class EpochRunner:
         return out
 
     def kernel_launches_per_epoch(self) -> int:
-        """Native (libqgtc_b200) kernels per epoch: 1 grouped entry conversion + the GEMM
-        stages (2 per layer) as one persistent epoch kernel per 8 stages; with rescan, per batch the block expansion (+ the gather
-        from dense words unless the blocks were shipped, QGT3)."""
+        """Native (libqgtc_b200) kernels per epoch: the slab reset, 1 grouped entry
+        conversion and the GEMM launches of the captured graph (2 per layer, fewer where
+        stage pairs are chained, one persistent kernel per 8 stages with FUSED_EPOCH);
+        with rescan, per batch the block expansion (+ the gather from dense words unless
+        the blocks were shipped, QGT3)."""
         from . import engine
         from .tiled import MAX_EPOCH_STAGES, blocked
         stages = 2 * len(self.model.layers)
-        per_epoch = 1 + (-(-stages // MAX_EPOCH_STAGES) if engine.FUSED_EPOCH else stages)
+        gemms = getattr(self, "gemm_launches", None)
+        if engine.FUSED_EPOCH:
+            gemms = -(-stages // MAX_EPOCH_STAGES)
+        elif gemms is None:
+            gemms = stages
+        per_epoch = 2 + gemms
         if self.rescan:
             blks = [blocked(b.adjacency) for b in self.batches]
             if all(not getattr(k, "_gather", True) for k in blks):

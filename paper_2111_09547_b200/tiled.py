@@ -62,7 +62,15 @@ class TiledArgs(ctypes.Structure):
                 ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
                 ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p), ("a_bits", ctypes.c_int32),
-                ("pair", ctypes.c_int32)]
+                ("pair", ctypes.c_int32), ("chain", ctypes.c_void_p)]
+
+
+class Chain(ctypes.Structure):
+    """Mirror of ``qg_chain``: a dense stage-2 GEMM fused behind a tiled stage."""
+
+    _fields_ = [("w", ctypes.c_void_p), ("w_npad", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("out_layout", ctypes.c_int32), ("pad_", ctypes.c_int32), ("out_npad", ctypes.c_int64),
+                ("epi", ctypes.POINTER(N.Epilogue))]
 
 
 _SIGS_DONE = False
@@ -70,6 +78,9 @@ _SIGS_DONE = False
 # When a list, launch() records stage arguments instead of launching (engine's fused
 # epoch); flush_epoch() then issues them as qg_tiled_epoch launches.
 EPOCH = None
+
+# qg_tiled_gemm launches issued so far (runtime.EpochRunner counts those of its graph)
+LAUNCHES = 0
 
 # An event the first adjacency-block launch must wait on (the e2e runner's side-stream
 # H2D of the schedule + blocks and their expansion); cleared once joined.
@@ -346,12 +357,17 @@ def use_pair(b_npad: int, row_blocks_total: int, sizes, mode: int) -> bool:
 
 
 def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: int, out_npad: int, epi_struct,
-           keep: list, work: float = 0.0, a_bits: bool = False, sizes=None):
+           keep: list, work: float = 0.0, a_bits: bool = False, sizes=None, chain: Chain | None = None):
     """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m).
-    ``sizes``: per segment (A source bytes, B source bytes), enabling the 2-SM pair path."""
+    ``sizes``: per segment (A source bytes, B source bytes), enabling the 2-SM pair path.
+    ``chain``: fuse a dense stage-2 GEMM behind this stage (one N tile, see qg_chain)."""
     rbs = [-(-s.m // TILE) for s in segs]
-    pair = use_pair(b_npad, sum(rbs), sizes, mode) and not a_bits
-    if pair:
+    pair = chain is None and use_pair(b_npad, sum(rbs), sizes, mode) and not a_bits
+    if chain is not None:
+        if b_npad > 256 or a_bits or EPOCH is not None:
+            raise ValueError("chained stage needs one N tile <= 256, byte blocks, per-stage launches")
+        bn = b_npad
+    elif pair:
         bn = max(64, min(256, b_npad))
     else:
         bn = choose_bn(b_npad, sum(rbs)) if EPOCH is None else choose_bn_fused(b_npad, sum(rbs), sm_count())
@@ -376,6 +392,9 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     args.pair = int(pair)
     if epi_struct is not None:
         args.epi = ctypes.pointer(epi_struct)
+    if chain is not None:
+        args.chain = ctypes.addressof(chain)
+        keep.append(chain)
     if not begin:
         return
     global PENDING_JOIN
@@ -387,9 +406,13 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
         EPOCH.append((args, work, table))
         keep.append(args)
         return
+    global LAUNCHES
+    LAUNCHES += 1
     from . import bitgemm
     if bitgemm.PHASE_HOOK is not None:
-        stamps = torch.zeros((begin, 8), dtype=torch.int64, device=N.device())
+        # no memset: a memset node inside a captured epoch would cut the PDL edge between the
+        # GEMM launches (every CTA writes all 8 slots; slot 7 is 0 unless the launch is chained)
+        stamps = torch.empty((begin, 8), dtype=torch.int64, device=N.device())
         args.phase_ns = stamps.data_ptr()
         bitgemm.PHASE_HOOK.append((stamps, work))
     if bitgemm.PROFILE_HOOK is not None:

@@ -113,3 +113,40 @@ def test_plain_c_consumer_device_bit_qnt(tmp_path):
     out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "device bit_qnt: OK" in out.stdout
+
+
+def test_ctypes_struct_layouts_match_the_header(tmp_path):
+    """Every ctypes mirror of a header struct has the C compiler's size and field
+    offsets (a drifted mirror would pass garbage through the C ABI)."""
+    import shutil
+
+    from paper_2111_09547_b200 import tiled
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    mirrors = {"qg_epilogue": N.Epilogue, "qg_gemm_args": N.GemmArgs, "qg_tseg": tiled.TSeg,
+               "qg_tiled_args": tiled.TiledArgs, "qg_chain": tiled.Chain, "qg_entry_seg": tiled.EntrySeg,
+               "qg_block_seg": tiled.BlockSeg}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "qgtc_b200.h"', "int main(void) {"]
+    for cname, cls in mirrors.items():
+        lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True,
+                   capture_output=True, text=True)
+    got = {}
+    for line in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.splitlines():
+        cname, field, val = line.split()
+        got[cname, field] = int(val)
+    for cname, cls in mirrors.items():
+        assert got[cname, "sizeof"] == ctypes_sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[cname, fname] == getattr(cls, fname).offset, (cname, fname)
+
+
+def ctypes_sizeof(cls):
+    import ctypes
+    return ctypes.sizeof(cls)

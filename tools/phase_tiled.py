@@ -1,6 +1,6 @@
 """Per-CTA phase timeline of the tiled GEMM launches of one epoch (%globaltimer stamps):
 0 entry, 1 setup done, 2 first K tile landed (MMA thread), 3 accumulator ready,
-4 epilogue done, 5 exit.      python tools/phase_tiled.py [C2] [bits]"""
+4 epilogue done, 5 exit, 7 (chained launches) stage-2 accumulator ready.      python tools/phase_tiled.py [C2] [bits]"""
 import os
 import sys
 
@@ -34,4 +34,10 @@ for i, (st, _) in enumerate(rec):
           f"  first-tile {d[:, 1].mean():.2f}({d[:, 1].max():.2f})  mainloop {d[:, 2].mean():.2f}({d[:, 2].max():.2f})"
           f"  epilogue {d[:, 3].mean():.2f}({d[:, 3].max():.2f})  teardown {d[:, 4].mean():.2f}({d[:, 4].max():.2f})"
           + (f"  gap-from-prev {(t0 - prev_end) / 1e3:.2f}us" if prev_end is not None else ""))
+    if (s[:, 7] > 0).all():
+        # chained launch: stamp 7 = stage-2 accumulator ready (after epilogue 1 + stage-2 MMAs)
+        e1 = (s[:, 7] - s[:, 3]) / 1e3
+        e2 = (s[:, 4] - s[:, 7]) / 1e3
+        print(f"          chained: epilogue-1 + stage-2 MMA {e1.mean():.2f}({e1.max():.2f})"
+              f"  epilogue-2 {e2.mean():.2f}({e2.max():.2f})")
     prev_end = s[:, 5].max()
