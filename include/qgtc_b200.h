@@ -293,9 +293,10 @@ typedef struct {
   const struct qg_chain* chain; /* optional: fuse a dense stage-2 GEMM behind this stage   */
 } qg_tiled_args;
 
-/* Chained stage 2 of a tiled GEMM (qg_tiled_args.chain): the GIN aggregate -> update
- * pair (engine.py:282-334, layer order AGGREGATE_THEN_UPDATE) in one launch.  Stage 1
- * (n_tiles == 1, EPILOGUE mode, packed output) requantizes its 128-row tile into u8
+/* Chained stage 2 of a tiled GEMM (qg_tiled_args.chain): an aggregation and the update
+ * that consumes its rows (engine.py:282-334: aggregate -> update inside a GCN layer, or
+ * a GIN layer's aggregation -> the next layer's update) in one launch.  Stage 1
+ * (n_tiles == 1, or 2 with split; EPILOGUE mode, packed output) requantizes its tile into u8
  * codes that stay in shared memory as the LEFT operand of stage 2, whose right operand
  * is `w` (right-tiled, K = stage-1 n); stage 2's epilogue uses the code row sums of
  * that tile.  segs[].q_codes / q_row_sums / out_real / status are then stage 2's
@@ -305,7 +306,9 @@ typedef struct qg_chain {
   int64_t w_npad;              /* padded N of w: power of two 32..256                    */
   int64_t n;                   /* stage-2 logical output columns (<= w_npad)             */
   int32_t out_layout;          /* 0 fp64 row-major, 2 right-tiled codes                  */
-  int32_t pad_;
+  int32_t split;               /* 1: a cluster of 2 CTAs per 128-row block (n_tiles == 2),
+                                  each computing half of both stages' columns; the stage-1
+                                  codes are exchanged through distributed shared memory  */
   int64_t out_npad;            /* right-tiled output: padded N                           */
   const qg_epilogue* epi;      /* stage-2 epilogue                                       */
 } qg_chain;

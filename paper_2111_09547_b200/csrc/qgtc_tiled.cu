@@ -40,7 +40,10 @@ struct TiledParams {
   int32_t pair;             // 1: CTA pairs (cluster of 2) run cta_group::2 MMAs, M = 256
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
-  // codes, which never leave shared memory (needs n_tiles == 1)
+  // codes, which never leave shared memory.  chain 1: one CTA per row block (n_tiles 1);
+  // chain 2: a cluster of 2 CTAs per row block, each computing half of both stages' N
+  // (n_tiles 2) and writing its stage-1 codes into both CTAs' shared memory (DSMEM).
+  // bn2 = this CTA's stage-2 N tile (half of w2_npad when chain == 2)
   int32_t chain, bn2, k2, out_layout2;
   int64_t n2, out_npad2, w2_npad;
   const uint8_t* w2;
@@ -62,6 +65,24 @@ static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile
 }
 
 constexpr int kTThreads = 256;
+
+// distributed shared memory (cluster peers): this CTA's smem address -> the peer's copy
+__device__ __forceinline__ uint32_t peer_addr(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_peer_v2(uint32_t cluster_addr, uint32_t lo, uint32_t hi) {
+  asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(cluster_addr), "r"(lo), "r"(hi) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_peer_u64(uint32_t cluster_addr) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 // exact requant of one element with the non-finite report (rare path, kept out of line)
 static __device__ __noinline__ uint32_t requant_exact(double x, double amin, double scale, double inv, uint32_t maxv,
@@ -92,6 +113,7 @@ struct EpiLane {
   uint32_t tmem_row;
   bool has_acc, rvalid;
   int first, step, nslices, nvalid;   // this lane's slices: first, first + step, ...
+  int peer;                            // chained stage 1 of a CTA pair: the peer's cluster rank, else -1
   int64_t myrow, n0;
   __device__ __forceinline__ void load8(int cl8, uint32_t (&v)[8]) const {
     if (has_acc) {
@@ -124,6 +146,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   const double* sB = sCol + bn;
   const double* sMean = sCol + 2 * bn;
   const double* sDen = sCol + 3 * bn;
+  const double* sInv = sCol + 6 * bn;       // RN(1 / denom): div_rn's correctly rounded division
   const double* sGam = sCol + 4 * bn;
   const double* sBeta = sCol + 5 * bn;
   const double k_acc = E.k_acc;
@@ -152,7 +175,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
       // ROW_ONLY (aggregation: exact 0/1 left operand, no bias): the reference adds
       // nothing else; otherwise the absent terms are +0.0
       if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), kconst), sB[cl]);
-      if (HAS_BN) x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, sMean[cl]), sDen[cl]), sGam[cl]), sBeta[cl]);
+      if (HAS_BN) x = __dadd_rn(__dmul_rn(div_rn(__dsub_rn(x, sMean[cl]), sDen[cl], sInv[cl]), sGam[cl]), sBeta[cl]);
       if (ACT == QG_ACT_RELU) {
         if (packed) {
           // sign mask: -0 also maps to +0, which requantizes to the same code
@@ -198,10 +221,13 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
     if (ST == 1) {
       // stage 2's LEFT operand in shared memory (UMMA K-major core matrices, one 16 KB
-      // slot per 128 K columns); rows past m hold zeros (their stage-2 rows are not stored)
-      uint8_t* slab = (cl8 >> 7) ? mid1 : mid0;
-      *reinterpret_cast<uint2*>(slab + (lrow >> 3) * 1024 + ((cl8 & 127) >> 4) * 128 + (lrow & 7) * 16 +
-                                (cl8 & 15)) = make_uint2(lo, hi);
+      // slot per 128 K columns); rows past m hold zeros (their stage-2 rows are not stored).
+      // A CTA pair writes its half of the columns into both CTAs' copies.
+      const int c = (int)L.n0 + cl8;
+      uint8_t* dst = ((c >> 7) ? mid1 : mid0) + (lrow >> 3) * 1024 + ((c & 127) >> 4) * 128 + (lrow & 7) * 16 +
+                     (c & 15);
+      *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
+      if (L.peer >= 0) st_peer_v2(peer_addr(smem_u32(dst), (uint32_t)L.peer), lo, hi);
       continue;
     }
     if (L.rvalid) {
@@ -326,7 +352,7 @@ template <int ST>
 __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tseg& G, TileRing& R, int64_t tile,
                                               int64_t rb, int64_t n0, int nk, uint32_t tmem, const double* sCol,
                                               bool fused, bool screen, uint8_t* mid0 = nullptr,
-                                              uint8_t* mid1 = nullptr) {
+                                              uint8_t* mid1 = nullptr, int peer = -1) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bn = ST == 2 ? P.bn2 : P.bn;
   const int64_t pn = ST == 2 ? P.n2 : P.n;
@@ -351,6 +377,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   L.rvalid = myrow < G.m;
   L.myrow = myrow;
   L.n0 = n0;
+  L.peer = peer;
   uint32_t rsum = 0;
   if (ST == 0 && !fused) {
     const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
@@ -395,8 +422,10 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
 #undef QG_EPI_CASE
     }
   }
+  // chained stage 2 accumulates into the second half of sRowSum (a CTA pair's peer may
+  // still read the first half, stage 1's partial sums)
   if (packed && (ST == 1 || G.q_row_sums) && rsum)
-    atomicAdd(&R.sRowSum[quad * 32 + lane], (unsigned long long)rsum);
+    atomicAdd(&R.sRowSum[(ST == 2 ? 128 : 0) + quad * 32 + lane], (unsigned long long)rsum);
 }
 
 // One work item: (segment, 128-row block, N tile) -> fused GEMM tile.  Ends with a
@@ -440,8 +469,12 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const bool screen = fused && !CHAIN && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
                       (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
   // chained stage 2: per-column constants after stage 1's (screen is off when chained)
-  double* sCol2 = sCol + (E.bn_mean ? 6 : 2) * bn;
+  double* sCol2 = sCol + (E.bn_mean ? 7 : 2) * bn;
+  // chain == 2: this CTA is rank nt of its row block's pair (n_tiles == 2, pairs aligned)
+  const bool cpair = CHAIN && P.chain == 2;
+  const int64_t n0_2 = cpair ? (int64_t)nt * P.bn2 : 0;
   if (tid < 128) R.sRowSum[tid] = 0ull;
+  if (CHAIN && tid < 128) R.sRowSum[128 + tid] = 0ull;
   if (tid == 0) tstamp(P, tile, 1);
 
   if (warp == 0 && lane == 0) {
@@ -508,7 +541,8 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         const int s = (int)(g % (uint32_t)S);
         if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
         mbar_expect_tx(&full[s], wb);
-        bulk_g2s(stage0 + (size_t)s * stage_bytes + a_bytes, P.w2 + (int64_t)j * (P.w2_npad << 7), wb, &full[s]);
+        bulk_g2s(stage0 + (size_t)s * stage_bytes + a_bytes,
+                 P.w2 + (int64_t)j * (P.w2_npad << 7) + (n0_2 >> 3) * 1024, wb, &full[s]);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -572,6 +606,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
           sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
           sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
           sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+          sCol[6 * bn + i] = ok ? E.bn_inv_denom[c] : 1.0;
         }
       }
     }
@@ -579,14 +614,16 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       const qg_epilogue& E2 = P.epi2;
       const int bn2 = P.bn2;
       for (int i = t; i < bn2; i += (int)blockDim.x - 64) {
-        const bool ok = i < P.n2;
-        sCol2[0 * bn2 + i] = (ok && E2.use_col) ? __dmul_rn(E2.k_col, (double)E2.col_sums[i]) : 0.0;
-        sCol2[1 * bn2 + i] = (ok && E2.bias) ? E2.bias[i] : 0.0;
+        const int64_t c = n0_2 + i;
+        const bool ok = c < P.n2;
+        sCol2[0 * bn2 + i] = (ok && E2.use_col) ? __dmul_rn(E2.k_col, (double)E2.col_sums[c]) : 0.0;
+        sCol2[1 * bn2 + i] = (ok && E2.bias) ? E2.bias[c] : 0.0;
         if (E2.bn_mean) {
-          sCol2[2 * bn2 + i] = ok ? E2.bn_mean[i] : 0.0;
-          sCol2[3 * bn2 + i] = ok ? E2.bn_denom[i] : 1.0;
-          sCol2[4 * bn2 + i] = ok ? E2.bn_gamma[i] : 0.0;
-          sCol2[5 * bn2 + i] = ok ? E2.bn_beta[i] : 0.0;
+          sCol2[2 * bn2 + i] = ok ? E2.bn_mean[c] : 0.0;
+          sCol2[3 * bn2 + i] = ok ? E2.bn_denom[c] : 1.0;
+          sCol2[4 * bn2 + i] = ok ? E2.bn_gamma[c] : 0.0;
+          sCol2[5 * bn2 + i] = ok ? E2.bn_beta[c] : 0.0;
+          sCol2[6 * bn2 + i] = ok ? E2.bn_inv_denom[c] : 1.0;
         }
       }
     }
@@ -635,18 +672,25 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     R.it0 += (uint32_t)P.k2;
     uint8_t* mid0 = stage0 + (size_t)(itc % (uint32_t)S) * stage_bytes;
     uint8_t* mid1 = stage0 + (size_t)((itc + 1) % (uint32_t)S) * stage_bytes;
-    tile_epilogue<1>(P, G, R, tile, rb, 0, nk, tmem, sCol, true, false, mid0, mid1);
+    // a pair writes into the peer's slots: both CTAs' stage-1 MMAs must have drained them
+    // (same row block => same K tiles => same ring positions and slot addresses)
+    if (cpair) cluster_barrier();
+    tile_epilogue<1>(P, G, R, tile, rb, n0, nk, tmem, sCol, true, false, mid0, mid1, cpair ? (nt ^ 1) : -1);
     // generic-proxy code stores -> visible to the tensor core; TMEM reads retired
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (cpair) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+    else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    if (cpair) cluster_barrier();
+    else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const qg_epilogue& E2 = P.epi2;
     if (tid < 128) {
       // stage 2's row terms: RN(k_row * code row sum), the sums of the codes just written
+      // (a pair adds the peer's partial sums over its half of the columns)
       const int64_t row = rb * 128 + tid;
-      R.sRowTerm[tid] = (E2.use_row && row < G.m) ? __dmul_rn(E2.k_row, (double)R.sRowSum[tid]) : 0.0;
-      R.sRowSum[tid] = 0ull;
+      unsigned long long rs = R.sRowSum[tid];
+      if (cpair) rs += ld_peer_u64(peer_addr(smem_u32(&R.sRowSum[tid]), (uint32_t)(nt ^ 1)));
+      R.sRowTerm[tid] = (E2.use_row && row < G.m) ? __dmul_rn(E2.k_row, (double)rs) : 0.0;
     }
     if (warp == 1 && lane == 0) {
       const uint32_t idesc2 = idesc_u8(P.bn2);
@@ -668,13 +712,15 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     asm volatile("tcgen05.fence::after_thread_sync;");
     __syncthreads();                                     // stage-2 row terms visible
     if (tid == 0) tstamp(P, tile, 7);
-    tile_epilogue<2>(P, G, R, tile, rb, 0, P.k2, tmem, sCol2, true, false);
+    tile_epilogue<2>(P, G, R, tile, rb, n0_2, P.k2, tmem, sCol2, true, false);
     if (tid == 0) tstamp(P, tile, 4);
     if (E2.out_kind == QG_OUT_PLANES && G.q_row_sums) {
       __syncthreads();
-      if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[tid])
-        atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
+      if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[128 + tid])
+        atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[128 + tid]);
     }
+    // the peer reads this CTA's shared memory (codes, row sums) until its own barrier
+    if (cpair) cluster_barrier();
   } else {
     tile_epilogue<0>(P, G, R, tile, rb, n0, nk, tmem, sCol, fused, screen);
     if (tid == 0) tstamp(P, tile, 4);
@@ -726,7 +772,7 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
   __shared__ uint32_t tmem_base_s;
-  __shared__ unsigned long long sRowSum[128];
+  __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];   // chained: [stage 1 | stage 2]
   __shared__ double sRowTerm[128];
   TileRing R;
   // schedule arrays and the segment table are static for the lifetime of a launch
@@ -969,6 +1015,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
           sCol[3 * bn + i] = ok ? E.bn_denom[cc] : 1.0;
           sCol[4 * bn + i] = ok ? E.bn_gamma[cc] : 0.0;
           sCol[5 * bn + i] = ok ? E.bn_beta[cc] : 0.0;
+          sCol[6 * bn + i] = ok ? E.bn_inv_denom[cc] : 1.0;
         }
       }
     }
@@ -1276,11 +1323,23 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (CHAIN && P.chain == 2) {
+    // chained CTA pairs: the two N halves of a row block share stage-1 codes through DSMEM
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB, NT, CHAIN>, P);
 }
 
@@ -1292,6 +1351,9 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   if (a->bn < 32 || a->bn > 256 || (a->bn & (a->bn - 1))) { rc = QG_ERR_ARG; return 0; }
   if (a->mode != QG_GEMM_I32 && a->mode != QG_GEMM_EPILOGUE) { rc = QG_ERR_ARG; return 0; }
   if (a->mode == QG_GEMM_EPILOGUE && !a->epi) { rc = QG_ERR_ARG; return 0; }
+  // batch norm needs all five vectors (bn_inv_denom = RN(1 / bn_denom) drives the division)
+  if (a->epi && a->epi->bn_mean && !(a->epi->bn_denom && a->epi->bn_gamma && a->epi->bn_beta && a->epi->bn_inv_denom))
+    { rc = QG_ERR_ARG; return 0; }
   if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) { rc = QG_ERR_SHAPE; return 0; }
   P = TiledParams{};
   P.segs = a->segs; P.nsegs = a->nsegs; P.a_blocks = a->a_blocks; P.b_npad = a->b_npad; P.n = a->n;
@@ -1306,19 +1368,25 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.slot_bn = P.bn;
   const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
                       (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
-  size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 6 : 2)) * (size_t)P.bn * 8;
+  size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 7 : 2)) * (size_t)P.bn * 8;
   if (a->chain) {
     const qg_chain* c = a->chain;
     // stage 1: one N tile covering all its columns, packed codes, no screen, byte blocks
-    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != 1 || a->n > a->bn || a->pair || P.a_bits || screen ||
+    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != (c->split ? 2 : 1) || a->n > (int64_t)a->n_tiles * a->bn ||
+        a->pair || P.a_bits || screen ||
         a->epi->out_kind != QG_OUT_PLANES)
       { rc = QG_ERR_UNSUPPORTED; return 0; }
     if (!c->w || !c->epi || c->w_npad < 32 || c->w_npad > 256 || (c->w_npad & (c->w_npad - 1)) || c->n < 1 ||
         c->n > c->w_npad || (c->out_layout != 0 && c->out_layout != 2) ||
-        (c->out_layout == 0) != (c->epi->out_kind == QG_OUT_REAL))
+        (c->out_layout == 0) != (c->epi->out_kind == QG_OUT_REAL) ||
+        (c->epi->bn_mean && !(c->epi->bn_denom && c->epi->bn_gamma && c->epi->bn_beta && c->epi->bn_inv_denom)))
       { rc = QG_ERR_ARG; return 0; }
-    P.chain = 1;
-    P.bn2 = (int32_t)c->w_npad;
+    if (c->split) {
+      // CTA pairs: n_tiles == 2 stage-1 halves, stage-2 halves of w_npad / 2 >= 16 columns
+      if (a->n_tiles != 2 || (a->total_ctas & 1) || c->w_npad < 32) { rc = QG_ERR_UNSUPPORTED; return 0; }
+    }
+    P.chain = c->split ? 2 : 1;
+    P.bn2 = (int32_t)(c->split ? c->w_npad / 2 : c->w_npad);
     P.k2 = (int32_t)((a->n + 127) / 128);
     P.n2 = c->n;
     P.out_layout2 = c->out_layout;
@@ -1327,7 +1395,7 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
     P.w2_npad = c->w_npad;
     P.epi2 = *c->epi;
     P.slot_bn = std::max(P.bn, P.bn2);
-    cols += (c->epi->bn_mean ? 6 : 2) * (size_t)P.bn2 * 8;
+    cols += (c->epi->bn_mean ? 7 : 2) * (size_t)P.bn2 * 8;
   }
   return cols;
 }

@@ -69,7 +69,7 @@ class Chain(ctypes.Structure):
     """Mirror of ``qg_chain``: a dense stage-2 GEMM fused behind a tiled stage."""
 
     _fields_ = [("w", ctypes.c_void_p), ("w_npad", ctypes.c_int64), ("n", ctypes.c_int64),
-                ("out_layout", ctypes.c_int32), ("pad_", ctypes.c_int32), ("out_npad", ctypes.c_int64),
+                ("out_layout", ctypes.c_int32), ("split", ctypes.c_int32), ("out_npad", ctypes.c_int64),
                 ("epi", ctypes.POINTER(N.Epilogue))]
 
 
@@ -364,9 +364,10 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     rbs = [-(-s.m // TILE) for s in segs]
     pair = chain is None and use_pair(b_npad, sum(rbs), sizes, mode) and not a_bits
     if chain is not None:
-        if b_npad > 256 or a_bits or EPOCH is not None:
-            raise ValueError("chained stage needs one N tile <= 256, byte blocks, per-stage launches")
-        bn = b_npad
+        if b_npad > 256 or a_bits or EPOCH is not None or (chain.split and b_npad < 64):
+            raise ValueError("chained stage needs one N tile <= 256 (two >= 32 when split), byte blocks, "
+                             "per-stage launches")
+        bn = b_npad // 2 if chain.split else b_npad
     elif pair:
         bn = max(64, min(256, b_npad))
     else:

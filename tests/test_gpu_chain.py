@@ -13,15 +13,15 @@ from paper_2111_09547_b200.synth import GraphConfig
 pytestmark = pytest.mark.gpu
 
 
-def _forward(batches, model, chain):
-    saved = engine.CHAIN
-    engine.CHAIN = chain
+def _forward(batches, model, chain, split=True):
+    saved = engine.CHAIN, engine.CHAIN_SPLIT
+    engine.CHAIN, engine.CHAIN_SPLIT = chain, split
     hook = []
     bitgemm.PROFILE_HOOK = hook
     try:
         outs = engine.model_forward_group(batches, model)
     finally:
-        engine.CHAIN = saved
+        engine.CHAIN, engine.CHAIN_SPLIT = saved
         bitgemm.PROFILE_HOOK = None
     return [o.cpu().numpy() for o in outs], len(hook)
 
@@ -40,14 +40,17 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("split", [True, False], ids=["pairs", "single"])
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-{c[2]}-{c[3]}x{c[4]}-b{c[5]}" for c in CASES])
-def test_chained_forward_equals_two_launch_forward(case):
+def test_chained_forward_equals_two_launch_forward(case, split):
+    """split: stages whose two-launch N tile is half the width chain as 2-CTA clusters
+    (codes exchanged through distributed shared memory); otherwise one CTA per row block."""
     kind, in_dim, hidden, classes, layers, bits, wbits = case
     # 3 batches of 2 parts; 1237 nodes -> part sizes not multiples of 128 (ragged row blocks)
     cfg = GraphConfig("chain-test", kind, 1237, 9000, 6, 2, in_dim, hidden, classes, layers, bits, wbits)
     batches, feats, _ = synth.planted_batches(cfg, seed=3)
     model = synth.calibrated_model(cfg, batches[0], feats[0], seed=3)
-    got, n_chained = _forward(batches, model, True)
+    got, n_chained = _forward(batches, model, True, split)
     want, n_plain = _forward(batches, model, False)
     assert len(got) == len(want)
     for g, w in zip(got, want):
@@ -57,13 +60,14 @@ def test_chained_forward_equals_two_launch_forward(case):
     assert n_plain - n_chained == saved
 
 
-def test_chained_forward_matches_oracle_small():
+@pytest.mark.parametrize("split", [True, False], ids=["pairs", "single"])
+def test_chained_forward_matches_oracle_small(split):
     """Direct oracle check of one chained GIN forward (small, CPU oracle in seconds)."""
     from oracle import qgtc_oracle as O
-    cfg = GraphConfig("chain-oracle", "gin", 300, 1500, 2, 2, 48, 32, 6, 3, 3, 3)
+    cfg = GraphConfig("chain-oracle", "gin", 300, 1500, 2, 2, 48, 64, 6, 3, 3, 3)
     batches, feats, xp = synth.planted_batches(cfg, seed=5)
     model = synth.calibrated_model(cfg, batches[0], feats[0], seed=5)
-    got, _ = _forward(batches, model, True)
+    got, _ = _forward(batches, model, True, split)
     for b, f, g in zip(batches, feats, got):
         codes = O.quantize_codes(f, xp.alpha_min, xp.alpha_max, xp.bits)
         want = O.model_forward(b.adjacency.words, b.adjacency.dims(), codes, xp, model.layers)
