@@ -455,9 +455,10 @@ def ours(args, world, rank):
                      "frac": round(achieved / peak, 5), "traffic": traffic, "peak_source": peak_src,
                      "work": "2 x 1024 x N_padded int8-MACs per non-zero 8x128 left tile (one u8 MAC "
                              "retires all bit-plane pairs)",
-                     "durations": "per-launch span (first CTA entry -> last CTA exit, %globaltimer) inside "
-                                  "an identical stamped epoch graph replayed after an L2 flush; CUDA events "
-                                  "around each replay give stamped_step_ms",
+                     "durations": "per launch, %globaltimer from the later of its first CTA entry and the "
+                                  "previous GEMM launch's last CTA exit (PDL lets CTAs enter early and wait) "
+                                  "to its last CTA exit, inside an identical stamped epoch graph replayed "
+                                  "after an L2 flush; CUDA events around each replay give stamped_step_ms",
                      "launches_per_epoch": gemm_launches, "kernel_ms_per_epoch": round(gemm_ms, 5),
                      "stamped_step_ms": round(stamped_step_ms, 5),
                      "kernel_share_of_step": round(gemm_ms / stamped_step_ms, 3)},

@@ -112,14 +112,24 @@ class EpochRunner:
         return self.logits
 
     def kernel_spans(self):
-        """[(span_ms, algorithmic_ops)] of the tiled GEMM launches of the LAST replay
-        (capture(stamps=True)): first CTA entry -> last CTA exit on %globaltimer."""
+        """[(duration_ms, algorithmic_ops)] of the tiled GEMM launches of the LAST replay
+        (capture(stamps=True)), on %globaltimer: from the later of the launch's first CTA
+        entry and the previous GEMM launch's last CTA exit, to this launch's last CTA exit.
+        With programmatic dependent launch a grid's CTAs enter while its predecessor is
+        still running and wait in griddepcontrol.wait; counting from the predecessor's end
+        keeps overlapped spans from being counted twice (the durations sum to the GEMM
+        window of the epoch)."""
         out = []
+        prev_end = None
         for st, work in self.stamps:
             s = st.cpu().numpy()
             s = s[s[:, 0] > 0]
             if len(s):
-                out.append(((s[:, 5].max() - s[:, 0].min()) / 1e6, work))
+                begin, end = s[:, 0].min(), s[:, 5].max()
+                if prev_end is not None:
+                    begin = max(begin, prev_end)
+                out.append(((end - begin) / 1e6, work))
+                prev_end = end
         return out
 
     def kernel_launches_per_epoch(self) -> int:
