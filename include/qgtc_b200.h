@@ -277,7 +277,7 @@ typedef struct {
   int64_t total_ctas;
   int64_t b_npad;              /* right operand padded N (multiple of bn)            */
   int64_t n;                   /* logical output columns                             */
-  int32_t bn, n_tiles;         /* N tile (power of two 32..256) and tiles per row block */
+  int32_t bn, n_tiles;         /* N tile (power of two 16..256) and tiles per row block */
   int32_t mode;                /* QG_GEMM_I32 or QG_GEMM_EPILOGUE                    */
   int32_t out_layout;          /* 0 row-major fp64/int32, 1 left-tiled codes, 2 right-tiled codes */
   int64_t out_npad;            /* right-tiled output: padded N                       */

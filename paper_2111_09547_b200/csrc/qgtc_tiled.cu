@@ -1348,7 +1348,7 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
 static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   rc = QG_OK;
   if (!a || !a->segs || a->nsegs < 1 || a->total_ctas < 1) { rc = QG_ERR_ARG; return 0; }
-  if (a->bn < 32 || a->bn > 256 || (a->bn & (a->bn - 1))) { rc = QG_ERR_ARG; return 0; }
+  if (a->bn < 16 || a->bn > 256 || (a->bn & (a->bn - 1))) { rc = QG_ERR_ARG; return 0; }
   if (a->mode != QG_GEMM_I32 && a->mode != QG_GEMM_EPILOGUE) { rc = QG_ERR_ARG; return 0; }
   if (a->mode == QG_GEMM_EPILOGUE && !a->epi) { rc = QG_ERR_ARG; return 0; }
   // batch norm needs all five vectors (bn_inv_denom = RN(1 / bn_denom) drives the division)
@@ -1501,7 +1501,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   }
   static const bool env_budget = getenv("QG_TILED_SMEM_KB") != nullptr;
   // TMEM columns: the widest accumulator (stage 1 or the chained stage 2)
-  const int tcols = P.slot_bn;
+  const int tcols = std::max(32, (int)P.slot_bn);     // TMEM allocations are >= 32 columns
   const bool three = !env_budget && !P.chain && tcols <= 128 && a->total_ctas >= 3 * (int64_t)sms;
   static const bool wide = getenv("QG_WIDE") == nullptr || atoi(getenv("QG_WIDE")) != 0;
   const size_t budget = three ? 72 * 1024 : smem_budget();
@@ -1514,6 +1514,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     // the split-N stages it replaces and two epilogues per tile: with fewer tiles than
     // SMs, 16 warps (1 CTA/SM) split the epilogue slices 4 ways
     static const int chain_nt = getenv("QG_CHAIN_NT") ? atoi(getenv("QG_CHAIN_NT")) : 0;
+    static const bool wide_chain = getenv("QG_CHAIN_WIDE") != nullptr && atoi(getenv("QG_CHAIN_WIDE")) != 0;
     const bool wide16 = chain_nt == 512 || (chain_nt == 0 && a->total_ctas <= (int64_t)sms);
     if (wide16) {
       switch (tcols) {
@@ -1527,7 +1528,12 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
         case 32: launch_tiled<32, 2, kTThreads, true>(P, grid, smem, st); break;
         case 64: launch_tiled<64, 2, kTThreads, true>(P, grid, smem, st); break;
         case 128: launch_tiled<128, 2, kTThreads, true>(P, grid, smem, st); break;
-        default: launch_tiled<256, 2, kTThreads, true>(P, grid, smem, st); break;
+        default:
+          // 128x256 tiles in both stages (C4): 3 warp groups split the two epilogues.
+          // Opt-in (QG_CHAIN_WIDE=1): the 80-register bound spills, C4 7.01 vs 6.86 ms
+          if (wide_chain) launch_tiled<256, 2, 384, true>(P, grid, smem, st);
+          else launch_tiled<256, 2, kTThreads, true>(P, grid, smem, st);
+          break;
       }
     }
   } else if (three) {

@@ -341,7 +341,7 @@ BN_MIN = int(os.environ.get("QG_BN_MIN", "32"))       # tuning experiments
 
 def choose_bn(npad: int, row_blocks_total: int) -> int:
     bn = min(BN_MAX, npad)
-    while bn > max(32, BN_MIN) and row_blocks_total * (npad // bn) < 148:
+    while bn > max(16, BN_MIN) and row_blocks_total * (npad // bn) < 148:
         bn //= 2
     return bn
 

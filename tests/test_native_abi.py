@@ -150,3 +150,44 @@ def test_ctypes_struct_layouts_match_the_header(tmp_path):
 def ctypes_sizeof(cls):
     import ctypes
     return ctypes.sizeof(cls)
+
+
+def test_tiled_chain_argument_validation_needs_no_gpu():
+    """qg_tiled_gemm rejects malformed qg_chain requests before any CUDA call."""
+    import ctypes
+
+    from paper_2111_09547_b200 import tiled
+    lib = N.lib()
+    lib.qg_tiled_gemm.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.qg_tiled_gemm.restype = ctypes.c_int
+    epi, epi2 = N.Epilogue(), N.Epilogue()
+    epi.out_kind, epi2.out_kind = N.OUT_PLANES, N.OUT_PLANES
+    fake = ctypes.c_uint64(0)                  # never dereferenced by the validation
+
+    def call(**kw):
+        a = tiled.TiledArgs()
+        a.segs, a.nsegs, a.total_ctas = ctypes.addressof(fake), 1, 2
+        a.b_npad, a.n, a.bn, a.n_tiles = 64, 64, 64, 1
+        a.mode, a.out_layout = N.GEMM_EPILOGUE, 1
+        a.epi = ctypes.pointer(epi)
+        c = tiled.Chain()
+        c.w, c.w_npad, c.n, c.out_layout, c.out_npad = ctypes.addressof(fake), 64, 40, 2, 64
+        c.epi = ctypes.pointer(epi2)
+        for k, v in kw.items():                  # c_<field>: the chain, else the launch args
+            if k.startswith("c_"):
+                setattr(c, k[2:], v)
+            else:
+                setattr(a, k, v)
+        a.chain = ctypes.addressof(c)
+        return lib.qg_tiled_gemm(ctypes.byref(a), None)
+
+    assert call(c_w_npad=48) == N.QG_ERR_ARG                  # not a power of two
+    assert call(c_n=65) == N.QG_ERR_ARG                       # more columns than w_npad
+    assert call(c_out_layout=1) == N.QG_ERR_ARG               # stage 2 writes right tiles or fp64
+    assert call(c_out_layout=0) == N.QG_ERR_ARG               # fp64 output needs an OUT_REAL epilogue
+    assert call(n_tiles=2, b_npad=128) == N.QG_ERR_UNSUPPORTED  # one N tile unless split
+    assert call(c_split=1) == N.QG_ERR_UNSUPPORTED            # split needs n_tiles == 2
+    assert call(mode=N.GEMM_I32) == N.QG_ERR_UNSUPPORTED      # stage 1 must requantize
+    mean = (ctypes.c_double * 1)(0.0)
+    epi2.bn_mean = ctypes.cast(mean, ctypes.c_void_p)         # BN without its other vectors
+    assert call() == N.QG_ERR_ARG
