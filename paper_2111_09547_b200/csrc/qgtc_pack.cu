@@ -363,6 +363,9 @@ static inline int64_t pad_up(int64_t n, int64_t m) { return (n + m - 1) / m * m;
 
 // Per-epoch slab reset in ONE kernel: zero the accumulator slab, clear the status slab.
 __global__ void slab_reset_kernel(int64_t* zero, int64_t nz, int64_t* status, int64_t ns) {
+  // a PDL-launched successor (the epoch's entry conversion) may start launching now; it
+  // waits for this grid's completion before touching any memory
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz + ns; i += stride) {
     if (i < nz) zero[i] = 0;

@@ -1238,6 +1238,9 @@ __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __
     if (segs[mid].unit_begin <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
   }
   const qg_entry_seg& G = segs[lo];
+  // PDL-launched: everything above read only the (static) segment table; the planes and
+  // the zeroed row sums come from the stream predecessor
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t u = (int64_t)blockIdx.x - G.unit_begin;
   const int64_t wpl = G.pr >> 5;                          // words per column of one plane
   const int64_t ncg = right ? (G.pitch + 127) >> 7 : (G.pc + 127) >> 7;
@@ -1293,7 +1296,19 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
                               int64_t total_units, void* stream) {
   if (!segs || nsegs < 1 || nplanes < 1 || nplanes > 8 || total_units < 0) return QG_ERR_ARG;
   if (total_units == 0) return QG_OK;
-  entry_tiles_kernel<<<(unsigned)total_units, 256, 0, (cudaStream_t)stream>>>(segs, nsegs, nplanes, right);
+  // programmatic dependent launch: the launch overlaps the predecessor's tail (the slab
+  // reset of a captured epoch); the kernel waits before reading any predecessor output
+  static const bool pdl = getenv("QG_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)total_units);
+  cfg.blockDim = dim3(256);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, entry_tiles_kernel, segs, (int)nsegs, (int)nplanes, (int)right);
   return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA;
 }
 
