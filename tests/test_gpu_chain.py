@@ -96,3 +96,15 @@ def test_chained_e2e_runner_equals_unchained_device_epoch():
             assert torch.equal(out, want)
     finally:
         engine.CHAIN = saved
+
+
+def test_op_counters_after_a_chained_forward():
+    """op_counters() after a forward whose last op is a chained update (GCN) resolves to the
+    same counters as after the two-launch forward (bitgemm.py:95-100 semantics)."""
+    cfg = GraphConfig("chain-counters", "gcn", 700, 4000, 4, 2, 64, 32, 5, 2, 3, 3)
+    batches, feats, _ = synth.planted_batches(cfg, seed=6)
+    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=6)
+    _forward(batches, model, False)
+    want = bitgemm.op_counters()
+    _forward(batches, model, True)
+    assert bitgemm.op_counters() == want
