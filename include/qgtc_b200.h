@@ -257,7 +257,8 @@ typedef struct {
   int64_t cta_begin;           /* first CTA of this segment                          */
   int32_t k_tiles;             /* dense left: K tiles                                */
   int32_t pad_;
-  int64_t pad2_;
+  int64_t rb_base;             /* dataflow epoch: global index of this segment's first
+                                  128-row block (the same in every stage)              */
   /* pair mode (qg_tiled_args.pair): 2-D TMA descriptors (CUtensorMap, 128 B, 64-B
    * aligned; qg_encode_linear_map) of the A source and the B source viewed as rows of
    * 128 bytes -- the pair's copies signal the leader CTA's mbarrier (cta_group::2) */
@@ -291,6 +292,14 @@ typedef struct {
                                   segs[].cta_begin then counts PAIRS, total_ctas = 2 x pairs,
                                   bn >= 64 (each CTA stages bn/2 columns of B)             */
   const struct qg_chain* chain; /* optional: fuse a dense stage-2 GEMM behind this stage   */
+  /* dataflow epoch (qg_tiled_epoch): per-128-row-block completion counters, indexed by
+   * segs[].rb_base + row block, zeroed before the epoch.  A tile of this stage waits
+   * until the previous stage's counters of the row blocks it reads reach expect_prev
+   * (that stage's n_tiles), and adds 1 to its own row block's counter when done. */
+  int32_t* ready_prev;         /* NULL for the first stage of a launch                   */
+  int32_t* ready_cur;
+  int32_t expect_prev;
+  int32_t pad3_;
 } qg_tiled_args;
 
 /* Chained stage 2 of a tiled GEMM (qg_tiled_args.chain): an aggregation and the update
@@ -325,6 +334,10 @@ int qg_tiled_gemm(const qg_tiled_args* args, void* stream);
  * order; grid_bar is 9 caller-owned device words (barrier + per-stage tile counters,
  * zeroed by the call, stream-ordered). */
 int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint32_t* grid_bar, void* stream);
+/* With stages[].ready_cur set, the epoch runs as a DATAFLOW kernel instead: no grid
+ * barriers and no cooperative launch; CTAs claim tiles of all stages from one queue
+ * (stage-major) and each tile waits only for the row blocks it reads.  Subgraph
+ * batches are block-diagonal, so the stages of different parts overlap. */
 
 /* Gather the non-zero 128x128 blocks (blk_rb/blk_kt) of a column-wise 1-bit matrix
  * into `packed` (2 KB each; skipped when a_words == NULL and `packed` is already

@@ -48,6 +48,10 @@ struct TiledParams {
   int64_t n2, out_npad2, w2_npad;
   const uint8_t* w2;
   qg_epilogue epi2;
+  // dataflow epoch (qg_tiled_args.ready_*): per-row-block completion counters
+  int32_t* ready_prev;
+  int32_t* ready_cur;
+  int32_t expect_prev;
 };
 
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
@@ -79,6 +83,18 @@ __device__ __forceinline__ unsigned long long ld_peer_u64(uint32_t cluster_addr)
   unsigned long long v;
   asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(cluster_addr) : "memory");
   return v;
+}
+// dataflow epoch: spin until a row block's completion counter reaches `expect`
+// (acquire), then make the other CTAs' generic-proxy stores visible to this thread's
+// bulk copies (async proxy)
+__device__ __forceinline__ void wait_ready(const int32_t* ctr, int32_t expect) {
+  int32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= expect) break;
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -512,6 +528,24 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       }
       it_begin = pre;
     }
+    // dataflow epoch: a dense left operand is the previous stage's output rows of this
+    // row block; an adjacency stage's K tile kt reads the previous stage's row block kt
+    const bool df_wait = P.ready_prev != nullptr;
+    if (df_wait && !P.a_blocks) wait_ready(P.ready_prev + G.rb_base + rb, P.expect_prev);
+    if (df_wait && P.a_blocks && nk > 0) {
+      // every row block this tile reads (block-diagonal parts: a few neighbours), then ONE
+      // proxy fence ahead of all the bulk copies
+      for (int it = 0; it < nk; ++it) {
+        const int32_t* ctr = P.ready_prev + G.rb_base + G.blk_kt[kbase + it];
+        int32_t v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+          if (v >= P.expect_prev) break;
+          __nanosleep(64);
+        }
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     for (int it = it_begin; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
@@ -566,6 +600,13 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     // RN(k_row * row_sum) (predecessor outputs) and the per-column constants
     const int t = tid - 64;
     if (R.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // dataflow epoch: a dense-left stage's row sums are the previous stage's outputs
+    if (P.ready_prev && !P.a_blocks && E.use_row && t < 128) {
+      int32_t v;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.ready_prev + G.rb_base + rb) : "memory");
+      } while (v < P.expect_prev);
+    }
     if (t < 128) {
       const int64_t row = rb * 128 + t;
       R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
@@ -734,6 +775,12 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (tid == 0) tstamp(P, tile, 5);
+  if (P.ready_cur && tid == 0) {
+    // dataflow epoch: every thread's epilogue stores precede the CTA barrier above; the
+    // gpu-scope fence makes them visible before the counter's release increment
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.ready_cur + G.rb_base + rb) : "memory");
+  }
 }
 
 // CTA setup shared by both kernels: TMEM allocation, ring barriers.
@@ -1056,6 +1103,8 @@ struct EpochParams {
   int32_t ring_stages;
   uint32_t stage_bytes_max;
   unsigned int* grid_bar;   // zeroed before the launch
+  int32_t dataflow;         // 1: one tile queue over all stages, per-row-block waits
+  int64_t total_all;        // dataflow: tiles of all stages
 };
 
 static __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
@@ -1101,6 +1150,21 @@ __global__ void __maxnreg__(112) tc_tiled_epoch_kernel(const __grid_constant__ E
   asm volatile("tcgen05.fence::after_thread_sync;");
   R.tmem = tmem_base_s;
   __shared__ int64_t s_tile;
+  if (EP.dataflow) {
+    // every tile is claimed from one stage-major queue: a tile only waits for tiles of
+    // earlier stages, which were claimed earlier by running CTAs, so the grid needs no
+    // co-residency (no static first tile: a CTA that is not yet resident owns nothing)
+    for (;;) {
+      int64_t t = next_tile(EP.grid_bar, &s_tile);
+      if (t >= EP.total_all) break;
+      int st = 0;
+      while (t >= EP.st[st].total_ctas) { t -= EP.st[st].total_ctas; ++st; }
+      tiled_tile<TMEM_COLS, false>(EP.st[st], t, R);
+    }
+    if ((threadIdx.x >> 5) == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
+    return;
+  }
   unsigned int gen = 0;
   for (int st = 0; st < EP.nstages; ++st) {
     const TiledParams& P = EP.st[st];
@@ -1381,6 +1445,9 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.a_bits = a->a_blocks ? a->a_bits : 0;
   P.pair = a->pair;
   P.slot_bn = P.bn;
+  P.ready_prev = a->ready_prev;
+  P.ready_cur = a->ready_cur;
+  P.expect_prev = a->expect_prev;
   const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
                       (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
   size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 7 : 2)) * (size_t)P.bn * 8;
@@ -1590,8 +1657,11 @@ static int launch_epoch(EpochParams& EP, size_t smem, int64_t max_tiles, cudaStr
   if (env_per_sm) per_sm = atoi(env_per_sm);
   // TMEM: COLS <= 256 columns per CTA, so every co-resident CTA can allocate (512 per SM)
   per_sm = std::min(per_sm, 512 / COLS);
+  // dataflow: no co-residency needed (see tc_tiled_epoch_kernel); 2 CTAs/SM fit in
+  // shared memory and TMEM although the occupancy API reports 1 for tcgen05.alloc kernels
+  if (EP.dataflow) per_sm = std::min(2, 512 / COLS);
   if (per_sm < 1) return QG_ERR_UNSUPPORTED;
-  const int64_t grid = std::min<int64_t>(max_tiles, (int64_t)sms * per_sm);
+  const int64_t grid = std::min<int64_t>(EP.dataflow ? EP.total_all : max_tiles, (int64_t)sms * per_sm);
   static const bool dbg = getenv("QG_DEBUG_EPOCH") != nullptr;
   if (dbg) {
     cudaFuncAttributes fa{};
@@ -1624,7 +1694,7 @@ static int launch_epoch(EpochParams& EP, size_t smem, int64_t max_tiles, cudaStr
   attr[0].id = cudaLaunchAttributeCooperative;          // grid barrier: all CTAs co-resident
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = EP.dataflow ? 0 : 1;
   const cudaError_t err = cudaLaunchKernelEx(&cfg, tc_tiled_epoch_kernel<COLS>, EP);
   if (dbg && err != cudaSuccess) fprintf(stderr, "qg_tiled_epoch launch: %s\n", cudaGetErrorString(err));
   return tstatus();
@@ -1652,6 +1722,12 @@ extern "C" int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint
   EP.ring_stages = ring;
   EP.stage_bytes_max = (uint32_t)stage;
   EP.grid_bar = grid_bar;
+  EP.dataflow = stages[0].ready_cur != nullptr;
+  for (int i = 0; i < nstages; ++i) {
+    if ((stages[i].ready_cur != nullptr) != (EP.dataflow != 0)) return QG_ERR_ARG;
+    if (EP.dataflow && i > 0 && stages[i].ready_prev && stages[i].expect_prev < 1) return QG_ERR_ARG;
+    EP.total_all += EP.st[i].total_ctas;
+  }
   const size_t smem = (size_t)ring * stage + cols_max;
   if (getenv("QG_DEBUG_EPOCH"))
     for (int i = 0; i < nstages; ++i)

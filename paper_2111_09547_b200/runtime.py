@@ -142,10 +142,8 @@ class EpochRunner:
         from .tiled import MAX_EPOCH_STAGES, blocked
         stages = 2 * len(self.model.layers)
         gemms = getattr(self, "gemm_launches", None)
-        if engine.FUSED_EPOCH:
-            gemms = -(-stages // MAX_EPOCH_STAGES)
-        elif gemms is None:
-            gemms = stages
+        if gemms is None:
+            gemms = -(-stages // MAX_EPOCH_STAGES) if engine.FUSED_EPOCH else stages
         per_epoch = 2 + gemms
         if self.rescan:
             blks = [blocked(b.adjacency) for b in self.batches]

@@ -50,7 +50,7 @@ class TSeg(ctypes.Structure):
                 ("q_codes", ctypes.c_void_p), ("q_row_sums", ctypes.c_void_p), ("out_real", ctypes.c_void_p),
                 ("out_i32", ctypes.c_void_p), ("status", ctypes.c_void_p), ("m", ctypes.c_int64),
                 ("r128", ctypes.c_int64), ("cta_begin", ctypes.c_int64), ("k_tiles", ctypes.c_int32),
-                ("pad_", ctypes.c_int32), ("pad2_", ctypes.c_int64), ("tmap_a", ctypes.c_uint8 * 128),
+                ("pad_", ctypes.c_int32), ("rb_base", ctypes.c_int64), ("tmap_a", ctypes.c_uint8 * 128),
                 ("tmap_b", ctypes.c_uint8 * 128)]
 
 
@@ -62,7 +62,8 @@ class TiledArgs(ctypes.Structure):
                 ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
                 ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p), ("a_bits", ctypes.c_int32),
-                ("pair", ctypes.c_int32), ("chain", ctypes.c_void_p)]
+                ("pair", ctypes.c_int32), ("chain", ctypes.c_void_p), ("ready_prev", ctypes.c_void_p),
+                ("ready_cur", ctypes.c_void_p), ("expect_prev", ctypes.c_int32), ("pad3_", ctypes.c_int32)]
 
 
 class Chain(ctypes.Structure):
@@ -81,6 +82,13 @@ EPOCH = None
 
 # qg_tiled_gemm launches issued so far (runtime.EpochRunner counts those of its graph)
 LAUNCHES = 0
+
+# The fused epoch as a DATAFLOW kernel (qg_tiled_args.ready_*): one tile queue over all
+# stages, each tile waiting only for the row blocks it reads.  Opt-in (QG_DATAFLOW=1):
+# bit-exact, but measured slower (C2 0.088 vs 0.055 ms/epoch, C3 0.33 vs 0.23): each
+# persistent CTA runs its ~3 tiles back to back (no PDL prefetch, no overlap of one tile's
+# epilogue with the next tile's loads), which costs more than the stage overlap gains.
+DATAFLOW = os.environ.get("QG_DATAFLOW", "0") == "1"
 
 # An event the first adjacency-block launch must wait on (the e2e runner's side-stream
 # H2D of the schedule + blocks and their expansion); cleared once joined.
@@ -309,6 +317,7 @@ class SegTable:
         arr = (kind * n).from_address(self.host.data_ptr())
         for i, s in enumerate(segs):
             arr[i] = s
+        self.segs = list(segs)
         self.dev = N.alloc(self.host.numel(), torch.uint8, "empty")
         if torch.cuda.is_current_stream_capturing():
             # a captured epoch reuses the same slab addresses every replay, so the table
@@ -371,10 +380,14 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     elif pair:
         bn = max(64, min(256, b_npad))
     else:
-        bn = choose_bn(b_npad, sum(rbs)) if EPOCH is None else choose_bn_fused(b_npad, sum(rbs), sm_count())
+        bn = (choose_bn(b_npad, sum(rbs)) if EPOCH is None or DATAFLOW
+              else choose_bn_fused(b_npad, sum(rbs), sm_count()))
     n_tiles = b_npad // bn
     begin = 0
+    rb_base = 0
     for s, r in zip(segs, rbs):
+        s.rb_base = rb_base                          # dataflow epoch counters (same in every stage)
+        rb_base += r
         s.cta_begin = begin
         begin += (-(-r // 2) if pair else r) * n_tiles
     if pair:
@@ -517,6 +530,11 @@ def entry_tiles(stacks, side: str, want_row_sums: bool, keep: list):
     return outs
 
 
+def _segs_of(table):
+    """Host copies of a SegTable's segments."""
+    return table.segs
+
+
 def flush_epoch(stages: list, keep: list) -> None:
     """Launch recorded stages as persistent epoch kernels (<= MAX_EPOCH_STAGES per launch):
     one cooperative grid, a grid barrier between stages (include/qgtc_b200.h qg_tiled_epoch)."""
@@ -524,6 +542,15 @@ def flush_epoch(stages: list, keep: list) -> None:
     for i in range(0, len(stages), MAX_EPOCH_STAGES):
         chunk = stages[i:i + MAX_EPOCH_STAGES]
         arr = (TiledArgs * len(chunk))(*[c[0] for c in chunk])
+        if DATAFLOW:
+            # per stage, one completion counter per 128-row block (zeroed per epoch)
+            nrb = max(1, max(sum(-(-sg.m // TILE) for sg in _segs_of(c[2])) for c in chunk))
+            ready = N.alloc((len(chunk), nrb), torch.int32, "volatile")
+            keep.append(ready)
+            for j, a in enumerate(arr):
+                a.ready_cur = ready[j].data_ptr()
+                if j > 0:
+                    a.ready_prev, a.expect_prev = ready[j - 1].data_ptr(), arr[j - 1].n_tiles
         bar = N.alloc(1 + MAX_EPOCH_STAGES, torch.int32, "empty")   # zeroed by the call (memset node)
         keep.extend([arr, bar])
         if bitgemm.PHASE_HOOK is not None:
@@ -538,6 +565,8 @@ def flush_epoch(stages: list, keep: list) -> None:
                 print("  py stage segs=%x nsegs=%d total=%d bn=%d | seg0 a=%x b=%x m=%d r128=%d cta_begin=%d k=%d"
                       % (a.segs, a.nsegs, a.total_ctas, a.bn, segs[0].a or 0, segs[0].b or 0, segs[0].m, segs[0].r128,
                          segs[0].cta_begin, segs[0].k_tiles), flush=True)
+        global LAUNCHES
+        LAUNCHES += 1
         N.check(_lib().qg_tiled_epoch(arr, len(chunk), bar.data_ptr(), N.stream()), "qg_tiled_epoch")
 
 

@@ -108,3 +108,31 @@ def test_op_counters_after_a_chained_forward():
     want = bitgemm.op_counters()
     _forward(batches, model, True)
     assert bitgemm.op_counters() == want
+
+
+@pytest.mark.parametrize("name,nb", [("C3", 24), ("C2", None), ("C4", 6)])
+def test_dataflow_epoch_equals_per_stage_launches(name, nb):
+    """The dataflow epoch kernel (one tile queue over all stages, per-row-block completion
+    counters instead of grid barriers; many tiles per CTA) returns the per-stage logits bit
+    for bit, eager and as a captured graph replayed twice."""
+    import torch
+
+    from paper_2111_09547_b200 import tiled
+    from paper_2111_09547_b200.runtime import EpochRunner
+    cfg = synth.with_bits(synth.CONFIGS[name], 4)
+    kw = {"batch_ids": range(nb)} if nb else {}
+    batches, feats, _ = synth.planted_batches(cfg, seed=7, **kw)
+    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=7)
+    want = [o.cpu() for o in engine.model_forward_group(batches, model)]
+    saved = tiled.DATAFLOW
+    try:
+        tiled.DATAFLOW = True
+        got = [o.cpu() for o in engine.model_forward_group(batches, model)]
+        runner = EpochRunner(model, batches, rescan=False).capture()
+        for _ in range(2):
+            outs = [o.cpu() for o in runner.run()]
+            torch.cuda.synchronize()
+            assert all(torch.equal(a, b) for a, b in zip(outs, want))
+    finally:
+        tiled.DATAFLOW = saved
+    assert all(torch.equal(a, b) for a, b in zip(got, want))

@@ -267,7 +267,7 @@ def test_bindings_match_golden():
         bb.to_val(ha)
 
 
-@pytest.mark.parametrize("variant", ["fused_epoch", "a_bits", "screen", "no_chain", "default"])
+@pytest.mark.parametrize("variant", ["fused_epoch", "dataflow", "a_bits", "screen", "no_chain", "default"])
 @pytest.mark.parametrize("i", [0, 3, 5])
 def test_opt_in_kernel_variants_match_golden(variant, i):
     """The opt-in engine variants (persistent fused epoch, in-smem adjacency expansion,
@@ -277,9 +277,10 @@ def test_opt_in_kernel_variants_match_golden(variant, i):
     c = model_case(load("model"), i)
     batch, _ = _batch_from_case(c)
     model = _model_from_case(c)
-    saved = (engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN, engine.CHAIN)
+    saved = (engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN, engine.CHAIN, tiled.DATAFLOW)
     try:
         engine.FUSED_EPOCH = variant == "fused_epoch"
+        tiled.DATAFLOW = variant == "dataflow"
         tiled.A_BITS = variant == "a_bits"
         engine.SCREEN = variant == "screen"
         engine.CHAIN = variant != "no_chain"
@@ -287,7 +288,7 @@ def test_opt_in_kernel_variants_match_golden(variant, i):
             batch.adjacency._blocked = None          # rebuild the blocks for the packed-operand path
         np.testing.assert_array_equal(bg.model_forward(batch, model), c.logits)
     finally:
-        engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN, engine.CHAIN = saved
+        engine.FUSED_EPOCH, tiled.A_BITS, engine.SCREEN, engine.CHAIN, tiled.DATAFLOW = saved
 
 
 def test_pipelined_e2e_runner_equals_single_graph():
