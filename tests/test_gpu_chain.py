@@ -136,3 +136,31 @@ def test_dataflow_epoch_equals_per_stage_launches(name, nb):
     finally:
         tiled.DATAFLOW = saved
     assert all(torch.equal(a, b) for a, b in zip(got, want))
+
+
+@pytest.mark.parametrize("kind", ["gcn", "gin"])
+@pytest.mark.parametrize("split", [True, False], ids=["pairs", "single"])
+def test_chained_row_blocks_without_adjacency_blocks(kind, split):
+    """A 128-row block with no non-zero adjacency block (isolated nodes, no self loops):
+    the chained stage-1 tile has no MMA (zero accumulator) and its stage 2 still runs.
+    Chained == two-launch == CPU oracle."""
+    from oracle import qgtc_oracle as O
+    from paper_2111_09547_b200 import bitpack, graph
+    cfg = GraphConfig("chain-empty", kind, 600, 3000, 2, 2, 48, 64, 7, 3, 3, 3)
+    batches, feats, xp = synth.planted_batches(cfg, seed=8)
+    b = batches[0]
+    a = b.adjacency
+    dense = O.unpack_words(np.asarray(a.words), O.COL, a.logical_rows, a.logical_cols, a.padded_rows,
+                           a.padded_cols)
+    dense[128:256, :] = 0                                   # row block 1: no edges at all
+    words, pr, pc = O.pack_words(dense, O.COL, 8)
+    adj = bitpack.PackedBitMatrix(bitpack.COLUMN_WISE, a.logical_rows, a.logical_cols, pr, pc, words)
+    nb = graph.SubgraphBatch(node_ids=b.node_ids, adjacency=adj, features=b.features, boundaries=b.boundaries,
+                             x_params=b.x_params)
+    model = synth.calibrated_model(cfg, nb, feats[0], seed=8)
+    got, _ = _forward([nb], model, True, split)
+    want, _ = _forward([nb], model, False)
+    np.testing.assert_array_equal(got[0], want[0])
+    codes = O.quantize_codes(feats[0], xp.alpha_min, xp.alpha_max, xp.bits)
+    np.testing.assert_array_equal(got[0], O.model_forward(words, (a.logical_rows, a.logical_cols, pr, pc), codes,
+                                                          xp, model.layers))
