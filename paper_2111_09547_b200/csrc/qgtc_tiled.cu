@@ -796,7 +796,12 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); mbar_init(&aready[i], 6); }
+    // aready: one arrival per expander warp (warps 2..)
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&aready[i], (blockDim.x >> 5) - 2);
+    }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
