@@ -37,6 +37,7 @@ CASES = [
     ("gcn", 200, 64, 9, 3, 3, 2),
     ("gcn", 256, 16, 3, 2, 8, 8),
     ("gcn", 24, 256, 33, 2, 5, 6),
+    ("gcn", 64, 16, 3, 2, 2, 2),        # C1-like: split pairs with 16-column stage-2 halves
 ]
 
 
