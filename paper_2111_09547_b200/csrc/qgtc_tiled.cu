@@ -14,6 +14,13 @@
 // No per-tile __syncthreads.  One launch may cover many batches ("segments"):
 // CTA -> (segment, 128-row block, N tile), so an epoch layer stage over all
 // subgraph batches is a single grid.
+//
+// Variants: CHAIN (qg_chain) runs a second, dense GEMM behind the epilogue over the
+// requantized codes left in the ring's shared memory (aggregation -> update in one
+// launch; chain == 2 splits it over a 2-CTA cluster exchanging codes through DSMEM);
+// tc_pair_kernel runs cta_group::2 MMAs (M = 256) for large int32 GEMMs; the epoch
+// kernel runs all stages of an epoch in one persistent grid (grid barriers, or the
+// dataflow mode's per-row-block completion counters).
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
