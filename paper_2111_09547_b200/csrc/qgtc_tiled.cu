@@ -45,6 +45,7 @@ struct TiledParams {
   int64_t total_ctas;       // work items (segment, row block, N tile) of this stage
   int32_t a_bits;           // 1: adjacency blocks are shipped packed (2 KB) and expanded in smem
   int32_t pair;             // 1: CTA pairs (cluster of 2) run cta_group::2 MMAs, M = 256
+  int32_t pair_swizzle;     // pair kernels: row-block pairs per N-major group (1 = plain order)
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory.  chain 1: one CTA per row block (n_tiles 1);
@@ -907,6 +908,22 @@ struct UnionCursor {
   }
 };
 
+// Work-item order of the pair kernels within a segment: groups of `gh` row-block pairs
+// walked N-tile-major, so the tiles in flight at once share their A row blocks and B
+// column tiles in L2 (gh = 1: row-pair-major, the plain order).  A bijection on
+// [0, nrbp * n_tiles).
+__device__ __forceinline__ void pair_swizzle(int64_t local, int64_t nrbp, int n_tiles, int gh, int64_t& rbp, int& nt) {
+  if (gh <= 1) {
+    rbp = local / n_tiles;
+    nt = (int)(local % n_tiles);
+    return;
+  }
+  const int64_t group = (int64_t)gh * n_tiles, g = local / group, r = local % group;
+  const int64_t rows = nrbp - g * gh < gh ? nrbp - g * gh : gh;
+  nt = (int)(r / rows);
+  rbp = g * gh + r % rows;
+}
+
 template <int TMEM_COLS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
     tc_pair_kernel(const __grid_constant__ TiledParams P) {
@@ -930,10 +947,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   }
   const qg_tseg& G = P.segs[lo];
   const int64_t local = pair - G.cta_begin;
-  const int64_t rbp = local / P.n_tiles;
-  const int nt = (int)(local % P.n_tiles);
-  const int64_t n0 = (int64_t)nt * bn;
   const int64_t nrb = G.r128 >> 7;
+  int64_t rbp;
+  int nt;
+  pair_swizzle(local, (nrb + 1) >> 1, P.n_tiles, P.pair_swizzle, rbp, nt);
+  const int64_t n0 = (int64_t)nt * bn;
   const int64_t rb = rbp * 2 + rank;                     // this CTA's row block (may be past the end)
   const int64_t rb_other = rbp * 2 + (rank ^ 1);
   const bool rb_ok = rb < nrb, other_ok = rb_other < nrb;
@@ -1101,6 +1119,218 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   cluster_sync_all();                                    // both CTAs done with TMEM and the ring
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 5);
+}
+
+// ------------------------------------------------ persistent 2-SM int32 GEMM
+// Persistent CTA pairs (one CTA per SM) for the int32 output mode: each pair loops over
+// (segment, row-block pair, N tile) work items with TWO TMEM accumulators (2 x bn
+// columns).  The producer and the leader's MMA thread run ahead into the next tile while
+// 8 epilogue warps per CTA drain the previous accumulator, so a tile's epilogue overlaps
+// the next tile's main loop inside the pair (the one-tile pair kernel relies on a second
+// co-resident CTA for that).  Barriers: full/empty (ring, as tc_pair_kernel), tfull[b]
+// (MMA commit -> both CTAs' epilogue warps), tempty[b] (16 epilogue-warp arrivals of both
+// CTAs, on the leader -> the MMA may overwrite accumulator b).
+constexpr int kPersistThreads = 320;    // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
+
+__device__ __forceinline__ void pair_item(const TiledParams& P, int64_t pair, const qg_tseg*& Gp, int64_t& rbp,
+                                          int& nt) {
+  int lo = 0, hi = P.nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.segs[mid].cta_begin <= pair) lo = mid; else hi = mid - 1;
+  }
+  Gp = &P.segs[lo];
+  const int64_t local = pair - Gp->cta_begin;
+  pair_swizzle(local, ((Gp->r128 >> 7) + 1) >> 1, P.n_tiles, P.pair_swizzle, rbp, nt);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPersistThreads, 1)
+    tc_pair_persist_kernel(const __grid_constant__ TiledParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int bn = P.bn, S = P.stages, bh = bn >> 1;
+  const int64_t pair_step = (int64_t)(gridDim.x >> 1), pair0 = (int64_t)(blockIdx.x >> 1);
+  const int64_t total_pairs = P.total_ctas >> 1;
+  const uint32_t a_bytes = 16384u, bh_bytes = (uint32_t)bh * 128u, stage_bytes = a_bytes + bh_bytes;
+  uint8_t* stage0 = smem;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 16); }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();                                    // barriers of both CTAs initialised
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer (both CTAs): own A block + own half of B, all tiles ----------------
+    const uint32_t leader_full = mapa_cluster(smem_u32(&full[0]), 0);
+    uint32_t it = 0;
+    for (int64_t pair = pair0; pair < total_pairs; pair += pair_step) {
+      const qg_tseg* Gp;
+      int64_t rbp;
+      int nt;
+      pair_item(P, pair, Gp, rbp, nt);
+      const qg_tseg& G = *Gp;
+      const int64_t n0 = (int64_t)nt * bn, nrb = G.r128 >> 7, rb = rbp * 2 + rank;
+      const bool rb_ok = rb < nrb;
+      const int64_t b_row0 = ((n0 + (int64_t)rank * bh) >> 3) * 8;
+      UnionCursor c{};
+      int nk = G.k_tiles, kbase_me = 0, i_me = 0;
+      if (P.a_blocks) {
+        const int64_t rb0 = rbp * 2, rb1 = rbp * 2 + 1;
+        c.l0 = G.blk_kt + G.blk_base[rb0];
+        c.n0 = G.blk_count[rb0];
+        c.l1 = rb1 < nrb ? G.blk_kt + G.blk_base[rb1] : nullptr;
+        c.n1 = rb1 < nrb ? G.blk_count[rb1] : 0;
+        kbase_me = rb_ok ? G.blk_base[rb] : 0;
+        nk = 0x7fffffff;
+      }
+      for (int k = 0; k < nk; ++k, ++it) {
+        int kt;
+        const void* amap;
+        int64_t arow;
+        if (P.a_blocks) {
+          if (!(c.i0 < c.n0 || c.i1 < c.n1)) break;
+          bool h0, h1;
+          kt = c.next(h0, h1);
+          const bool mine = rank == 0 ? h0 : h1;
+          const bool real = rb_ok && mine;
+          amap = real ? (const void*)G.tmap_a : (const void*)&P.zero_map;
+          arow = real ? (int64_t)(kbase_me + i_me) * 128 : 0;
+          i_me += mine;
+        } else {
+          kt = k;
+          amap = rb_ok ? (const void*)G.tmap_a : (const void*)&P.zero_map;
+          arow = rb_ok ? (((int64_t)kt * (G.r128 << 7) + rb * 16384) >> 7) : 0;
+        }
+        const int s = (int)(it % (uint32_t)S);
+        if (it >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
+        uint8_t* dst = stage0 + (size_t)s * stage_bytes;
+        if (rank == 0) mbar_expect_tx(&full[s], 2u * (a_bytes + bh_bytes));
+        const uint32_t bar = leader_full + (uint32_t)s * 8u;
+        tma_2d_pair(dst, amap, 0, (int32_t)arow, bar);
+        tma_2d_pair(dst + a_bytes, G.tmap_b, 0, (int32_t)(((int64_t)kt * (P.b_npad << 7) >> 7) + b_row0), bar);
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ---------------- MMA issuer (leader), accumulators alternate per tile ----------------
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    uint32_t it = 0;
+    int tcount = 0;
+    for (int64_t pair = pair0; pair < total_pairs; pair += pair_step, ++tcount) {
+      const qg_tseg* Gp;
+      int64_t rbp;
+      int nt;
+      pair_item(P, pair, Gp, rbp, nt);
+      const qg_tseg& G = *Gp;
+      int nk = G.k_tiles;
+      if (P.a_blocks) {
+        const int64_t nrb = G.r128 >> 7, rb0 = rbp * 2, rb1 = rbp * 2 + 1;
+        UnionCursor c{};
+        c.l0 = G.blk_kt + G.blk_base[rb0];
+        c.n0 = G.blk_count[rb0];
+        c.l1 = rb1 < nrb ? G.blk_kt + G.blk_base[rb1] : nullptr;
+        c.n1 = rb1 < nrb ? G.blk_count[rb1] : 0;
+        nk = 0;
+        bool h0, h1;
+        while (c.i0 < c.n0 || c.i1 < c.n1) { c.next(h0, h1); ++nk; }
+      }
+      const int b = tcount & 1;
+      const uint32_t use = (uint32_t)(tcount >> 1);
+      if (use > 0) mbar_wait(smem_u32(&tempty[b]), (use - 1) & 1);   // both CTAs drained accumulator b
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t acc = tmem + (uint32_t)(b * bn);
+      for (int k = 0; k < nk; ++k, ++it) {
+        const int s = (int)(it % (uint32_t)S);
+        mbar_wait(smem_u32(&full[s]), (it / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_i8_pair(acc, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc, (k > 0 || kk > 0) ? 1u : 0u);
+        umma_commit_pair(&empty[s]);
+      }
+      if (nk > 0) {
+        umma_commit_pair(&tfull[b]);
+      } else {
+        // no K tile: nothing to commit; release both CTAs' epilogues directly (zeros)
+        mbar_arrive(&tfull[b]);
+        mbar_arrive_remote(mapa_cluster(smem_u32(&tfull[b]), 1));
+      }
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: 8 warps; warp w reads TMEM lanes 32*(w % 4).., column half (w-2)/4
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t leader_tempty = mapa_cluster(smem_u32(&tempty[0]), 0);
+    int tcount = 0;
+    for (int64_t pair = pair0; pair < total_pairs; pair += pair_step, ++tcount) {
+      const qg_tseg* Gp;
+      int64_t rbp;
+      int nt;
+      pair_item(P, pair, Gp, rbp, nt);
+      const qg_tseg& G = *Gp;
+      const int64_t n0 = (int64_t)nt * bn, nrb = G.r128 >> 7, rb = rbp * 2 + rank;
+      bool has_acc = G.k_tiles > 0;
+      if (P.a_blocks) {
+        const int64_t rb1 = rbp * 2 + 1;
+        has_acc = G.blk_count[rbp * 2] + (rb1 < nrb ? G.blk_count[rb1] : 0) > 0;
+      }
+      const int b = tcount & 1;
+      mbar_wait(smem_u32(&tfull[b]), (uint32_t)(tcount >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int64_t myrow = rb * 128 + quad * 32 + lane;
+      const bool rvalid = rb < nrb && myrow < G.m;
+      const int64_t rem = P.n - n0;
+      const int ncols = rem <= 0 ? 0 : (rem < bn ? (int)rem : bn);
+      const int nslices = (ncols + 7) >> 3;
+      const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
+      const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * bn);
+      for (int sl = half; sl < nslices; sl += 2) {
+        uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (has_acc) {
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                         "=r"(v[7])
+                       : "r"(trow + (uint32_t)(sl * 8)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
+        if (rvalid) {
+          int32_t* dst = G.out_i32 + myrow * P.n + n0 + sl * 8;
+          if (vec_ok && sl * 8 + 8 <= ncols) {
+            reinterpret_cast<int4*>(dst)[0] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+            reinterpret_cast<int4*>(dst)[1] = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (sl * 8 + jj < ncols) dst[jj] = (int32_t)v[jj];
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) mbar_arrive(&tempty[b]);
+        else mbar_arrive_remote(leader_tempty + (uint32_t)b * 8u);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();                                    // both CTAs done with TMEM and the ring
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // ------------------------------------------------ persistent epoch kernel
@@ -1569,10 +1799,45 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     void* zero = nullptr;
     cudaGetSymbolAddress(&zero, g_zero_block);
     if (qg_encode_linear_map(zero, 16384, 128, &P.zero_map) != QG_OK) return QG_ERR_UNSUPPORTED;
+    // 8 row-block pairs per N-major group: the ~148 pairs in flight then share A row
+    // blocks and B column tiles in L2 (C5 16k: 73% -> 79% of the int8 peak)
+    static const int swz = getenv("QG_PAIR_SWIZZLE") ? atoi(getenv("QG_PAIR_SWIZZLE")) : 8;
+    P.pair_swizzle = swz < 1 ? 1 : swz;
     const size_t stage = 16384 + (size_t)P.bn * 64;
+    cudaStream_t st = (cudaStream_t)stream;
+    static const bool persist = getenv("QG_PAIR_PERSIST") != nullptr && atoi(getenv("QG_PAIR_PERSIST")) != 0;
+    if (persist && P.mode == QG_GEMM_I32) {
+      // persistent pairs, one CTA per SM: a deep ring and two TMEM accumulators
+      static int psms = 0;
+      if (!psms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&psms, cudaDevAttrMultiProcessorCount, dev);
+      }
+      P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (size_t)(200 * 1024) / stage));
+      const size_t smem = (size_t)P.stages * stage;
+      static size_t pattr = 0;
+      if (smem > pattr) {
+        cudaFuncSetAttribute(tc_pair_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        pattr = smem;
+      }
+      const int64_t grid = std::min<int64_t>(a->total_ctas, (int64_t)(psms & ~1));
+      static const bool pdl = getenv("QG_NO_PDL") == nullptr;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3(kPersistThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl ? 1 : 0;
+      cudaLaunchKernelEx(&cfg, tc_pair_persist_kernel, P);
+      return tstatus();
+    }
     P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
     const size_t smem = (size_t)P.stages * stage + cols;
-    cudaStream_t st = (cudaStream_t)stream;
     const unsigned grid = (unsigned)a->total_ctas;
     switch (P.bn) {
       case 64: launch_pair<64>(P, grid, smem, st); break;
