@@ -1,21 +1,32 @@
-"""QGTC B200 benchmark (driver contract; see DESIGN.md "Measurement").
+"""QGTC B200 benchmark (driver contract; see DESIGN.md section 5).
 
 Metric (BASELINE.json): QGNN inference ms/epoch per bitwidth, plus bit-GEMM
-effective TOPS vs the tensor-pipe peak.  Workload at N=1: configs[1] -- a
-3-layer GIN (hidden 64) over a synthetic BlogCatalog-shaped graph (10k nodes,
-334k undirected edges, 16 planted parts in one batch), bit sweep 1..8; the
-headline is the 4-bit point (the reference CLI default, cli.py:112-113).
+effective TOPS vs the tensor-pipe peak.  Default workload: configs[3] = C4, the
+north star's target config -- a 3-layer GIN (hidden 256, 8-bit features /
+activations / weights) over a synthetic ogbn-products-shaped planted graph
+(2,449,029 nodes, 61.9M undirected edges, 1,500 parts, 8 parts per batch =
+188 subgraph batches).  It fits one B200.
 
-A step = one epoch = the reference's timed region (cli.py:215-222): every
-batch through model_forward.  Ours replays it as ONE CUDA graph (tile scan +
-fused bit-GEMMs).  `value` is device-resident ms/epoch (L2 flushed between
-steps, events around each step); `e2e` is the same epoch through the public
-runtime with pinned host QGT2 images -> H2D -> graph -> fp64 logits D2H.
+A step = one epoch = the reference's timed region (cli.py:215-222): every batch
+through ``model_forward``.
 
-`--impl reference` times the reference algorithm's CPU port (oracle/) on all
-host cores (process pool over the independent subgraph parts) on the same
-config.  N>1 (torchrun): weak scaling -- every rank runs its own epoch
-replica (different seed), value = total time / epochs of all ranks.
+* ``value``: device-resident ms/epoch, the epoch replayed as ONE CUDA graph, L2
+  flushed between steps (the C4 inputs are also > L2).
+* ``e2e``: the public runtime (``runtime.HostEpochRunner``): pinned host QGT3
+  images -> H2D -> epoch -> fp64 logits D2H into pinned host memory, every
+  step.  ``e2e_dropin``: the reference-API call sequence per batch,
+  ``model_forward(unpack_batch(QGTB bytes), model)`` -> numpy (eager).
+* N > 1: ``--gpus N`` spawns N ranks itself (torch.distributed.run) unless
+  launched under torchrun.  Multi-batch configs (C3/C4) SHARD the batches (LPT,
+  strong scaling, no data-path collective: every rank D2Hs its own logits over
+  its own PCIe link); the NCCL gather of all logits to rank 0 is timed
+  separately (``collective``).  Single-batch configs (C1/C2) run replicas.
+
+``--impl reference`` times the REAL reference (``oracle/_ref/bitgnn``, staged
+by oracle/make_ref.py) -- ``model_forward`` on batches built on the host by the
+reference's own ``build_batch``, nothing from this package's kernels -- over a
+process pool on all host cores, on a bounded sample of subgraph parts,
+extrapolated to the epoch and labelled so.
 """
 
 from __future__ import annotations
@@ -23,6 +34,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -41,30 +54,40 @@ INT8_PEAK_FILE = os.path.join(ROOT, "profiles", "int8_peak.json")
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=1000)
-    p.add_argument("--warmup", type=int, default=20)
-    p.add_argument("--config", default="C2")
-    p.add_argument("--bits", type=int, default=4)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
+    p.add_argument("--bits", type=int, default=None, help="feature/weight bits (default: the config's)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the C2 bit sweep, the C5 point and bit_qnt")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-sample-s", type=float, default=12.0)
-    p.add_argument("--no-c5", action="store_true")
+    p.add_argument("--no-dropin", action="store_true")
+    p.add_argument("--ref-budget-s", type=float, default=120.0)
     p.add_argument("--c5-n", type=int, default=16384)
     return p.parse_args()
 
 
 # ----------------------------------------------------------------- helpers
-def dist_setup():
+def spawn_ranks(args) -> None:
+    """--gpus N without torchrun: re-launch this script under torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def dist_setup(impl):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 and impl == "ours":
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -82,6 +105,18 @@ def max_over_ranks(world, v: float) -> float:
     t = torch.tensor([v], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def host_info(cores_used: int) -> dict:
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "cores_used": cores_used, "lscpu_model": model}
 
 
 class ClockSampler:
@@ -143,32 +178,39 @@ def int8_peak_tops():
     return 2.0 * bf16, "2 x measured bf16 (MEASURED_PEAKS.json)"
 
 
+def hbm_peak_gbs():
+    if os.path.exists(MEASURED):
+        return float(json.load(open(MEASURED))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    return 6531.9, "B200_PROFILING.md fallback"
+
+
+def so_loaded() -> list:
+    """In-tree native libraries mapped into this process (evidence for the arms)."""
+    try:
+        with open("/proc/self/maps") as fh:
+            return sorted({ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so") and ROOT in ln})
+    except OSError:
+        return []
+
+
 # --------------------------------------------------------------- workload
-def build_workload(cfg_name, bits, seed, batch_ids=None):
+def config_of(name, bits):
+    from paper_2111_09547_b200 import synth_host
+    base = synth_host.CONFIGS[name]
+    return synth_host.with_bits(base, bits) if bits is not None else base
+
+
+def build_workload(cfg, seed, batch_ids=None):
     """Batches (all, or ``batch_ids``) + a model calibrated on global batch 0 (cli.py:209)."""
     from paper_2111_09547_b200 import synth
-    cfg = synth.with_bits(synth.CONFIGS[cfg_name], bits)
     if batch_ids is None:
         batches, feats, _ = synth.planted_batches(cfg, seed=seed)
         model = synth.calibrated_model(cfg, batches[0], feats[0], seed=seed)
-        return cfg, batches, feats, model
+        return batches, feats, model
     b0, f0, _ = synth.planted_batches(cfg, seed=seed, batch_ids=[0])
     model = synth.calibrated_model(cfg, b0[0], f0[0], seed=seed)
     batches, feats, _ = synth.planted_batches(cfg, seed=seed, batch_ids=batch_ids)
-    return cfg, batches, feats, model
-
-
-class ShardedStep:
-    """One sharded epoch step: this rank's epoch graph over its LPT share of the batches,
-    then ONE all_gather_into_tensor of the logits (NCCL) -- paper_2111_09547_b200.shard."""
-
-    def __init__(self, runner, gather):
-        self.runner, self.gather, self.stream = runner, gather, runner.stream
-
-    def run(self):
-        outs = self.runner.run()
-        self.gather.gather(outs)
-        return outs
+    return batches, feats, model
 
 
 def time_device_epochs(runner, steps, warmup, world):
@@ -217,6 +259,28 @@ def time_e2e(host_runner, steps, warmup, world):
     return sum(s.elapsed_time(e) for s, e in ev), wall
 
 
+def time_dropin(batches, model, steps, world):
+    """Reference-API sequence per batch: QGTB bytes on the host -> unpack_batch (one H2D)
+    -> model_forward -> numpy fp64 logits.  Wall clock per epoch (host-synchronous API)."""
+    import torch
+    import paper_2111_09547_b200 as bg
+    bufs = [bg.pack_batch(b).data for b in batches]
+    h2d = sum(len(x) for x in bufs)
+    d2h = sum(b.total_nodes for b in batches) * model.layers[-1].out_dim * 8
+
+    def epoch():
+        return [bg.model_forward(bg.unpack_batch(x), model) for x in bufs]
+    epoch()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        outs = epoch()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    barrier(world)
+    return ms, h2d, d2h, outs
+
+
 def kernel_roofline(model, batches, reps=20):
     """Bit-GEMM launch durations inside the epoch graph.  CUDA events cannot sit between
     the kernels of one graph, so an identical epoch graph is captured with per-CTA
@@ -243,152 +307,278 @@ def kernel_roofline(model, batches, reps=20):
             ops += sum(w for _, w in ks)
             launches += len(ks)
             step_ms += s.elapsed_time(e)
+    del r
     return spans / reps, ops / reps, launches / reps, step_ms / reps
 
 
-# ------------------------------------------------------------- CPU oracle
-def _oracle_part_inputs(batch, feats, parts):
-    """Host operands of the first `parts` subgraphs (block-diagonal => independent)."""
-    from oracle import qgtc_oracle as O
-    hi = int(batch.boundaries[parts])
-    a = batch.adjacency
-    dense = O.unpack_words(a.words, O.COL, a.logical_rows, a.logical_cols, a.padded_rows, a.padded_cols)
-    sub = np.ascontiguousarray(dense[:hi, :hi])
-    aw, pr, pc = O.pack_words(sub, O.COL, 8)
-    return aw, (hi, hi, pr, pc), np.asarray(feats[:hi], dtype=np.float64)
+# --------------------------------------------------- real reference (CPU)
+def _ref_module():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import make_ref
+    if not make_ref.available():
+        return None
+    return make_ref.import_reference()
 
 
-def _oracle_forward(args):
-    aw, dims, feats, x, layers = args
-    sys.path.insert(0, ROOT)
-    from oracle import qgtc_oracle as O
-    codes = O.quantize_codes(feats, x.alpha_min, x.alpha_max, x.bits)
-    return O.model_forward(aw, dims, codes, x, layers)
+def _ref_model(R, cfg, seed):
+    """Reference ModelConfig: the reference preset (same seed => same weights) calibrated
+    by the reference's calibrate_model on the reference-built global batch 0."""
+    from paper_2111_09547_b200 import synth_host as H
+    builder = R.gcn_model if cfg.model == "gcn" else R.gin_model
+    model = builder(cfg.in_dim, cfg.classes, hidden_dim=cfg.hidden, num_layers=cfg.layers,
+                    feature_bits=cfg.bits, weight_bits=cfg.wbits, seed=seed)
+    edges, bnd, x = H.host_batch(cfg, seed, 0)
+    b0 = _ref_build(R, cfg, edges, bnd, x)
+    R.calibrate_model(model, b0, np.asarray(x, dtype=np.float64))
+    return model
 
 
-def _part_slices(batch, feats):
-    from oracle import qgtc_oracle as O
-    a = batch.adjacency
-    dense = O.unpack_words(a.words, O.COL, a.logical_rows, a.logical_cols, a.padded_rows, a.padded_cols)
-    out = []
-    for p in range(batch.num_subgraphs):
-        lo, hi = int(batch.boundaries[p]), int(batch.boundaries[p + 1])
-        aw, pr, pc = O.pack_words(np.ascontiguousarray(dense[lo:hi, lo:hi]), O.COL, 8)
-        out.append((aw, (hi - lo, hi - lo, pr, pc), np.asarray(feats[lo:hi], dtype=np.float64)))
-    return out
+def _ref_build(R, cfg, edges, boundaries, x):
+    """Reference build_batch over the parts in ``edges`` (their own graph: cross-part
+    edges are dropped by build_batch anyway, graph.py:337)."""
+    from paper_2111_09547_b200 import synth_host as H
+    total = int(boundaries[-1])
+    el = H.batch_edge_list(edges, boundaries, self_loops=False)
+    g = R.Graph(total, el, features=np.asarray(x, dtype=np.float64))
+    part_of = np.repeat(np.arange(len(boundaries) - 1), np.diff(boundaries))
+    assign = R.PartitionAssignment(len(boundaries) - 1, part_of)
+    return R.build_batch(g, assign, list(range(len(boundaries) - 1)), R.QuantParams(0.0, 1.0, cfg.bits))
 
 
-def cpu_baseline(batches, feats, model, x_params, logits_dev, budget_s):
-    """Single-thread oracle on the first parts of batch 0; extrapolated to the epoch."""
-    b0 = batches[0]
-    parts = 1
-    t_used, out = None, None
-    while True:
-        args = _oracle_part_inputs(b0, feats[0], parts) + (x_params, model.layers)
+def ref_part_batch(R, cfg, seed, b, p):
+    """Part p of batch b as a one-part reference SubgraphBatch + its host features."""
+    from paper_2111_09547_b200 import synth_host as H
+    edges, bnd, x = H.host_batch(cfg, seed, b)
+    lo, hi = int(bnd[p]), int(bnd[p + 1])
+    xb = x[lo:hi]
+    return _ref_build(R, cfg, [edges[p]], np.array([0, hi - lo]), xb), lo, hi
+
+
+def sample_parts(cfg, n, seed=0):
+    """A fixed spread of (batch, part) ids: first and last part, the rest seeded random."""
+    from paper_2111_09547_b200 import synth_host as H
+    nb = H.num_batches(cfg)
+    allp = [(b, p) for b in range(nb) for p in range(len(H.batch_part_sizes(cfg)[b]))]
+    if n >= len(allp):
+        return allp
+    rng = np.random.default_rng(seed)
+    mid = rng.choice(np.arange(1, len(allp) - 1), size=max(0, n - 2), replace=False)
+    return [allp[0]] + [allp[i] for i in sorted(mid)] + [allp[-1]]
+
+
+_POOL_STATE = {}
+
+
+def _pool_forward(i):
+    from threadpoolctl import threadpool_limits
+    R, model, batches = _POOL_STATE["R"], _POOL_STATE["model"], _POOL_STATE["batches"]
+    with threadpool_limits(1):
         t0 = time.perf_counter()
-        out = _oracle_forward(args)
-        t_used = time.perf_counter() - t0
-        if t_used * 2 > budget_s or parts * 2 > b0.num_subgraphs:
-            break
-        parts *= 2
-    hi = int(b0.boundaries[parts])
-    exact = bool(np.array_equal(out, logits_dev[0][:hi].cpu().numpy()))
-    total_parts = sum(b.num_subgraphs for b in batches)
-    ms_epoch = t_used * 1e3 * total_parts / parts
-    return {"value": ms_epoch, "unit": "ms/epoch", "cores": 1, "kind": "port",
-            "sample": f"oracle/qgtc_oracle.model_forward on {parts}/{total_parts} subgraph parts "
-                      f"({hi} nodes, {t_used:.1f} s), x{total_parts / parts:g} extrapolated",
-            "parity_on_sample": "bit-exact" if exact else "MISMATCH"}
+        R.model_forward(batches[i], model)
+        return time.perf_counter() - t0
 
 
-# ----------------------------------------------------------- reference arm
 def reference_arm(args, world, rank):
+    """--impl reference: the real bitgnn.model_forward on host-built batches, all cores."""
     if rank != 0:
         return
     import multiprocessing as mp
-    cfg, batches, feats, model = build_workload(args.config, args.bits, seed=0)
-    x = batches[0].x_params
-    jobs = []
-    for b, f in zip(batches, feats):
-        for sl in _part_slices(b, f):
-            jobs.append(sl + (x, model.layers))
+    cfg = config_of(args.config, args.bits)
+    R = _ref_module()
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not staged (python oracle/make_ref.py)"}))
+        return
+    from paper_2111_09547_b200 import synth_host as H
     cores = os.cpu_count() or 1
+    total_parts = cfg.num_parts
+    t0 = time.perf_counter()
+    model = _ref_model(R, cfg, seed=0)
+    sample = sample_parts(cfg, cores)
+    batches = [ref_part_batch(R, cfg, 0, b, p)[0] for b, p in sample]
+    setup_s = time.perf_counter() - t0
+    _POOL_STATE.update(R=R, model=model, batches=batches)
+    pool_n = min(cores, len(batches))
     ctx = mp.get_context("fork")
-    steps, warm = max(1, args.steps), max(0, args.warmup)
-    # bounded: cap the timed loop so the whole run stays within a few minutes
-    with ctx.Pool(min(cores, len(jobs))) as pool:
+    with ctx.Pool(pool_n) as pool:
         t0 = time.perf_counter()
-        pool.map(_oracle_forward, jobs, chunksize=1)
+        pool.map(_pool_forward, range(len(batches)), chunksize=1)
         one = time.perf_counter() - t0
-        budget = 150.0
-        steps = max(1, min(steps, int(budget / max(one, 1e-3))))
-        warm = min(warm, 1)
-        for _ in range(warm):
-            pool.map(_oracle_forward, jobs, chunksize=1)
+        steps = max(1, min(args.steps, int(args.ref_budget_s / max(one, 1e-3))))
+        warm = min(args.warmup, 1)          # the probe step above is the first warm-up
+        for _ in range(max(0, warm - 1)):
+            pool.map(_pool_forward, range(len(batches)), chunksize=1)
         times = []
         for _ in range(steps):
             t0 = time.perf_counter()
-            pool.map(_oracle_forward, jobs, chunksize=1)
+            pool.map(_pool_forward, range(len(batches)), chunksize=1)
             times.append(time.perf_counter() - t0)
-    ms = float(np.mean(times)) * 1e3
+    step_s = float(np.mean(times))
+    sample_nodes = sum(b.total_nodes for b in batches)
+    ms = step_s * 1e3 * cfg.num_nodes / sample_nodes
+    hi = host_info(pool_n)
     line = {
-        "metric": METRIC,
-        "value": ms, "unit": "ms/epoch", "impl": "reference", "n_gpus": args.gpus, "steps": steps,
-        "warmup": warm, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": f"u{args.bits}", "data": "synthetic",
-        "config": {"workload": cfg.name, "bits": args.bits, "nodes": cfg.num_nodes,
-                   "edges_undirected": cfg.num_edges, "parts": cfg.num_parts},
-        "cpu_baseline": {"value": ms, "unit": "ms/epoch", "cores": min(cores, len(jobs)), "kind": "port",
-                         "sample": f"full epoch: {len(jobs)} independent subgraph parts over a "
-                                   f"{min(cores, len(jobs))}-process pool (oracle/qgtc_oracle.py)"},
-        "e2e": {"value": ms, "unit": "ms/epoch", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "impl": "reference",
+        "value": round(ms, 3), "unit": "ms/epoch", "n_gpus": world, "steps": steps, "warmup": warm,
+        "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": f"u{cfg.bits} codes (numpy bit-serial AND+popcount, fp64 epilogue)",
+        "data": "synthetic planted-partition graph, U[0,1) features, random-init weights",
+        "config": {"workload": cfg.name, "model": f"{cfg.model} {cfg.layers} layers hidden {cfg.hidden}",
+                   "bits": cfg.bits, "nodes": cfg.num_nodes, "edges_undirected": cfg.num_edges,
+                   "parts": cfg.num_parts, "batches": H.num_batches(cfg)},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/epoch", "cores": pool_n, "kind": "reference",
+                         "sample": (f"real reference bitgnn.model_forward (oracle/_ref, staged unmodified from "
+                                    f"/root/reference) on {len(batches)} of {total_parts} subgraph parts "
+                                    f"({sample_nodes} of {cfg.num_nodes} nodes; first, last and seeded-random "
+                                    f"parts), each a one-part SubgraphBatch from the reference's build_batch, "
+                                    f"{pool_n}-process pool (1 BLAS thread each); step time x "
+                                    f"{cfg.num_nodes / sample_nodes:.1f} (node-proportional) = EXTRAPOLATED "
+                                    f"ms/epoch"),
+                         "host": hi, "setup_s": round(setup_s, 1), "step_s": [round(t, 3) for t in times]},
+        "e2e": {"value": round(ms, 3), "unit": "ms/epoch", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "our_native_so_loaded": so_loaded(),
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_one_core(cfg, model_ours, logits_batch0, budget_s=60.0):
+    """1-core real-reference time on the first part(s) of batch 0, extrapolated; the
+    reference's logits are compared with ours for those rows (config-scale parity)."""
+    from threadpoolctl import threadpool_limits
+    R = _ref_module()
+    if R is None:
+        return None
+    t0 = time.perf_counter()
+    model = _ref_model(R, cfg, seed=0)
+    setup_s = time.perf_counter() - t0
+    # calibrated grids must be the ones our engine derived (engine.calibrate_model mirror)
+    def grid(q):
+        return None if q is None else (q.alpha_min, q.alpha_max, q.bits)
+    grids_equal = all(
+        grid(a.mid_params) == grid(b.mid_params) and grid(a.out_params) == grid(b.out_params)
+        for a, b in zip(model.layers, model_ours.layers))
+    rb, lo, hi = ref_part_batch(R, cfg, 0, 0, 0)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        out = R.model_forward(rb, model)
+        t = time.perf_counter() - t0
+    exact = bool(np.array_equal(out, logits_batch0[lo:hi]))
+    ms = t * 1e3 * cfg.num_nodes / (hi - lo)
+    return {"value": round(ms, 1), "unit": "ms/epoch", "cores": 1, "kind": "reference",
+            "sample": (f"real reference bitgnn.model_forward (oracle/_ref), 1 core, on part 0 of batch 0 "
+                       f"({hi - lo} nodes, {t:.2f} s), x{cfg.num_nodes / (hi - lo):.0f} node-proportional = "
+                       f"EXTRAPOLATED ms/epoch"),
+            "parity_vs_reference_on_sample": "bit-exact" if exact else "MISMATCH",
+            "calibrated_grids_equal": bool(grids_equal), "setup_s": round(setup_s, 1),
+            "host": host_info(1)}
+
+
+# ------------------------------------------------------------------ extras
+def c2_sweep(steps):
+    """configs[1]: the C2 bit sweep 1..8 (device ms/epoch, one graph per epoch)."""
+    from paper_2111_09547_b200.runtime import EpochRunner
+    out = {}
+    for bits in range(1, 9):
+        cfg = config_of("C2", bits)
+        bb, _, mm = build_workload(cfg, seed=0)
+        rr = EpochRunner(mm, bb, rescan=False).capture()
+        t, _ = time_device_epochs(rr, steps, 5, 1)
+        out[str(bits)] = round(t / steps, 5)
+        del rr, bb, mm
+    return out
+
+
+def c5_point(n, bits, peak):
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from c5_sweep import run_point
+    c5 = run_point(n, 0.1, bits, reps=10, int8_peak=peak)
+    c5.update({"bound": "tensor", "peak": peak, "unit": "TOPS",
+               "kernel": "tc_pair_kernel (2-SM cluster, tcgen05.mma.cta_group::2.kind::i8 M=256, TMA)",
+               "config": "C5: A Bernoulli(0.1) 1-bit x X uniform codes, reduce_bitplanes(bmm_1bit_by_nbit) "
+                         "in one launch, CUDA-graph replays timed with CUDA events"})
+    return c5
 
 
 # ------------------------------------------------------------------- ours
 def ours(args, world, rank):
     import torch
     from paper_2111_09547_b200 import _native as N
+    from paper_2111_09547_b200 import shard, synth_host
     from paper_2111_09547_b200.runtime import EpochRunner, HostEpochRunner
 
     N.lib()
-    from paper_2111_09547_b200 import shard, synth
-    base = synth.with_bits(synth.CONFIGS[args.config], args.bits)
-    sizes = synth.batch_part_sizes(base)
+    cfg = config_of(args.config, args.bits)
+    sizes = synth_host.batch_part_sizes(cfg)
     sharded = world > 1 and len(sizes) > 1
+    plan = None
     if sharded:
         # strong scaling over independent subgraph batches: LPT plan, same on every rank
-        costs = [shard.batch_cost(s, base.in_dim, base.bits) for s in sizes]
+        costs = [shard.batch_cost(s, cfg.in_dim, cfg.bits) for s in sizes]
         plan = shard.assign_lpt(costs, world)
-        cfg, batches, feats, model = build_workload(args.config, args.bits, seed=0, batch_ids=plan[rank])
+        batches, feats, model = build_workload(cfg, seed=0, batch_ids=plan[rank])
     else:
         # replicas (a single-batch config cannot shard): every rank its own epoch
-        cfg, batches, feats, model = build_workload(args.config, args.bits, seed=rank)
+        batches, feats, model = build_workload(cfg, seed=rank)
     runner = EpochRunner(model, batches, rescan=False).capture()
-    step = runner
-    if sharded:
-        rows = [int(s.sum()) for s in sizes]
-        step = ShardedStep(runner, shard.LogitGather(plan, rows, model.layers[-1].out_dim, torch.device("cuda")))
-    total_ms, clocks = time_device_epochs(step, args.steps, args.warmup, world)
+    total_ms, clocks = time_device_epochs(runner, args.steps, args.warmup, world)
     total_ms = max_over_ranks(world, total_ms)
     epochs = args.steps if sharded else args.steps * world
     ms_epoch = total_ms / epochs
     launches = runner.kernel_launches_per_epoch() * args.steps
 
-    # end to end through the public runtime: pinned H2D -> graph -> D2H every step
+    # end to end through the public runtime: pinned H2D -> graph -> D2H every step (per rank)
     host = HostEpochRunner(model, batches)
     e2e_ms, e2e_wall = time_e2e(host, args.steps, min(args.warmup, 5), world)
     e2e_ms = max_over_ranks(world, e2e_ms) / epochs
-
-    # parity of the e2e path against the device path
     with torch.cuda.stream(runner.stream):
-        dev_logits = torch.cat([o for o in runner.run()])
+        dev_out = runner.run()
+        dev_logits = torch.cat(list(dev_out))
     torch.cuda.synchronize()
-    dev_logits = dev_logits.cpu()
+    dev_logits_h = dev_logits.cpu()
     host_out = host.run_host()
     host.stream.synchronize()
-    e2e_parity = bool(torch.equal(dev_logits, host_out))
+    e2e_parity = bool(torch.equal(dev_logits_h, host_out))
+    logits_b0 = dev_out[0].cpu().numpy()
+    e2e_h2d, e2e_d2h = host.h2d_bytes, host.d2h_bytes
+    del host
+    torch.cuda.empty_cache()
+
+    collective = None
+    if sharded:
+        # the only collective: all logits to rank 0 (NCCL over NVLink), timed on its own
+        import torch.distributed as dist
+        rows = [int(s.sum()) for s in sizes]
+        gather = shard.LogitGather(plan, rows, model.layers[-1].out_dim, torch.device("cuda"))
+        outs = list(dev_out)
+        for _ in range(2):
+            gather.gather(outs)
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k = 5
+        s.record()
+        for _ in range(k):
+            gather.gather(outs)
+        e.record()
+        torch.cuda.synchronize()
+        gms = max_over_ranks(world, s.elapsed_time(e) / k)
+        collective = {"op": "LogitGather (one all_gather_into_tensor of padded fp64 logit shards, NCCL)",
+                      "ms_per_epoch": round(gms, 4), "bytes_per_rank": int(gather.send.numel() * 8),
+                      "in_value": False}
+        del gather
+
+    dropin = None
+    if not args.no_dropin:
+        k = max(1, min(3, args.steps))
+        d_ms, d_h2d, d_d2h, d_outs = time_dropin(batches, model, k, world)
+        d_ms = max_over_ranks(world, d_ms) * (1 if sharded else 1.0 / world)
+        dropin = {"value": round(d_ms, 3), "unit": "ms/epoch", "h2d_bytes_per_step": d_h2d,
+                  "d2h_bytes_per_step": d_d2h, "steps": k,
+                  "parity_vs_device_path": "bit-exact" if bool(np.array_equal(np.concatenate(d_outs),
+                                                                                 dev_logits_h.numpy()))
+                  else "MISMATCH",
+                  "path": "per batch: pack_batch QGTB bytes (host) -> unpack_batch (one H2D) -> "
+                          "model_forward -> numpy fp64 logits (eager, host-synchronous; wall clock)"}
+        del d_outs
 
     # roofline of the dominant kernel (bit-GEMM) -- algorithmic int8-MAC work per launch
     gemm_ms, gemm_ops, gemm_launches, stamped_step_ms = kernel_roofline(model, batches)
@@ -397,41 +587,22 @@ def ours(args, world, rank):
     traffic = None
     if os.path.exists(PROFILE_SUMMARY):
         try:
-            traffic = json.load(open(PROFILE_SUMMARY)).get("bitgemm_dram_bytes_per_launch")
+            traffic = json.load(open(PROFILE_SUMMARY)).get(f"{cfg.name}:bitgemm_dram_bytes_per_launch")
         except Exception:
             traffic = None
     eff_tops = 2.0 * sum(
         b.total_nodes * b.total_nodes * (ly.out_dim if ly.order == "update-then-aggregate" else ly.in_dim)
         for b in batches for ly in model.layers) / (ms_epoch * 1e-3) / 1e12
 
-    sweep = {}
-    if not args.no_sweep and not sharded:
-        for bits in range(1, 9):
-            if bits == args.bits:
-                sweep[str(bits)] = round(ms_epoch, 5)
-                continue
-            _, bb, _, mm = build_workload(args.config, bits, seed=rank)
-            rr = EpochRunner(mm, bb, rescan=False).capture()
-            k = max(20, args.steps // 4)
-            t, _ = time_device_epochs(rr, k, 5, world)
-            sweep[str(bits)] = round(max_over_ranks(world, t) / (k * world), 5)
-            del rr, bb, mm
-
-    # configs[4] (C5): the standalone 1-bit x s-bit bit-GEMM at M=N=K=16k -- where the
-    # kernel is tensor-pipe bound rather than launch/latency bound like the C2 epoch
-    c5 = None
-    if not args.no_c5:
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        from c5_sweep import run_point
-        c5 = run_point(args.c5_n, 0.1, args.bits, reps=10, int8_peak=peak)
-        c5.update({"bound": "tensor", "peak": peak, "unit": "TOPS",
-                   "kernel": "tc_pair_kernel (2-SM cluster, tcgen05.mma.cta_group::2.kind::i8 M=256, TMA)",
-                   "config": "C5: A Bernoulli(0.1) 1-bit x X uniform codes, reduce_bitplanes(bmm_1bit_by_nbit) "
-                             "in one launch, CUDA-graph replays timed with CUDA events"})
-
+    extras = {}
     cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        del runner
+        torch.cuda.empty_cache()
+        extras["c2_sweep_ms_per_epoch_by_bits"] = c2_sweep(max(20, args.steps))
+        extras["gemm_roofline_c5"] = c5_point(args.c5_n, 4, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(batches, feats, model, batches[0].x_params, runner.run(), args.cpu_sample_s)
+        cpu = cpu_baseline_one_core(cfg, model, logits_b0)
 
     if rank != 0:
         return
@@ -440,15 +611,15 @@ def ours(args, world, rank):
         "value": round(ms_epoch, 5), "unit": "ms/epoch", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_epoch, 5), "higher_is_better": False,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-        "dtype": f"u{args.bits} codes / s32 acc / fp64 epilogue",
+        "dtype": f"u{cfg.bits} codes / s32 acc / fp64 epilogue",
         "data": "synthetic planted-partition graph, U[0,1) features, random-init weights",
-        "config": {"workload": cfg.name, "model": f"batched-{cfg.model} {cfg.layers} layers hidden {cfg.hidden}", "bits": args.bits,
-                   "nodes": cfg.num_nodes, "edges_undirected": cfg.num_edges, "parts": cfg.num_parts,
-                   "batches": len(batches), "in_dim": cfg.in_dim, "classes": cfg.classes,
-                   "l2": "flushed between steps (256 MB write)",
-                   "parallelism": (f"batch-sharded x{world} (LPT, 1 NCCL all_gather of logits per epoch)"
+        "config": {"workload": cfg.name, "model": f"batched-{cfg.model} {cfg.layers} layers hidden {cfg.hidden}",
+                   "bits": cfg.bits, "nodes": cfg.num_nodes, "edges_undirected": cfg.num_edges,
+                   "parts": cfg.num_parts, "batches": len(sizes), "batches_this_rank": len(batches),
+                   "in_dim": cfg.in_dim, "classes": cfg.classes,
+                   "l2": "flushed between steps (256 MB write); inputs also > L2",
+                   "parallelism": (f"batch-sharded x{world} (LPT; per-rank H2D/D2H, no data-path collective)"
                                    if sharded else f"replicas x{world}")},
-        "sweep_ms_per_epoch_by_bits": sweep,
         "effective_tops": round(eff_tops, 3),
         "roofline": {"bound": "tensor", "kernel": "tc_tiled_kernel (tcgen05.mma kind::i8, cp.async.bulk ring)",
                      "achieved": round(achieved, 3), "peak": peak, "unit": "TOPS",
@@ -462,29 +633,33 @@ def ours(args, world, rank):
                      "launches_per_epoch": gemm_launches, "kernel_ms_per_epoch": round(gemm_ms, 5),
                      "stamped_step_ms": round(stamped_step_ms, 5),
                      "kernel_share_of_step": round(gemm_ms / stamped_step_ms, 3)},
-        "gemm_roofline_c5": c5,
         "cpu_baseline": cpu,
-        "e2e": {"value": round(e2e_ms, 5), "unit": "ms/epoch", "h2d_bytes_per_step": host.h2d_bytes,
-                "d2h_bytes_per_step": host.d2h_bytes, "wall_ms_per_step": round(e2e_wall / args.steps, 5),
+        "e2e": {"value": round(e2e_ms, 5), "unit": "ms/epoch", "h2d_bytes_per_step": e2e_h2d,
+                "d2h_bytes_per_step": e2e_d2h, "wall_ms_per_step": round(e2e_wall / args.steps, 5),
                 "parity_vs_device_path": "bit-exact" if e2e_parity else "MISMATCH",
-                "path": ("ONE CUDA graph per step: pinned QGT3 images (schedule + non-zero 128x128 adjacency "
-                         "blocks + feature planes) -> H2D -> block expansion + epoch -> fp64 logits -> D2H"
-                         + (f"; {host.chunks} batch chunks pipelined (H2D / compute / D2H overlapped on "
-                            "two copy engines)" if host.chunks > 1 else "; one H2D and one D2H"))},
+                "path": ("public runtime.HostEpochRunner, ONE CUDA graph per step: pinned QGT3 images (schedule + "
+                         "non-zero 128x128 adjacency bit blocks + feature planes) -> H2D -> block expansion + "
+                         "epoch -> fp64 logits -> D2H into pinned host memory (batch chunks pipelined on two "
+                         "copy engines)" + (", per rank over its own PCIe link" if sharded else ""))},
+        "e2e_dropin": dropin,
+        "collective": collective,
         "gpu_launches": launches,
         "clocks": clocks,
+        **extras,
     }
     print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
-    world, rank, _ = dist_setup()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+    world, rank, _ = dist_setup(args.impl)
     if args.impl == "reference":
         reference_arm(args, world, rank)
     else:
         ours(args, world, rank)
-    if world > 1:
+    if world > 1 and args.impl == "ours":
         import torch.distributed as dist
         dist.destroy_process_group()
 

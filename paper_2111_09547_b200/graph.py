@@ -55,6 +55,17 @@ class Graph:
     def num_edges(self) -> int:
         return len(self.edges)
 
+    def edge_set(self) -> set[tuple[int, int]]:
+        """Edges as a Python set of (src, dst) pairs (graph.py:70-71)."""
+        return set(map(tuple, self.edges.tolist()))
+
+    def neighbors(self) -> list[list[int]]:
+        """Undirected adjacency lists, sorted, no self references (graph.py:73-81)."""
+        e = self.edges[self.edges[:, 0] != self.edges[:, 1]] if len(self.edges) else self.edges.reshape(0, 2)
+        both = np.unique(np.concatenate([e, e[:, ::-1]]), axis=0)
+        starts = np.searchsorted(both[:, 0], np.arange(self.num_nodes + 1))
+        return [both[starts[v]:starts[v + 1], 1].tolist() for v in range(self.num_nodes)]
+
     def device_edges(self) -> torch.Tensor:
         if self._dev_edges is None:
             self._dev_edges = N.to_device(self.edges)
