@@ -314,44 +314,18 @@ def kernel_roofline(model, batches, reps=20):
 # --------------------------------------------------- real reference (CPU)
 def _ref_module():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import make_ref
-    if not make_ref.available():
-        return None
-    return make_ref.import_reference()
+    import ref_inputs
+    return ref_inputs.ref_module()
 
 
 def _ref_model(R, cfg, seed):
-    """Reference ModelConfig: the reference preset (same seed => same weights) calibrated
-    by the reference's calibrate_model on the reference-built global batch 0."""
-    from paper_2111_09547_b200 import synth_host as H
-    builder = R.gcn_model if cfg.model == "gcn" else R.gin_model
-    model = builder(cfg.in_dim, cfg.classes, hidden_dim=cfg.hidden, num_layers=cfg.layers,
-                    feature_bits=cfg.bits, weight_bits=cfg.wbits, seed=seed)
-    edges, bnd, x = H.host_batch(cfg, seed, 0)
-    b0 = _ref_build(R, cfg, edges, bnd, x)
-    R.calibrate_model(model, b0, np.asarray(x, dtype=np.float64))
-    return model
-
-
-def _ref_build(R, cfg, edges, boundaries, x):
-    """Reference build_batch over the parts in ``edges`` (their own graph: cross-part
-    edges are dropped by build_batch anyway, graph.py:337)."""
-    from paper_2111_09547_b200 import synth_host as H
-    total = int(boundaries[-1])
-    el = H.batch_edge_list(edges, boundaries, self_loops=False)
-    g = R.Graph(total, el, features=np.asarray(x, dtype=np.float64))
-    part_of = np.repeat(np.arange(len(boundaries) - 1), np.diff(boundaries))
-    assign = R.PartitionAssignment(len(boundaries) - 1, part_of)
-    return R.build_batch(g, assign, list(range(len(boundaries) - 1)), R.QuantParams(0.0, 1.0, cfg.bits))
+    import ref_inputs
+    return ref_inputs.ref_model(R, cfg, seed)
 
 
 def ref_part_batch(R, cfg, seed, b, p):
-    """Part p of batch b as a one-part reference SubgraphBatch + its host features."""
-    from paper_2111_09547_b200 import synth_host as H
-    edges, bnd, x = H.host_batch(cfg, seed, b)
-    lo, hi = int(bnd[p]), int(bnd[p + 1])
-    xb = x[lo:hi]
-    return _ref_build(R, cfg, [edges[p]], np.array([0, hi - lo]), xb), lo, hi
+    import ref_inputs
+    return ref_inputs.ref_part_batch(R, cfg, seed, b, p)
 
 
 def sample_parts(cfg, n, seed=0):
