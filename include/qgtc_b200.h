@@ -174,13 +174,8 @@ typedef struct {
   int64_t q_codes_ld;
   int32_t q_codes_colmajor;
   int32_t q_skip_planes;       /* 1: write only the code cache (planes built lazily) */
-  /* Tiled fast path, packed output only: affine screen of the requantized code.
-   * y = P_c*acc + G_c*row_term + R_c approximates the reference quotient
-   * (x - q_amin)/q_scale within screen_tol (host-derived bound on both chains'
-   * rounding); codes whose y lies within screen_tol of a code boundary are
-   * recomputed with the exact reference expression.  0 disables the screen. */
-  double screen_tol;
-  double screen_r0;            /* 2^12 + RN(-q_amin * q_inv_scale): ReLU floor in r-space */
+  double reserved_d0;          /* reserved, 0 (round-1 affine requant screen, removed) */
+  double reserved_d1;
 } qg_epilogue;
 
 /*
@@ -257,8 +252,7 @@ typedef struct {
   int64_t cta_begin;           /* first CTA of this segment                          */
   int32_t k_tiles;             /* dense left: K tiles                                */
   int32_t pad_;
-  int64_t rb_base;             /* dataflow epoch: global index of this segment's first
-                                  128-row block (the same in every stage)              */
+  int64_t reserved0;           /* reserved, 0                                         */
   /* pair mode (qg_tiled_args.pair): 2-D TMA descriptors (CUtensorMap, 128 B, 64-B
    * aligned; qg_encode_linear_map) of the A source and the B source viewed as rows of
    * 128 bytes -- the pair's copies signal the leader CTA's mbarrier (cta_group::2) */
@@ -292,20 +286,16 @@ typedef struct {
                                   segs[].cta_begin then counts PAIRS, total_ctas = 2 x pairs,
                                   bn >= 64 (each CTA stages bn/2 columns of B)             */
   const struct qg_chain* chain; /* optional: fuse a dense stage-2 GEMM behind this stage   */
-  /* dataflow epoch (qg_tiled_epoch): per-128-row-block completion counters, indexed by
-   * segs[].rb_base + row block, zeroed before the epoch.  A tile of this stage waits
-   * until the previous stage's counters of the row blocks it reads reach expect_prev
-   * (that stage's n_tiles), and adds 1 to its own row block's counter when done. */
-  int32_t* ready_prev;         /* NULL for the first stage of a launch                   */
-  int32_t* ready_cur;
-  int32_t expect_prev;
+  void* reserved1;             /* reserved, NULL (round-1 dataflow epoch, removed)       */
+  void* reserved2;
+  int32_t reserved3;
   int32_t pad3_;
 } qg_tiled_args;
 
 /* Chained stage 2 of a tiled GEMM (qg_tiled_args.chain): an aggregation and the update
  * that consumes its rows (engine.py:282-334: aggregate -> update inside a GCN layer, or
  * a GIN layer's aggregation -> the next layer's update) in one launch.  Stage 1
- * (n_tiles == 1, or 2 with split; EPILOGUE mode, packed output) requantizes its tile into u8
+ * (n_tiles == 1; EPILOGUE mode, packed output) requantizes its tile into u8
  * codes that stay in shared memory as the LEFT operand of stage 2, whose right operand
  * is `w` (right-tiled, K = stage-1 n); stage 2's epilogue uses the code row sums of
  * that tile.  segs[].q_codes / q_row_sums / out_real / status are then stage 2's
@@ -315,9 +305,7 @@ typedef struct qg_chain {
   int64_t w_npad;              /* padded N of w: power of two 32..256                    */
   int64_t n;                   /* stage-2 logical output columns (<= w_npad)             */
   int32_t out_layout;          /* 0 fp64 row-major, 2 right-tiled codes                  */
-  int32_t split;               /* 1: a cluster of 2 CTAs per 128-row block (n_tiles == 2),
-                                  each computing half of both stages' columns; the stage-1
-                                  codes are exchanged through distributed shared memory  */
+  int32_t reserved;            /* reserved, 0 (round-1 DSMEM split chain, removed)        */
   int64_t out_npad;            /* right-tiled output: padded N                           */
   const qg_epilogue* epi;      /* stage-2 epilogue                                       */
 } qg_chain;
@@ -327,17 +315,6 @@ typedef struct qg_chain {
  * qg_bitgemm's EPILOGUE / I32 modes; replaces the per-batch loop of
  * engine.py:320-332 for a whole epoch layer stage. */
 int qg_tiled_gemm(const qg_tiled_args* args, void* stream);
-
-/* Every GEMM stage of an epoch (<= 8, e.g. 2 per layer over all batches) in ONE
- * persistent cooperative launch: CTAs sweep each stage's tiles and meet at a grid
- * barrier before the next stage.  Same arithmetic as nstages qg_tiled_gemm calls in
- * order; grid_bar is 9 caller-owned device words (barrier + per-stage tile counters,
- * zeroed by the call, stream-ordered). */
-int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint32_t* grid_bar, void* stream);
-/* With stages[].ready_cur set, the epoch runs as a DATAFLOW kernel instead: no grid
- * barriers and no cooperative launch; CTAs claim tiles of all stages from one queue
- * (stage-major) and each tile waits only for the row blocks it reads.  Subgraph
- * batches are block-diagonal, so the stages of different parts overlap. */
 
 /* Gather the non-zero 128x128 blocks (blk_rb/blk_kt) of a column-wise 1-bit matrix
  * into `packed` (2 KB each; skipped when a_words == NULL and `packed` is already

@@ -33,7 +33,7 @@ EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes"
            "qg_tile_scan", "qg_plane_zero_tiles", "qg_epilogue_apply", "qg_bitgemm", "qg_reduce_planes",
            "qg_popcount32", "qg_edges_to_bits", "qg_test_div", "qg_planes_to_codes",
            "qg_test_requant", "qg_tiled_gemm", "qg_block_prepare", "qg_codes_to_tiles",
-           "qg_tiles_to_codes", "qg_entry_tiles", "qg_tiled_epoch",
+           "qg_tiles_to_codes", "qg_entry_tiles",
            "qg_block_prepare_grouped", "qg_bmm_1xs", "qg_gemm_sxt", "qg_batch_h2d", "qg_bmm_counters",
            "qg_gemm_counters", "qg_encode_linear_map", "qg_slab_reset")
 
@@ -55,7 +55,7 @@ class Epilogue(ctypes.Structure):
         ("q_prows", _i64), ("q_pcols", _i64),
         ("out_real", _vp), ("q_planes", _vp), ("q_row_sums", _vp), ("status", _vp),
         ("q_codes", _vp), ("q_codes_ld", _i64), ("q_codes_colmajor", ctypes.c_int32),
-        ("q_skip_planes", ctypes.c_int32), ("screen_tol", _f64), ("screen_r0", _f64),
+        ("q_skip_planes", ctypes.c_int32), ("reserved_d0", _f64), ("reserved_d1", _f64),
     ]
 
 

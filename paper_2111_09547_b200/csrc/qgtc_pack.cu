@@ -70,44 +70,112 @@ __global__ void __launch_bounds__(256) quantize_pack_col_kernel(
   }
 }
 
-// Row-wise: one warp per (32-row group v, 32 consecutive columns).  Lane l owns
-// column c0+l and walks the 32 rows (each step is a coalesced row segment).
-template <typename SrcT, int BITS>
-__global__ void __launch_bounds__(256) quantize_pack_row_kernel(
-    const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale,
-    int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
-    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wpc = prows >> 5;             // words per column
-  const int64_t cgroups = (pcols + 31) >> 5;
-  const int64_t item = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (item >= wpc * cgroups) return;
-  const int64_t v = item / cgroups;
-  const int64_t c = (item % cgroups) * 32 + lane;
-  const uint32_t maxv = (1u << BITS) - 1u;
-  uint32_t word[BITS];
-#pragma unroll
-  for (int p = 0; p < BITS; ++p) word[p] = 0;
-  for (int i = 0; i < 32; ++i) {
-    const int64_t r = v * 32 + i;
-    uint32_t code = 0;
-    if (r < rows && c < cols) {
-      code = load_code<SrcT>(src, 0, r, c, ld, cols, amin, scale, maxv, status, status_base);
-      if (codes) codes[r * cols + c] = (uint8_t)code;
+// Row-wise, vectorised (the feature path, bitpack.py:181-191 + quantize.py:93-105).
+// CTA = 8 warps over a tile of 8 row groups (256 rows) x 128 columns.  Lane l owns
+// columns 4l..4l+3 of the tile: one 16-byte (fp32) / 2x16-byte (fp64) / 4-byte (u8)
+// load per row, so every warp row is a full 512 B (fp32) coalesced segment.  The
+// quantize is the exact division-free form (quantize_code_fast: RN(1/scale) product,
+// IEEE fallback only within 2^-40 of a code boundary).  Bits accumulate in registers
+// (word[p][j] bit i = plane p of row 32v+i, column 4l+j); the row sums come from one
+// redux.sync per row, kept by lane i and written once per (row, column tile).  The
+// plane words are staged in shared memory so the stores run along the row-group index
+// (8 consecutive words = 32 B per (plane, column)) instead of striding by the column
+// pitch.
+template <typename SrcT>
+__device__ __forceinline__ void load4(const SrcT* __restrict__ src, int64_t r, int64_t c, int64_t ld, int64_t cols,
+                                      bool vec, double (&x)[4]) {
+  const SrcT* p = src + r * ld + c;
+  if (vec && c + 3 < cols) {
+    if constexpr (sizeof(SrcT) == 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else if constexpr (sizeof(SrcT) == 8) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+    } else {
+      const uchar4 v = *reinterpret_cast<const uchar4*>(p);
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
     }
+  } else {
 #pragma unroll
-    for (int p = 0; p < BITS; ++p) word[p] |= ((code >> p) & 1u) << i;
-    if (row_sums && r < rows) {
-      int64_t s = code;
+    for (int j = 0; j < 4; ++j) x[j] = c + j < cols ? (double)p[j] : 0.0;
+  }
+}
+
+constexpr int kRowTileCols = 128, kRowTileGroups = 8, kRowStride = 132;
+
+template <typename SrcT, int BITS>
+__global__ void __launch_bounds__(256) quantize_pack_row_vec_kernel(
+    const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale, double inv,
+    int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
+    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base, int vec, int single_tile) {
+  __shared__ __align__(16) uint32_t sw[BITS][kRowTileGroups][kRowStride];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wpc = prows >> 5;                          // words per column (row groups)
+  const int64_t v0 = (int64_t)blockIdx.x * kRowTileGroups, v = v0 + warp;
+  const int64_t c0 = (int64_t)blockIdx.y * kRowTileCols, c = c0 + 4 * lane;
+  const uint32_t maxv = (1u << BITS) - 1u;
+  uint32_t word[BITS][4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(QG_FULL, s, o);
-      if (lane == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(row_sums + r), (unsigned long long)s);
+  for (int p = 0; p < BITS; ++p)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) word[p][j] = 0u;
+  uint32_t my_sum = 0;                                     // lane i: row 32v + i
+  if (v < wpc) {
+    for (int i = 0; i < 32; ++i) {
+      const int64_t r = v * 32 + i;
+      if (r >= rows) break;                                // warp-uniform
+      uint32_t q[4] = {0u, 0u, 0u, 0u};
+      if (c < cols) {
+        double x[4];
+        load4<SrcT>(src, r, c, ld, cols, vec != 0, x);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (c + j >= cols) continue;
+          if constexpr (sizeof(SrcT) == 1) {
+            uint32_t t = (uint32_t)x[j];
+            if (t > maxv) { status_min(status, status_base + r * cols + c + j); t &= maxv; }
+            q[j] = t;
+          } else {
+            if (!isfinite(x[j])) status_min(status, status_base + r * cols + c + j);
+            q[j] = quantize_code_fast(x[j], amin, scale, inv, maxv);
+          }
+        }
+        if (codes) {
+          if (vec && c + 3 < cols && (cols & 3) == 0)
+            *reinterpret_cast<uchar4*>(codes + r * cols + c) = make_uchar4(q[0], q[1], q[2], q[3]);
+          else
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (c + j < cols) codes[r * cols + c + j] = (uint8_t)q[j];
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < BITS; ++p)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) word[p][j] |= ((q[j] >> p) & 1u) << i;
+      const uint32_t s = __reduce_add_sync(QG_FULL, (q[0] + q[1]) + (q[2] + q[3]));
+      if (lane == i) my_sum = s;
+    }
+    if (row_sums) {
+      const int64_t r = v * 32 + lane;
+      if (r < rows && my_sum) {
+        if (single_tile) row_sums[r] += (int64_t)my_sum;   // the only writer of row r
+        else atomicAdd(reinterpret_cast<unsigned long long*>(row_sums + r), (unsigned long long)my_sum);
+      }
     }
   }
-  if (c < pcols) {
-    const int64_t wpp = pcols * wpc;
 #pragma unroll
-    for (int p = 0; p < BITS; ++p) planes[p * wpp + c * wpc + v] = word[p];
+  for (int p = 0; p < BITS; ++p)
+    *reinterpret_cast<uint4*>(&sw[p][warp][4 * lane]) = make_uint4(word[p][0], word[p][1], word[p][2], word[p][3]);
+  __syncthreads();
+  // plane p, column c0 + cc, row group v0 + w: word p * wpp + (c0 + cc) * wpc + v0 + w
+  const int64_t wpp = pcols * wpc;
+  for (int idx = threadIdx.x; idx < BITS * kRowTileCols * kRowTileGroups; idx += blockDim.x) {
+    const int w = idx & 7, cc = (idx >> 3) & 127, p = idx >> 10;
+    const int64_t col = c0 + cc, vg = v0 + w;
+    if (col < pcols && vg < wpc) planes[p * wpp + col * wpc + vg] = sw[p][w][cc];
   }
 }
 
@@ -143,9 +211,16 @@ int launch_quantize_pack(const SrcT* src, int64_t rows, int64_t cols, int64_t ld
     if (orientation == QG_COLUMN_WISE)
       quantize_pack_col_kernel<SrcT, BITS><<<(unsigned)blocks, 256, 0, st>>>(
           src, rows, cols, ld, amin, scale, prows, pcols, planes, codes, row_sums, status, status_base);
-    else
-      quantize_pack_row_kernel<SrcT, BITS><<<(unsigned)blocks, 256, 0, st>>>(
-          src, rows, cols, ld, amin, scale, prows, pcols, planes, codes, row_sums, status, status_base);
+    else {
+      // vectorised loads need an aligned base and a row pitch of whole vectors
+      const size_t vb = sizeof(SrcT) == 1 ? 4 : 16;
+      const int vec = (reinterpret_cast<uintptr_t>(src) % vb == 0) && ((ld * (int64_t)sizeof(SrcT)) % (int64_t)vb == 0);
+      const dim3 grid((unsigned)(((prows >> 5) + kRowTileGroups - 1) / kRowTileGroups),
+                      (unsigned)((pcols + kRowTileCols - 1) / kRowTileCols));
+      quantize_pack_row_vec_kernel<SrcT, BITS><<<grid, 256, 0, st>>>(
+          src, rows, cols, ld, amin, scale, 1.0 / scale, prows, pcols, planes, codes, row_sums, status, status_base,
+          vec, (int)(grid.y == 1));
+    }
   }
   if (col_sums && cols > 0 && rows > 0)
     col_sums_kernel<SrcT><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(src, rows, cols, ld, amin, scale,

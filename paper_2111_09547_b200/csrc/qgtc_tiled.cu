@@ -17,10 +17,7 @@
 //
 // Variants: CHAIN (qg_chain) runs a second, dense GEMM behind the epilogue over the
 // requantized codes left in the ring's shared memory (aggregation -> update in one
-// launch; chain == 2 splits it over a 2-CTA cluster exchanging codes through DSMEM);
-// tc_pair_kernel runs cta_group::2 MMAs (M = 256) for large int32 GEMMs; the epoch
-// kernel runs all stages of an epoch in one persistent grid (grid barriers, or the
-// dataflow mode's per-row-block completion counters).
+// launch); tc_pair_kernel runs cta_group::2 MMAs (M = 256) for large int32 GEMMs.
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -43,23 +40,15 @@ struct TiledParams {
   qg_epilogue epi;          // shared scalars + per-column vectors (per-row pointers come from segs)
   int64_t* phase_ns;        // optional per-tile %globaltimer stamps (tools/phase_tiled.py)
   int64_t total_ctas;       // work items (segment, row block, N tile) of this stage
-  int32_t a_bits;           // 1: adjacency blocks are shipped packed (2 KB) and expanded in smem
   int32_t pair;             // 1: CTA pairs (cluster of 2) run cta_group::2 MMAs, M = 256
   int32_t pair_swizzle;     // pair kernels: row-block pairs per N-major group (1 = plain order)
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
-  // codes, which never leave shared memory.  chain 1: one CTA per row block (n_tiles 1);
-  // chain 2: a cluster of 2 CTAs per row block, each computing half of both stages' N
-  // (n_tiles 2) and writing its stage-1 codes into both CTAs' shared memory (DSMEM).
-  // bn2 = this CTA's stage-2 N tile (half of w2_npad when chain == 2)
+  // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
   int32_t chain, bn2, k2, out_layout2;
   int64_t n2, out_npad2, w2_npad;
   const uint8_t* w2;
   qg_epilogue epi2;
-  // dataflow epoch (qg_tiled_args.ready_*): per-row-block completion counters
-  int32_t* ready_prev;
-  int32_t* ready_cur;
-  int32_t expect_prev;
 };
 
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
@@ -78,57 +67,11 @@ static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile
 
 constexpr int kTThreads = 256;
 
-// distributed shared memory (cluster peers): this CTA's smem address -> the peer's copy
-__device__ __forceinline__ uint32_t peer_addr(uint32_t local_addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_peer_v2(uint32_t cluster_addr, uint32_t lo, uint32_t hi) {
-  asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(cluster_addr), "r"(lo), "r"(hi) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_peer_u64(uint32_t cluster_addr) {
-  unsigned long long v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(cluster_addr) : "memory");
-  return v;
-}
-// dataflow epoch: spin until a row block's completion counter reaches `expect`
-// (acquire), then make the other CTAs' generic-proxy stores visible to this thread's
-// bulk copies (async proxy)
-__device__ __forceinline__ void wait_ready(const int32_t* ctr, int32_t expect) {
-  int32_t v;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    if (v >= expect) break;
-    __nanosleep(64);
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_barrier() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
 // exact requant of one element with the non-finite report (rare path, kept out of line)
 static __device__ __noinline__ uint32_t requant_exact(double x, double amin, double scale, double inv, uint32_t maxv,
                                                       int64_t* status, int64_t flat) {
   if (!isfinite(x) && status) status_min(status, flat);
   return quantize_code_fast(x, amin, scale, inv, maxv);
-}
-
-// Exact reference requant of one element, column constants from global memory (the
-// screened epilogue's rare fallback; identical expression to epi_slices, absent
-// terms +0.0).
-static __device__ __noinline__ uint32_t exact_code_global(const qg_epilogue& E, uint32_t accbits, double rterm,
-                                                          int64_t c, uint32_t maxv, int64_t* status, int64_t flat) {
-  double x = __dadd_rn(__dmul_rn(E.k_acc, (double)(int32_t)accbits), rterm);
-  const double sC = E.use_col ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
-  const double kc = E.use_const ? E.k_const : 0.0;
-  const double sB = E.bias ? E.bias[c] : 0.0;
-  x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC), kc), sB);
-  if (E.bn_mean)
-    x = __dadd_rn(__dmul_rn(__ddiv_rn(__dsub_rn(x, E.bn_mean[c]), E.bn_denom[c]), E.bn_gamma[c]), E.bn_beta[c]);
-  if (E.act == QG_ACT_RELU) x = (x < 0.0) ? 0.0 : x;
-  return requant_exact(x, E.q_amin, E.q_scale, E.q_inv_scale, maxv, status, flat);
 }
 
 // Per-thread epilogue context: this lane owns one accumulator row (TMEM lane) and
@@ -137,7 +80,6 @@ struct EpiLane {
   uint32_t tmem_row;
   bool has_acc, rvalid;
   int first, step, nslices, nvalid;   // this lane's slices: first, first + step, ...
-  int peer;                            // chained stage 1 of a CTA pair: the peer's cluster rank, else -1
   int64_t myrow, n0;
   __device__ __forceinline__ void load8(int cl8, uint32_t (&v)[8]) const {
     if (has_acc) {
@@ -246,12 +188,10 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     if (ST == 1) {
       // stage 2's LEFT operand in shared memory (UMMA K-major core matrices, one 16 KB
       // slot per 128 K columns); rows past m hold zeros (their stage-2 rows are not stored).
-      // A CTA pair writes its half of the columns into both CTAs' copies.
       const int c = (int)L.n0 + cl8;
       uint8_t* dst = ((c >> 7) ? mid1 : mid0) + (lrow >> 3) * 1024 + ((c & 127) >> 4) * 128 + (lrow & 7) * 16 +
                      (c & 15);
       *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
-      if (L.peer >= 0) st_peer_v2(peer_addr(smem_u32(dst), (uint32_t)L.peer), lo, hi);
       continue;
     }
     if (L.rvalid) {
@@ -276,89 +216,13 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
   return rsum;
 }
 
-// Screened fused requant (packed hidden outputs, act none/relu): per element
-//   r = fma(P_c, acc, fma(G_c, row_term, R_c))  [+ max with the ReLU floor]
-// is 2^12 + y, y ~ (x - q_amin)/q_scale within screen_tol of the reference quotient,
-// so floor(y) is the reference code unless y is within screen_tol of a code boundary
-// 1..maxv (boundaries at 0 and maxv+1 clip to the same code on both sides).  The
-// high word of r in [2^12, 2^13) holds 0x40B00000 + (floor << 8) + top fraction bits.
-// Flagged slices (rare) and ragged edges take exact_code_global.
-template <bool RELU>
-__device__ __forceinline__ uint32_t epi_slices_screen(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
-                                                      const double* __restrict__ sCol, double rterm) {
-  const qg_epilogue& E = P.epi;
-  const int bn = P.bn;
-  const double* sP = sCol;
-  const double* sG = sCol + bn;
-  const double* sR = sCol + 2 * bn;
-  const uint32_t maxv = (1u << E.q_bits) - 1u;
-  const double r0 = E.screen_r0;
-  const uint64_t tb = (uint64_t)(E.screen_tol * 0x1p40) + 4u;   // tolerance in 2^-40 units
-  const int out_layout = P.out_layout;
-  uint8_t* const q_codes = G.q_codes;
-  int64_t* const status = G.status;
-  const int64_t r128 = G.r128, out_npad = P.out_npad, pn = P.n;
-  uint32_t rsum = 0;
-  for (int sl = L.first; sl < L.nslices; sl += L.step) {
-    const int cl8 = sl * 8;
-    uint32_t v[8];
-    L.load8(cl8, v);
-    bool slow = false;
-    uint32_t q[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int cl = cl8 + jj;
-      // acc >= 0 (non-negative operands): 2^52 + acc is exact, one DADD instead of I2F
-      const double a = __dsub_rn(__hiloint2double(0x43300000, (int)v[jj]), 0x1p52);
-      double r = __fma_rn(sP[cl], a, __fma_rn(sG[cl], rterm, sR[cl]));
-      if (RELU) r = fmax(r, r0);
-      const uint64_t bits = (uint64_t)__double_as_longlong(r);
-      // code: floor(y) of r = 2^12 + y in [2^12, 2^13), clamped (sign-preserving shift:
-      // negative r -> 0, r >= 2^13 -> maxv)
-      const int kc = (int)((int64_t)bits >> 40) - 0x40B000;
-      q[jj] = (uint32_t)min(max(kc, 0), (int)maxv);
-      // ambiguous: the 40-bit fraction within tb of a code boundary B >= 1
-      const uint64_t x = bits + tb;
-      slow |= ((x & 0xFFFFFFFFFFull) < 2 * tb) & (x >= 0x40B0010000000000ull) & (cl < L.nvalid);
-    }
-    if (slow && L.rvalid) {
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-        if (cl8 + jj < L.nvalid)
-          q[jj] = exact_code_global(E, v[jj], rterm, L.n0 + cl8 + jj, maxv, status, L.myrow * pn + L.n0 + cl8 + jj);
-    }
-    const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
-    const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
-    rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
-    if (L.rvalid) {
-      const int64_t cb = L.n0 + cl8;
-      if (out_layout == 1) {
-        *reinterpret_cast<uint2*>(q_codes + left_tile_off(L.myrow, cb, r128)) = make_uint2(lo, hi);
-      } else {
-        uint8_t* base = q_codes + right_tile_off(L.myrow, cb, out_npad);
-        if (cl8 + 8 <= L.nvalid) {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) base[jj * 16] = (uint8_t)q[jj];
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)q[jj];
-        }
-      }
-    }
-  }
-  return rsum;
-}
-
-// Per-CTA state that persists across the tiles one CTA processes (the persistent
-// epoch kernel runs many tiles of many stages through the same ring / TMEM).
+// Per-CTA state of the tile pipeline (ring position, accumulator phase).
 struct TileRing {
   uint8_t* stage0;            // S ring slots of (16 KB + bn_max * 128 B)
   double* sCol;               // per-column epilogue constants
   uint64_t* full;
   uint64_t* empty;
   uint64_t* done;
-  uint64_t* aready;           // a_bits: expanded A operand of a ring slot is ready
   unsigned long long* sRowSum;
   double* sRowTerm;
   uint32_t tmem;
@@ -375,8 +239,7 @@ struct TileRing {
 template <int ST>
 __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tseg& G, TileRing& R, int64_t tile,
                                               int64_t rb, int64_t n0, int nk, uint32_t tmem, const double* sCol,
-                                              bool fused, bool screen, uint8_t* mid0 = nullptr,
-                                              uint8_t* mid1 = nullptr, int peer = -1) {
+                                              bool fused, uint8_t* mid0 = nullptr, uint8_t* mid1 = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bn = ST == 2 ? P.bn2 : P.bn;
   const int64_t pn = ST == 2 ? P.n2 : P.n;
@@ -401,7 +264,6 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   L.rvalid = myrow < G.m;
   L.myrow = myrow;
   L.n0 = n0;
-  L.peer = peer;
   uint32_t rsum = 0;
   if (ST == 0 && !fused) {
     const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
@@ -425,10 +287,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
     // one uniform dispatch per tile: the slice loop below is straight-line per variant
     const double rterm = rvalid ? R.sRowTerm[quad * 32 + lane] : 0.0;
     const bool row_only = !E.use_col && !E.use_const && !E.bias;
-    if (ST == 0 && screen) {
-      rsum = E.act == QG_ACT_RELU ? epi_slices_screen<true>(P, G, L, sCol, rterm)
-                                  : epi_slices_screen<false>(P, G, L, sCol, rterm);
-    } else switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
+    switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
 #define QG_EPI_CASE(i, A, B, Rw) \
   case i: rsum = epi_slices<A, B, Rw, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
       QG_EPI_CASE(0, QG_ACT_NONE, false, false)
@@ -446,8 +305,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
 #undef QG_EPI_CASE
     }
   }
-  // chained stage 2 accumulates into the second half of sRowSum (a CTA pair's peer may
-  // still read the first half, stage 1's partial sums)
+  // chained stage 2 accumulates into the second half of sRowSum
   if (packed && (ST == 1 || G.q_row_sums) && rsum)
     atomicAdd(&R.sRowSum[(ST == 2 ? 128 : 0) + quad * 32 + lane], (unsigned long long)rsum);
 }
@@ -472,11 +330,10 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const int nt = (int)(local % P.n_tiles);
   const int64_t n0 = (int64_t)nt * bn;
 
-  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B][a_bits: 2 KB packed bit block]
+  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B]
   const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u, slot_b = (uint32_t)P.slot_bn * 128u;
-  const bool abits = P.a_blocks && P.a_bits;
   uint8_t* stage0 = R.stage0;
-  const uint32_t stage_bytes = abits ? ((a_bytes + slot_b + 2048u + 1023u) & ~1023u) : a_bytes + slot_b;
+  const uint32_t stage_bytes = a_bytes + slot_b;
   double* sCol = R.sCol;
   uint64_t* full = R.full;
   uint64_t* empty = R.empty;
@@ -490,13 +347,8 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
 
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
-  const bool screen = fused && !CHAIN && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
-                      (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
-  // chained stage 2: per-column constants after stage 1's (screen is off when chained)
+  // chained stage 2: per-column constants after stage 1's
   double* sCol2 = sCol + (E.bn_mean ? 7 : 2) * bn;
-  // chain == 2: this CTA is rank nt of its row block's pair (n_tiles == 2, pairs aligned)
-  const bool cpair = CHAIN && P.chain == 2;
-  const int64_t n0_2 = cpair ? (int64_t)nt * P.bn2 : 0;
   if (tid < 128) R.sRowSum[tid] = 0ull;
   if (CHAIN && tid < 128) R.sRowSum[128 + tid] = 0ull;
   if (tid == 0) tstamp(P, tile, 1);
@@ -514,16 +366,9 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       for (int it = 0; it < pre; ++it) {
         uint8_t* dst = dst0 + (size_t)((it0 + it) % S) * stage_bytes;
         uint64_t* fb = &full[(it0 + it) % S];
-        if (abits) {
-          mbar_expect_tx(fb, 2048u + b_bytes);
-          bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
-        } else if (P.a_blocks) {
-          mbar_expect_tx(fb, a_bytes + b_bytes);
-          bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
-        } else {
-          mbar_expect_tx(fb, a_bytes + b_bytes);
-          bulk_g2s(dst + a_bytes, bbase + (int64_t)it * (P.b_npad << 7), b_bytes, fb);
-        }
+        mbar_expect_tx(fb, a_bytes + b_bytes);
+        if (P.a_blocks) bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
+        else bulk_g2s(dst + a_bytes, bbase + (int64_t)it * (P.b_npad << 7), b_bytes, fb);
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = 0; it < pre; ++it) {
@@ -536,24 +381,6 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       }
       it_begin = pre;
     }
-    // dataflow epoch: a dense left operand is the previous stage's output rows of this
-    // row block; an adjacency stage's K tile kt reads the previous stage's row block kt
-    const bool df_wait = P.ready_prev != nullptr;
-    if (df_wait && !P.a_blocks) wait_ready(P.ready_prev + G.rb_base + rb, P.expect_prev);
-    if (df_wait && P.a_blocks && nk > 0) {
-      // every row block this tile reads (block-diagonal parts: a few neighbours), then ONE
-      // proxy fence ahead of all the bulk copies
-      for (int it = 0; it < nk; ++it) {
-        const int32_t* ctr = P.ready_prev + G.rb_base + G.blk_kt[kbase + it];
-        int32_t v;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-          if (v >= P.expect_prev) break;
-          __nanosleep(64);
-        }
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
     for (int it = it_begin; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
@@ -561,17 +388,10 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       int kt;
       const uint8_t* asrc;
       uint8_t* dst = stage0 + (size_t)s * stage_bytes;
-      if (abits) {
-        // 2 KB packed block -> staging; the expander warps build the 16 KB operand
-        kt = G.blk_kt[kbase + it];
-        mbar_expect_tx(&full[s], 2048u + b_bytes);
-        bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
-      } else {
-        if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
-        else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
-        mbar_expect_tx(&full[s], a_bytes + b_bytes);
-        bulk_g2s(dst, asrc, a_bytes, &full[s]);
-      }
+      if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
+      else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
+      mbar_expect_tx(&full[s], a_bytes + b_bytes);
+      bulk_g2s(dst, asrc, a_bytes, &full[s]);
       bulk_g2s(dst + a_bytes, bbase + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
     }
     if (CHAIN) {
@@ -583,8 +403,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         const int s = (int)(g % (uint32_t)S);
         if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
         mbar_expect_tx(&full[s], wb);
-        bulk_g2s(stage0 + (size_t)s * stage_bytes + a_bytes,
-                 P.w2 + (int64_t)j * (P.w2_npad << 7) + (n0_2 >> 3) * 1024, wb, &full[s]);
+        bulk_g2s(stage0 + (size_t)s * stage_bytes + a_bytes, P.w2 + (int64_t)j * (P.w2_npad << 7), wb, &full[s]);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -593,7 +412,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     for (int it = 0; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
-      mbar_wait(smem_u32(abits ? &R.aready[s] : &full[s]), (g / S) & 1);
+      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
       if (it == 0) tstamp(P, tile, 2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
@@ -608,62 +427,31 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     // RN(k_row * row_sum) (predecessor outputs) and the per-column constants
     const int t = tid - 64;
     if (R.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
-    // dataflow epoch: a dense-left stage's row sums are the previous stage's outputs
-    if (P.ready_prev && !P.a_blocks && E.use_row && t < 128) {
-      int32_t v;
-      do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.ready_prev + G.rb_base + rb) : "memory");
-      } while (v < P.expect_prev);
-    }
     if (t < 128) {
       const int64_t row = rb * 128 + t;
       R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
     }
-    if (screen) {
-      // screened requant: per-column affine coefficients P_c, G_c, R_c (see epi_slices_screen)
-      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
-        const int64_t c = n0 + i;
-        double pc = 0.0, gc = 0.0, rc = 0x1p12;
-        if (c < P.n) {
-          const double inv = E.q_inv_scale;
-          const double sC = E.use_col ? E.k_col * (double)E.col_sums[c] : 0.0;
-          const double base = (sC + (E.use_const ? E.k_const : 0.0)) + (E.bias ? E.bias[c] : 0.0);
-          double g = 1.0, center = base;
-          if (E.bn_mean) {
-            g = E.bn_gamma[c] / E.bn_denom[c];
-            center = (base - E.bn_mean[c]) * g + E.bn_beta[c];
-          }
-          gc = g * inv;
-          pc = E.k_acc * gc;
-          rc = 0x1p12 + (center - E.q_amin) * inv;
-        }
-        sCol[i] = pc;
-        sCol[bn + i] = gc;
-        sCol[2 * bn + i] = rc;
-      }
-    } else {
-      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
-        const int64_t c = n0 + i;
-        const bool ok = c < P.n;
-        // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
-        // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
-        // evaluates the reference's grouping without per-element branches
-        sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
-        sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
-        if (E.bn_mean) {
-          sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
-          sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
-          sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
-          sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
-          sCol[6 * bn + i] = ok ? E.bn_inv_denom[c] : 1.0;
-        }
+    for (int i = t; i < bn; i += (int)blockDim.x - 64) {
+      const int64_t c = n0 + i;
+      const bool ok = c < P.n;
+      // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
+      // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
+      // evaluates the reference's grouping without per-element branches
+      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
+      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
+      if (E.bn_mean) {
+        sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
+        sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
+        sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
+        sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+        sCol[6 * bn + i] = ok ? E.bn_inv_denom[c] : 1.0;
       }
     }
     if (CHAIN) {
       const qg_epilogue& E2 = P.epi2;
       const int bn2 = P.bn2;
       for (int i = t; i < bn2; i += (int)blockDim.x - 64) {
-        const int64_t c = n0_2 + i;
+        const int64_t c = i;
         const bool ok = c < P.n2;
         sCol2[0 * bn2 + i] = (ok && E2.use_col) ? __dmul_rn(E2.k_col, (double)E2.col_sums[c]) : 0.0;
         sCol2[1 * bn2 + i] = (ok && E2.bias) ? E2.bias[c] : 0.0;
@@ -675,31 +463,6 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
           sCol2[6 * bn2 + i] = ok ? E2.bn_inv_denom[c] : 1.0;
         }
       }
-    }
-  }
-  if (abits && warp >= 2) {
-    // expander warps: packed 128x128 bit block -> UMMA K-major 0/1 bytes (16 KB) per
-    // ring slot; thread -> (row, 16-bit K-core) = one 16-byte store
-    const int et = tid - 64;
-    for (int it = 0; it < nk; ++it) {
-      const uint32_t g = it0 + (uint32_t)it;
-      const int s = (int)(g % (uint32_t)S);
-      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
-      uint8_t* slot = stage0 + (size_t)s * stage_bytes;
-      const uint32_t* bits = reinterpret_cast<const uint32_t*>(slot + a_bytes + slot_b);
-      // u = (row/8, K-core, row%8) is exactly the UMMA core-matrix order: the 16-byte
-      // store for unit u lands at u * 16 (consecutive lanes -> consecutive addresses)
-      for (int u = et; u < 1024; u += (int)blockDim.x - 64) {
-        const int r = ((u >> 6) << 3) | (u & 7), c = (u >> 3) & 7;
-        const uint32_t x = bits[r * 4 + (c >> 1)] >> ((c & 1) * 16);
-        *reinterpret_cast<uint4*>(slot + u * 16) =
-            make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu), expand_nibble((x >> 8) & 0xFu),
-                       expand_nibble((x >> 12) & 0xFu));
-      }
-      // generic-proxy smem writes -> visible to the tensor core (async proxy)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&R.aready[s]);
     }
   }
   __syncwarp();
@@ -721,24 +484,17 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     R.it0 += (uint32_t)P.k2;
     uint8_t* mid0 = stage0 + (size_t)(itc % (uint32_t)S) * stage_bytes;
     uint8_t* mid1 = stage0 + (size_t)((itc + 1) % (uint32_t)S) * stage_bytes;
-    // a pair writes into the peer's slots: both CTAs' stage-1 MMAs must have drained them
-    // (same row block => same K tiles => same ring positions and slot addresses)
-    if (cpair) cluster_barrier();
-    tile_epilogue<1>(P, G, R, tile, rb, n0, nk, tmem, sCol, true, false, mid0, mid1, cpair ? (nt ^ 1) : -1);
+    tile_epilogue<1>(P, G, R, tile, rb, n0, nk, tmem, sCol, true, mid0, mid1);
     // generic-proxy code stores -> visible to the tensor core; TMEM reads retired
-    if (cpair) asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
-    else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
-    if (cpair) cluster_barrier();
-    else __syncthreads();
+    __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const qg_epilogue& E2 = P.epi2;
     if (tid < 128) {
       // stage 2's row terms: RN(k_row * code row sum), the sums of the codes just written
-      // (a pair adds the peer's partial sums over its half of the columns)
       const int64_t row = rb * 128 + tid;
-      unsigned long long rs = R.sRowSum[tid];
-      if (cpair) rs += ld_peer_u64(peer_addr(smem_u32(&R.sRowSum[tid]), (uint32_t)(nt ^ 1)));
+      const unsigned long long rs = R.sRowSum[tid];
       R.sRowTerm[tid] = (E2.use_row && row < G.m) ? __dmul_rn(E2.k_row, (double)rs) : 0.0;
     }
     if (warp == 1 && lane == 0) {
@@ -761,17 +517,15 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     asm volatile("tcgen05.fence::after_thread_sync;");
     __syncthreads();                                     // stage-2 row terms visible
     if (tid == 0) tstamp(P, tile, 7);
-    tile_epilogue<2>(P, G, R, tile, rb, n0_2, P.k2, tmem, sCol2, true, false);
+    tile_epilogue<2>(P, G, R, tile, rb, 0, P.k2, tmem, sCol2, true);
     if (tid == 0) tstamp(P, tile, 4);
     if (E2.out_kind == QG_OUT_PLANES && G.q_row_sums) {
       __syncthreads();
       if (tid < 128 && rb * 128 + tid < G.m && R.sRowSum[128 + tid])
         atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[128 + tid]);
     }
-    // the peer reads this CTA's shared memory (codes, row sums) until its own barrier
-    if (cpair) cluster_barrier();
   } else {
-    tile_epilogue<0>(P, G, R, tile, rb, n0, nk, tmem, sCol, fused, screen);
+    tile_epilogue<0>(P, G, R, tile, rb, n0, nk, tmem, sCol, fused);
     if (tid == 0) tstamp(P, tile, 4);
     if (P.mode == QG_GEMM_EPILOGUE && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
       __syncthreads();
@@ -783,19 +537,12 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (tid == 0) tstamp(P, tile, 5);
-  if (P.ready_cur && tid == 0) {
-    // dataflow epoch: every thread's epilogue stores precede the CTA barrier above; the
-    // gpu-scope fence makes them visible before the counter's release increment
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.ready_cur + G.rb_base + rb) : "memory");
-  }
 }
 
-// CTA setup shared by both kernels: TMEM allocation, ring barriers.
+// CTA setup: TMEM allocation, ring barriers.
 template <int TMEM_COLS>
 __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t* full, uint64_t* empty,
-                                            uint64_t* aready, uint64_t* done, uint32_t* tmem_base_s,
-                                            unsigned long long* sRowSum,
+                                            uint64_t* done, uint32_t* tmem_base_s, unsigned long long* sRowSum,
                                             double* sRowTerm, int S, uint32_t stage_bytes_max) {
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) {
@@ -804,11 +551,9 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
-    // aready: one arrival per expander warp (warps 2..)
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
-      mbar_init(&aready[i], (blockDim.x >> 5) - 2);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -818,7 +563,6 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.full = full;
   R.empty = empty;
   R.done = done;
-  R.aready = aready;
   R.sRowSum = sRowSum;
   R.sRowTerm = sRowTerm;
   R.S = S;
@@ -830,7 +574,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
 template <int TMEM_COLS, int MINB, int NT, bool CHAIN = false>
 __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
+  __shared__ __align__(8) uint64_t full[8], empty[8], done;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];   // chained: [stage 1 | stage 2]
   __shared__ double sRowTerm[128];
@@ -838,9 +582,8 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   // schedule arrays and the segment table are static for the lifetime of a launch
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
-  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
-                         P.a_bits ? ((16384u + (uint32_t)P.slot_bn * 128u + 2048u + 1023u) & ~1023u)
-                                  : 16384u + (uint32_t)P.slot_bn * 128u);
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
+                         16384u + (uint32_t)P.slot_bn * 128u);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -990,8 +733,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   }
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
-  const bool screen = fused && E.out_kind == QG_OUT_PLANES && E.screen_tol > 0.0 &&
-                      (E.act == QG_ACT_NONE || E.act == QG_ACT_RELU);
   if (tid < 128) sRowSum[tid] = 0ull;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1000,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base_s;
   TileRing R;
-  R.stage0 = stage0; R.sCol = sCol; R.full = full; R.empty = empty; R.done = &done; R.aready = nullptr;
+  R.stage0 = stage0; R.sCol = sCol; R.full = full; R.empty = empty; R.done = &done;
   R.sRowSum = sRowSum; R.sRowTerm = sRowTerm; R.S = S; R.it0 = 0; R.ndone = 0; R.pdl_wait = false; R.tmem = tmem;
 
   if (warp == 0 && lane == 0) {
@@ -1060,40 +801,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       const int64_t row = rb * 128 + t;
       sRowTerm[t] = (E.use_row && rb_ok && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
     }
-    if (screen) {
-      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
-        const int64_t cc = n0 + i;
-        double pc = 0.0, gc = 0.0, rc = 0x1p12;
-        if (cc < P.n) {
-          const double inv = E.q_inv_scale;
-          const double sC = E.use_col ? E.k_col * (double)E.col_sums[cc] : 0.0;
-          const double base = (sC + (E.use_const ? E.k_const : 0.0)) + (E.bias ? E.bias[cc] : 0.0);
-          double g = 1.0, center = base;
-          if (E.bn_mean) {
-            g = E.bn_gamma[cc] / E.bn_denom[cc];
-            center = (base - E.bn_mean[cc]) * g + E.bn_beta[cc];
-          }
-          gc = g * inv;
-          pc = E.k_acc * gc;
-          rc = 0x1p12 + (center - E.q_amin) * inv;
-        }
-        sCol[i] = pc;
-        sCol[bn + i] = gc;
-        sCol[2 * bn + i] = rc;
-      }
-    } else {
-      for (int i = t; i < bn; i += (int)blockDim.x - 64) {
-        const int64_t cc = n0 + i;
-        const bool ok = cc < P.n;
-        sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[cc]) : 0.0;
-        sCol[1 * bn + i] = (ok && E.bias) ? E.bias[cc] : 0.0;
-        if (E.bn_mean) {
-          sCol[2 * bn + i] = ok ? E.bn_mean[cc] : 0.0;
-          sCol[3 * bn + i] = ok ? E.bn_denom[cc] : 1.0;
-          sCol[4 * bn + i] = ok ? E.bn_gamma[cc] : 0.0;
-          sCol[5 * bn + i] = ok ? E.bn_beta[cc] : 0.0;
-          sCol[6 * bn + i] = ok ? E.bn_inv_denom[cc] : 1.0;
-        }
+    for (int i = t; i < bn; i += (int)blockDim.x - 64) {
+      const int64_t cc = n0 + i;
+      const bool ok = cc < P.n;
+      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[cc]) : 0.0;
+      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[cc] : 0.0;
+      if (E.bn_mean) {
+        sCol[2 * bn + i] = ok ? E.bn_mean[cc] : 0.0;
+        sCol[3 * bn + i] = ok ? E.bn_denom[cc] : 1.0;
+        sCol[4 * bn + i] = ok ? E.bn_gamma[cc] : 0.0;
+        sCol[5 * bn + i] = ok ? E.bn_beta[cc] : 0.0;
+        sCol[6 * bn + i] = ok ? E.bn_inv_denom[cc] : 1.0;
       }
     }
   }
@@ -1105,7 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   __syncthreads();
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 3);
   if (rb_ok) {
-    tile_epilogue<0>(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused, screen);
+    tile_epilogue<0>(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused);
     if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
     if (fused && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
       __syncthreads();
@@ -1119,305 +837,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   cluster_sync_all();                                    // both CTAs done with TMEM and the ring
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 5);
-}
-
-// ------------------------------------------------ persistent 2-SM int32 GEMM
-// Persistent CTA pairs (one CTA per SM) for the int32 output mode: each pair loops over
-// (segment, row-block pair, N tile) work items with TWO TMEM accumulators (2 x bn
-// columns).  The producer and the leader's MMA thread run ahead into the next tile while
-// 8 epilogue warps per CTA drain the previous accumulator, so a tile's epilogue overlaps
-// the next tile's main loop inside the pair (the one-tile pair kernel relies on a second
-// co-resident CTA for that).  Barriers: full/empty (ring, as tc_pair_kernel), tfull[b]
-// (MMA commit -> both CTAs' epilogue warps), tempty[b] (16 epilogue-warp arrivals of both
-// CTAs, on the leader -> the MMA may overwrite accumulator b).
-constexpr int kPersistThreads = 320;    // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-
-__device__ __forceinline__ void pair_item(const TiledParams& P, int64_t pair, const qg_tseg*& Gp, int64_t& rbp,
-                                          int& nt) {
-  int lo = 0, hi = P.nsegs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (P.segs[mid].cta_begin <= pair) lo = mid; else hi = mid - 1;
-  }
-  Gp = &P.segs[lo];
-  const int64_t local = pair - Gp->cta_begin;
-  pair_swizzle(local, ((Gp->r128 >> 7) + 1) >> 1, P.n_tiles, P.pair_swizzle, rbp, nt);
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPersistThreads, 1)
-    tc_pair_persist_kernel(const __grid_constant__ TiledParams P) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], tfull[2], tempty[2];
-  __shared__ uint32_t tmem_base_s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint32_t rank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const int bn = P.bn, S = P.stages, bh = bn >> 1;
-  const int64_t pair_step = (int64_t)(gridDim.x >> 1), pair0 = (int64_t)(blockIdx.x >> 1);
-  const int64_t total_pairs = P.total_ctas >> 1;
-  const uint32_t a_bytes = 16384u, bh_bytes = (uint32_t)bh * 128u, stage_bytes = a_bytes + bh_bytes;
-  uint8_t* stage0 = smem;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_s)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  if (tid == 32) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 16); }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("griddepcontrol.launch_dependents;");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  cluster_sync_all();                                    // barriers of both CTAs initialised
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base_s;
-
-  if (warp == 0 && lane == 0) {
-    // ---------------- producer (both CTAs): own A block + own half of B, all tiles ----------------
-    const uint32_t leader_full = mapa_cluster(smem_u32(&full[0]), 0);
-    uint32_t it = 0;
-    for (int64_t pair = pair0; pair < total_pairs; pair += pair_step) {
-      const qg_tseg* Gp;
-      int64_t rbp;
-      int nt;
-      pair_item(P, pair, Gp, rbp, nt);
-      const qg_tseg& G = *Gp;
-      const int64_t n0 = (int64_t)nt * bn, nrb = G.r128 >> 7, rb = rbp * 2 + rank;
-      const bool rb_ok = rb < nrb;
-      const int64_t b_row0 = ((n0 + (int64_t)rank * bh) >> 3) * 8;
-      UnionCursor c{};
-      int nk = G.k_tiles, kbase_me = 0, i_me = 0;
-      if (P.a_blocks) {
-        const int64_t rb0 = rbp * 2, rb1 = rbp * 2 + 1;
-        c.l0 = G.blk_kt + G.blk_base[rb0];
-        c.n0 = G.blk_count[rb0];
-        c.l1 = rb1 < nrb ? G.blk_kt + G.blk_base[rb1] : nullptr;
-        c.n1 = rb1 < nrb ? G.blk_count[rb1] : 0;
-        kbase_me = rb_ok ? G.blk_base[rb] : 0;
-        nk = 0x7fffffff;
-      }
-      for (int k = 0; k < nk; ++k, ++it) {
-        int kt;
-        const void* amap;
-        int64_t arow;
-        if (P.a_blocks) {
-          if (!(c.i0 < c.n0 || c.i1 < c.n1)) break;
-          bool h0, h1;
-          kt = c.next(h0, h1);
-          const bool mine = rank == 0 ? h0 : h1;
-          const bool real = rb_ok && mine;
-          amap = real ? (const void*)G.tmap_a : (const void*)&P.zero_map;
-          arow = real ? (int64_t)(kbase_me + i_me) * 128 : 0;
-          i_me += mine;
-        } else {
-          kt = k;
-          amap = rb_ok ? (const void*)G.tmap_a : (const void*)&P.zero_map;
-          arow = rb_ok ? (((int64_t)kt * (G.r128 << 7) + rb * 16384) >> 7) : 0;
-        }
-        const int s = (int)(it % (uint32_t)S);
-        if (it >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
-        uint8_t* dst = stage0 + (size_t)s * stage_bytes;
-        if (rank == 0) mbar_expect_tx(&full[s], 2u * (a_bytes + bh_bytes));
-        const uint32_t bar = leader_full + (uint32_t)s * 8u;
-        tma_2d_pair(dst, amap, 0, (int32_t)arow, bar);
-        tma_2d_pair(dst + a_bytes, G.tmap_b, 0, (int32_t)(((int64_t)kt * (P.b_npad << 7) >> 7) + b_row0), bar);
-      }
-    }
-  } else if (warp == 1 && lane == 0 && rank == 0) {
-    // ---------------- MMA issuer (leader), accumulators alternate per tile ----------------
-    const uint32_t idesc = (2u << 4) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-    uint32_t it = 0;
-    int tcount = 0;
-    for (int64_t pair = pair0; pair < total_pairs; pair += pair_step, ++tcount) {
-      const qg_tseg* Gp;
-      int64_t rbp;
-      int nt;
-      pair_item(P, pair, Gp, rbp, nt);
-      const qg_tseg& G = *Gp;
-      int nk = G.k_tiles;
-      if (P.a_blocks) {
-        const int64_t nrb = G.r128 >> 7, rb0 = rbp * 2, rb1 = rbp * 2 + 1;
-        UnionCursor c{};
-        c.l0 = G.blk_kt + G.blk_base[rb0];
-        c.n0 = G.blk_count[rb0];
-        c.l1 = rb1 < nrb ? G.blk_kt + G.blk_base[rb1] : nullptr;
-        c.n1 = rb1 < nrb ? G.blk_count[rb1] : 0;
-        nk = 0;
-        bool h0, h1;
-        while (c.i0 < c.n0 || c.i1 < c.n1) { c.next(h0, h1); ++nk; }
-      }
-      const int b = tcount & 1;
-      const uint32_t use = (uint32_t)(tcount >> 1);
-      if (use > 0) mbar_wait(smem_u32(&tempty[b]), (use - 1) & 1);   // both CTAs drained accumulator b
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t acc = tmem + (uint32_t)(b * bn);
-      for (int k = 0; k < nk; ++k, ++it) {
-        const int s = (int)(it % (uint32_t)S);
-        mbar_wait(smem_u32(&full[s]), (it / S) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_i8_pair(acc, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc, (k > 0 || kk > 0) ? 1u : 0u);
-        umma_commit_pair(&empty[s]);
-      }
-      if (nk > 0) {
-        umma_commit_pair(&tfull[b]);
-      } else {
-        // no K tile: nothing to commit; release both CTAs' epilogues directly (zeros)
-        mbar_arrive(&tfull[b]);
-        mbar_arrive_remote(mapa_cluster(smem_u32(&tfull[b]), 1));
-      }
-    }
-  } else if (warp >= 2) {
-    // ---------------- epilogue: 8 warps; warp w reads TMEM lanes 32*(w % 4).., column half (w-2)/4
-    const int quad = warp & 3, half = (warp - 2) >> 2;
-    const uint32_t leader_tempty = mapa_cluster(smem_u32(&tempty[0]), 0);
-    int tcount = 0;
-    for (int64_t pair = pair0; pair < total_pairs; pair += pair_step, ++tcount) {
-      const qg_tseg* Gp;
-      int64_t rbp;
-      int nt;
-      pair_item(P, pair, Gp, rbp, nt);
-      const qg_tseg& G = *Gp;
-      const int64_t n0 = (int64_t)nt * bn, nrb = G.r128 >> 7, rb = rbp * 2 + rank;
-      bool has_acc = G.k_tiles > 0;
-      if (P.a_blocks) {
-        const int64_t rb1 = rbp * 2 + 1;
-        has_acc = G.blk_count[rbp * 2] + (rb1 < nrb ? G.blk_count[rb1] : 0) > 0;
-      }
-      const int b = tcount & 1;
-      mbar_wait(smem_u32(&tfull[b]), (uint32_t)(tcount >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const int64_t myrow = rb * 128 + quad * 32 + lane;
-      const bool rvalid = rb < nrb && myrow < G.m;
-      const int64_t rem = P.n - n0;
-      const int ncols = rem <= 0 ? 0 : (rem < bn ? (int)rem : bn);
-      const int nslices = (ncols + 7) >> 3;
-      const bool vec_ok = (P.n & 3) == 0 && (reinterpret_cast<uintptr_t>(G.out_i32) & 15) == 0;
-      const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * bn);
-      for (int sl = half; sl < nslices; sl += 2) {
-        uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (has_acc) {
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                         "=r"(v[7])
-                       : "r"(trow + (uint32_t)(sl * 8)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        }
-        if (rvalid) {
-          int32_t* dst = G.out_i32 + myrow * P.n + n0 + sl * 8;
-          if (vec_ok && sl * 8 + 8 <= ncols) {
-            reinterpret_cast<int4*>(dst)[0] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
-            reinterpret_cast<int4*>(dst)[1] = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
-          } else {
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (sl * 8 + jj < ncols) dst[jj] = (int32_t)v[jj];
-          }
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncwarp();
-      if (lane == 0) {
-        if (rank == 0) mbar_arrive(&tempty[b]);
-        else mbar_arrive_remote(leader_tempty + (uint32_t)b * 8u);
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  cluster_sync_all();                                    // both CTAs done with TMEM and the ring
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// ------------------------------------------------ persistent epoch kernel
-// All GEMM stages of an epoch (2 per layer, every batch) in ONE cooperative launch:
-// CTAs loop over each stage's tiles, then meet at a grid barrier before the next
-// stage (whose operands the previous stage's epilogues wrote).  TMEM, the mbarrier
-// ring and the per-CTA prologue are paid once per epoch instead of once per stage.
-constexpr int kMaxEpochStages = 8;
-struct EpochParams {
-  TiledParams st[kMaxEpochStages];
-  int32_t nstages;
-  int32_t ring_stages;
-  uint32_t stage_bytes_max;
-  unsigned int* grid_bar;   // zeroed before the launch
-  int32_t dataflow;         // 1: one tile queue over all stages, per-row-block waits
-  int64_t total_all;        // dataflow: tiles of all stages
-};
-
-static __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int target = (gen + 1u) * nblocks;
-    // release: this CTA's epilogue stores (ordered by the CTA barrier) before the arrival
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  ++gen;
-  __syncthreads();
-  // the next stage reads the previous stage's generic-proxy stores with bulk copies
-  // (async proxy)
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// Dynamic tile scheduler: one counter per stage (zeroed with the barrier word); the
-// CTA's next tile is broadcast through shared memory.
-static __device__ __forceinline__ int64_t next_tile(unsigned int* ctr, int64_t* s_tile) {
-  __syncthreads();
-  if (threadIdx.x == 0) *s_tile = (int64_t)atomicAdd(ctr, 1u);
-  __syncthreads();
-  return *s_tile;
-}
-
-template <int TMEM_COLS>
-__global__ void __maxnreg__(112) tc_tiled_epoch_kernel(const __grid_constant__ EpochParams EP) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
-  __shared__ uint32_t tmem_base_s;
-  __shared__ unsigned long long sRowSum[128];
-  __shared__ double sRowTerm[128];
-  TileRing R;
-  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, EP.ring_stages,
-                         EP.stage_bytes_max);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  R.tmem = tmem_base_s;
-  __shared__ int64_t s_tile;
-  if (EP.dataflow) {
-    // every tile is claimed from one stage-major queue: a tile only waits for tiles of
-    // earlier stages, which were claimed earlier by running CTAs, so the grid needs no
-    // co-residency (no static first tile: a CTA that is not yet resident owns nothing)
-    for (;;) {
-      int64_t t = next_tile(EP.grid_bar, &s_tile);
-      if (t >= EP.total_all) break;
-      int st = 0;
-      while (t >= EP.st[st].total_ctas) { t -= EP.st[st].total_ctas; ++st; }
-      tiled_tile<TMEM_COLS, false>(EP.st[st], t, R);
-    }
-    if ((threadIdx.x >> 5) == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
-    return;
-  }
-  unsigned int gen = 0;
-  for (int st = 0; st < EP.nstages; ++st) {
-    const TiledParams& P = EP.st[st];
-    // first tile static (every CTA has one while tiles last), the rest claimed dynamically
-    for (int64_t tile = blockIdx.x; tile < P.total_ctas;
-         tile = (int64_t)gridDim.x + next_tile(EP.grid_bar + 1 + st, &s_tile))
-      tiled_tile<TMEM_COLS, false>(P, tile, R);
-    if (st + 1 < EP.nstages) grid_sync(EP.grid_bar, gridDim.x, gen);
-  }
-  if ((threadIdx.x >> 5) == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
 }
 
 // ------------------------------------------------ adjacency block preparation
@@ -1651,14 +1070,6 @@ static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaS
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  if (CHAIN && P.chain == 2) {
-    // chained CTA pairs: the two N halves of a row block share stage-1 codes through DSMEM
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = 2;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-  }
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, tc_tiled_kernel<COLS, MINB, NT, CHAIN>, P);
@@ -1676,6 +1087,10 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   if (a->epi && a->epi->bn_mean && !(a->epi->bn_denom && a->epi->bn_gamma && a->epi->bn_beta && a->epi->bn_inv_denom))
     { rc = QG_ERR_ARG; return 0; }
   if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) { rc = QG_ERR_SHAPE; return 0; }
+  // reserved fields (round-1 opt-in variants, removed) must be zero
+  if (a->a_bits || a->reserved1 || a->reserved2 || a->reserved3 ||
+      (a->epi && (a->epi->reserved_d0 != 0.0 || a->epi->reserved_d1 != 0.0)))
+    { rc = QG_ERR_UNSUPPORTED; return 0; }
   P = TiledParams{};
   P.segs = a->segs; P.nsegs = a->nsegs; P.a_blocks = a->a_blocks; P.b_npad = a->b_npad; P.n = a->n;
   P.bn = a->bn; P.n_tiles = a->n_tiles; P.mode = a->mode; P.out_layout = a->out_layout; P.out_npad = a->out_npad;
@@ -1684,20 +1099,13 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   if (a->epi) P.epi = *a->epi;
   P.phase_ns = a->phase_ns;
   P.total_ctas = a->total_ctas;
-  P.a_bits = a->a_blocks ? a->a_bits : 0;
   P.pair = a->pair;
   P.slot_bn = P.bn;
-  P.ready_prev = a->ready_prev;
-  P.ready_cur = a->ready_cur;
-  P.expect_prev = a->expect_prev;
-  const bool screen = a->epi && a->epi->out_kind == QG_OUT_PLANES && a->epi->screen_tol > 0.0 &&
-                      (a->epi->act == QG_ACT_NONE || a->epi->act == QG_ACT_RELU);
-  size_t cols = (screen ? 3 : (a->epi && a->epi->bn_mean ? 7 : 2)) * (size_t)P.bn * 8;
+  size_t cols = (a->epi && a->epi->bn_mean ? 7 : 2) * (size_t)P.bn * 8;
   if (a->chain) {
     const qg_chain* c = a->chain;
-    // stage 1: one N tile covering all its columns, packed codes, no screen, byte blocks
-    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != (c->split ? 2 : 1) || a->n > (int64_t)a->n_tiles * a->bn ||
-        a->pair || P.a_bits || screen ||
+    // stage 1: one N tile covering all its columns, packed codes
+    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != 1 || a->n > a->bn || a->pair || c->reserved ||
         a->epi->out_kind != QG_OUT_PLANES)
       { rc = QG_ERR_UNSUPPORTED; return 0; }
     if (!c->w || !c->epi || c->w_npad < 32 || c->w_npad > 256 || (c->w_npad & (c->w_npad - 1)) || c->n < 1 ||
@@ -1705,12 +1113,8 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
         (c->out_layout == 0) != (c->epi->out_kind == QG_OUT_REAL) ||
         (c->epi->bn_mean && !(c->epi->bn_denom && c->epi->bn_gamma && c->epi->bn_beta && c->epi->bn_inv_denom)))
       { rc = QG_ERR_ARG; return 0; }
-    if (c->split) {
-      // CTA pairs: n_tiles == 2 stage-1 halves, stage-2 halves of w_npad / 2 >= 16 columns
-      if (a->n_tiles != 2 || (a->total_ctas & 1) || c->w_npad < 32) { rc = QG_ERR_UNSUPPORTED; return 0; }
-    }
-    P.chain = c->split ? 2 : 1;
-    P.bn2 = (int32_t)(c->split ? c->w_npad / 2 : c->w_npad);
+    P.chain = 1;
+    P.bn2 = (int32_t)c->w_npad;
     P.k2 = (int32_t)((a->n + 127) / 128);
     P.n2 = c->n;
     P.out_layout2 = c->out_layout;
@@ -1795,7 +1199,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   if (rc != QG_OK) return rc;
   if (P.pair) {
     // total_ctas = 2 x pairs; a stage holds the own A block + half of the B tile
-    if (P.a_bits || (a->total_ctas & 1) || P.bn < 64) return QG_ERR_UNSUPPORTED;
+    if ((a->total_ctas & 1) || P.bn < 64) return QG_ERR_UNSUPPORTED;
     void* zero = nullptr;
     cudaGetSymbolAddress(&zero, g_zero_block);
     if (qg_encode_linear_map(zero, 16384, 128, &P.zero_map) != QG_OK) return QG_ERR_UNSUPPORTED;
@@ -1805,37 +1209,6 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     P.pair_swizzle = swz < 1 ? 1 : swz;
     const size_t stage = 16384 + (size_t)P.bn * 64;
     cudaStream_t st = (cudaStream_t)stream;
-    static const bool persist = getenv("QG_PAIR_PERSIST") != nullptr && atoi(getenv("QG_PAIR_PERSIST")) != 0;
-    if (persist && P.mode == QG_GEMM_I32) {
-      // persistent pairs, one CTA per SM: a deep ring and two TMEM accumulators
-      static int psms = 0;
-      if (!psms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&psms, cudaDevAttrMultiProcessorCount, dev);
-      }
-      P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (size_t)(200 * 1024) / stage));
-      const size_t smem = (size_t)P.stages * stage;
-      static size_t pattr = 0;
-      if (smem > pattr) {
-        cudaFuncSetAttribute(tc_pair_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        pattr = smem;
-      }
-      const int64_t grid = std::min<int64_t>(a->total_ctas, (int64_t)(psms & ~1));
-      static const bool pdl = getenv("QG_NO_PDL") == nullptr;
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)grid);
-      cfg.blockDim = dim3(kPersistThreads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = pdl ? 1 : 0;
-      cudaLaunchKernelEx(&cfg, tc_pair_persist_kernel, P);
-      return tstatus();
-    }
     P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
     const size_t smem = (size_t)P.stages * stage + cols;
     const unsigned grid = (unsigned)a->total_ctas;
@@ -1846,8 +1219,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     }
     return tstatus();
   }
-  const size_t stage = P.a_bits ? ((16384 + (size_t)P.slot_bn * 128 + 2048 + 1023) & ~(size_t)1023)
-                                : 16384 + (size_t)P.slot_bn * 128;
+  const size_t stage = 16384 + (size_t)P.slot_bn * 128;
   // Occupancy: 2 CTAs/SM by default (one CTA's fp64 epilogue overlaps the other's main
   // loop).  Stages with N tiles <= 128 and >= 3 CTAs per SM of work run 3 CTAs/SM
   // (80-register variant, 72 KB ring, 3 x <= 128 TMEM columns): more warps hide the
@@ -1872,9 +1244,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     // chained aggregate -> update: one tile per CTA.  A chained stage has half the CTAs of
     // the split-N stages it replaces and two epilogues per tile: with fewer tiles than
     // SMs, 16 warps (1 CTA/SM) split the epilogue slices 4 ways
-    static const int chain_nt = getenv("QG_CHAIN_NT") ? atoi(getenv("QG_CHAIN_NT")) : 0;
-    static const bool wide_chain = getenv("QG_CHAIN_WIDE") != nullptr && atoi(getenv("QG_CHAIN_WIDE")) != 0;
-    const bool wide16 = chain_nt == 512 || (chain_nt == 0 && a->total_ctas <= (int64_t)sms);
+    const bool wide16 = a->total_ctas <= (int64_t)sms;
     if (wide16) {
       switch (tcols) {
         case 32: launch_tiled<32, 1, 512, true>(P, grid, smem, st); break;
@@ -1887,12 +1257,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
         case 32: launch_tiled<32, 2, kTThreads, true>(P, grid, smem, st); break;
         case 64: launch_tiled<64, 2, kTThreads, true>(P, grid, smem, st); break;
         case 128: launch_tiled<128, 2, kTThreads, true>(P, grid, smem, st); break;
-        default:
-          // 128x256 tiles in both stages (C4): 3 warp groups split the two epilogues.
-          // Opt-in (QG_CHAIN_WIDE=1): the 80-register bound spills, C4 7.01 vs 6.86 ms
-          if (wide_chain) launch_tiled<256, 2, 384, true>(P, grid, smem, st);
-          else launch_tiled<256, 2, kTThreads, true>(P, grid, smem, st);
-          break;
+        default: launch_tiled<256, 2, kTThreads, true>(P, grid, smem, st); break;
       }
     }
   } else if (three) {
@@ -1915,109 +1280,6 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     }
   }
   return tstatus();
-}
-
-template <int COLS>
-static int launch_epoch(EpochParams& EP, size_t smem, int64_t max_tiles, cudaStream_t st) {
-  static size_t attr_done = 0;
-  if (smem > attr_done) {
-    cudaFuncSetAttribute(tc_tiled_epoch_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tc_tiled_epoch_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    attr_done = smem;
-  }
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_tiled_epoch_kernel<COLS>, kTThreads, smem);
-  static const char* env_per_sm = getenv("QG_EPOCH_PER_SM");    // co-residency experiments
-  if (env_per_sm) per_sm = atoi(env_per_sm);
-  // TMEM: COLS <= 256 columns per CTA, so every co-resident CTA can allocate (512 per SM)
-  per_sm = std::min(per_sm, 512 / COLS);
-  // dataflow: no co-residency needed (see tc_tiled_epoch_kernel); 2 CTAs/SM fit in
-  // shared memory and TMEM although the occupancy API reports 1 for tcgen05.alloc kernels
-  if (EP.dataflow) per_sm = std::min(2, 512 / COLS);
-  if (per_sm < 1) return QG_ERR_UNSUPPORTED;
-  const int64_t grid = std::min<int64_t>(EP.dataflow ? EP.total_all : max_tiles, (int64_t)sms * per_sm);
-  static const bool dbg = getenv("QG_DEBUG_EPOCH") != nullptr;
-  if (dbg) {
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, tc_tiled_epoch_kernel<COLS>);
-    int per_sm_single = 0;
-    cudaFuncAttributes fb{};
-    cudaFuncGetAttributes(&fb, tc_tiled_kernel<COLS, 2, kTThreads>);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2, kTThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tc_tiled_kernel<COLS, 2, kTThreads>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_single, tc_tiled_kernel<COLS, 2, kTThreads>, kTThreads, smem);
-    int smem_sm = 0, smem_blk = 0, p2 = 0, p3 = 0;
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, tc_tiled_epoch_kernel<COLS>, kTThreads, 90 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p3, tc_tiled_epoch_kernel<COLS>, kTThreads, 60 * 1024);
-    fprintf(stderr, "params=%zu tiledparams=%zu\n", sizeof(EpochParams), sizeof(TiledParams));
-    fprintf(stderr, "qg_tiled_epoch: COLS=%d smem=%zu per_sm=%d grid=%lld stages=%d ring=%d regs=%d static=%zu "
-            "maxThreads=%d | single-stage kernel regs=%d per_sm=%d | smem/SM=%d smem/blk=%d occ@90K=%d occ@60K=%d\n",
-            COLS, smem, per_sm, (long long)grid, EP.nstages, EP.ring_stages, fa.numRegs, fa.sharedSizeBytes,
-            fa.maxThreadsPerBlock, fb.numRegs, per_sm_single, smem_sm, smem_blk, p2, p3);
-  }
-  cudaMemsetAsync(EP.grid_bar, 0, sizeof(unsigned int) * (1 + kMaxEpochStages), st);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kTThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;          // grid barrier: all CTAs co-resident
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = EP.dataflow ? 0 : 1;
-  const cudaError_t err = cudaLaunchKernelEx(&cfg, tc_tiled_epoch_kernel<COLS>, EP);
-  if (dbg && err != cudaSuccess) fprintf(stderr, "qg_tiled_epoch launch: %s\n", cudaGetErrorString(err));
-  return tstatus();
-}
-
-extern "C" int qg_tiled_epoch(const qg_tiled_args* stages, int32_t nstages, uint32_t* grid_bar, void* stream) {
-  if (!stages || nstages < 1 || nstages > kMaxEpochStages || !grid_bar) return QG_ERR_ARG;
-  EpochParams EP{};
-  size_t cols_max = 0;
-  int bn_max = 32;
-  int64_t max_tiles = 1;
-  for (int i = 0; i < nstages; ++i) {
-    int rc;
-    if (stages[i].chain) return QG_ERR_UNSUPPORTED;
-    const size_t cols = tiled_params(&stages[i], EP.st[i], rc);
-    if (rc != QG_OK) return rc;
-    cols_max = std::max(cols_max, cols);
-    bn_max = std::max(bn_max, EP.st[i].bn);
-    max_tiles = std::max<int64_t>(max_tiles, EP.st[i].total_ctas);
-  }
-  const size_t stage = (16384 + (size_t)bn_max * 128 + 2048 + 1023) & ~(size_t)1023;   // + packed bit block
-  const int ring = (int)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols_max) / stage));
-  for (int i = 0; i < nstages; ++i) EP.st[i].stages = ring;
-  EP.nstages = nstages;
-  EP.ring_stages = ring;
-  EP.stage_bytes_max = (uint32_t)stage;
-  EP.grid_bar = grid_bar;
-  EP.dataflow = stages[0].ready_cur != nullptr;
-  for (int i = 0; i < nstages; ++i) {
-    if ((stages[i].ready_cur != nullptr) != (EP.dataflow != 0)) return QG_ERR_ARG;
-    if (EP.dataflow && i > 0 && stages[i].ready_prev && stages[i].expect_prev < 1) return QG_ERR_ARG;
-    EP.total_all += EP.st[i].total_ctas;
-  }
-  const size_t smem = (size_t)ring * stage + cols_max;
-  if (getenv("QG_DEBUG_EPOCH"))
-    for (int i = 0; i < nstages; ++i)
-      fprintf(stderr, "  stage %d: segs=%p nsegs=%d total=%lld bn=%d n_tiles=%d a_blocks=%d mode=%d n=%lld b_npad=%lld\n",
-              i, (const void*)EP.st[i].segs, EP.st[i].nsegs, (long long)EP.st[i].total_ctas, EP.st[i].bn,
-              EP.st[i].n_tiles, EP.st[i].a_blocks, EP.st[i].mode, (long long)EP.st[i].n, (long long)EP.st[i].b_npad);
-  cudaStream_t st = (cudaStream_t)stream;
-  switch (bn_max) {
-    case 32: return launch_epoch<32>(EP, smem, max_tiles, st);
-    case 64: return launch_epoch<64>(EP, smem, max_tiles, st);
-    case 128: return launch_epoch<128>(EP, smem, max_tiles, st);
-    default: return launch_epoch<256>(EP, smem, max_tiles, st);
-  }
 }
 
 extern "C" int qg_block_prepare(const uint32_t* a_words, int64_t rows, int64_t padded_rows, int64_t padded_cols,

@@ -135,15 +135,12 @@ class EpochRunner:
     def kernel_launches_per_epoch(self) -> int:
         """Native (libqgtc_b200) kernels per epoch: the slab reset, 1 grouped entry
         conversion and the GEMM launches of the captured graph (2 per layer, fewer where
-        stage pairs are chained, one persistent kernel per 8 stages with FUSED_EPOCH);
-        with rescan, per batch the block expansion (+ the gather from dense words unless
-        the blocks were shipped, QGT3)."""
-        from . import engine
-        from .tiled import MAX_EPOCH_STAGES, blocked
-        stages = 2 * len(self.model.layers)
+        stage pairs are chained); with rescan, per batch the block expansion (+ the gather
+        from dense words unless the blocks were shipped, QGT3)."""
+        from .tiled import blocked
         gemms = getattr(self, "gemm_launches", None)
         if gemms is None:
-            gemms = -(-stages // MAX_EPOCH_STAGES) if engine.FUSED_EPOCH else stages
+            gemms = 2 * len(self.model.layers)
         per_epoch = 2 + gemms
         if self.rescan:
             blks = [blocked(b.adjacency) for b in self.batches]

@@ -50,7 +50,7 @@ class TSeg(ctypes.Structure):
                 ("q_codes", ctypes.c_void_p), ("q_row_sums", ctypes.c_void_p), ("out_real", ctypes.c_void_p),
                 ("out_i32", ctypes.c_void_p), ("status", ctypes.c_void_p), ("m", ctypes.c_int64),
                 ("r128", ctypes.c_int64), ("cta_begin", ctypes.c_int64), ("k_tiles", ctypes.c_int32),
-                ("pad_", ctypes.c_int32), ("rb_base", ctypes.c_int64), ("tmap_a", ctypes.c_uint8 * 128),
+                ("pad_", ctypes.c_int32), ("reserved0", ctypes.c_int64), ("tmap_a", ctypes.c_uint8 * 128),
                 ("tmap_b", ctypes.c_uint8 * 128)]
 
 
@@ -62,46 +62,26 @@ class TiledArgs(ctypes.Structure):
                 ("bn", ctypes.c_int32), ("n_tiles", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("out_layout", ctypes.c_int32), ("out_npad", ctypes.c_int64),
                 ("epi", ctypes.POINTER(N.Epilogue)), ("phase_ns", ctypes.c_void_p), ("a_bits", ctypes.c_int32),
-                ("pair", ctypes.c_int32), ("chain", ctypes.c_void_p), ("ready_prev", ctypes.c_void_p),
-                ("ready_cur", ctypes.c_void_p), ("expect_prev", ctypes.c_int32), ("pad3_", ctypes.c_int32)]
+                ("pair", ctypes.c_int32), ("chain", ctypes.c_void_p), ("reserved1", ctypes.c_void_p),
+                ("reserved2", ctypes.c_void_p), ("reserved3", ctypes.c_int32), ("pad3_", ctypes.c_int32)]
 
 
 class Chain(ctypes.Structure):
     """Mirror of ``qg_chain``: a dense stage-2 GEMM fused behind a tiled stage."""
 
     _fields_ = [("w", ctypes.c_void_p), ("w_npad", ctypes.c_int64), ("n", ctypes.c_int64),
-                ("out_layout", ctypes.c_int32), ("split", ctypes.c_int32), ("out_npad", ctypes.c_int64),
+                ("out_layout", ctypes.c_int32), ("reserved", ctypes.c_int32), ("out_npad", ctypes.c_int64),
                 ("epi", ctypes.POINTER(N.Epilogue))]
 
 
 _SIGS_DONE = False
 
-# When a list, launch() records stage arguments instead of launching (engine's fused
-# epoch); flush_epoch() then issues them as qg_tiled_epoch launches.
-EPOCH = None
-
 # qg_tiled_gemm launches issued so far (runtime.EpochRunner counts those of its graph)
 LAUNCHES = 0
-
-# The fused epoch as a DATAFLOW kernel (qg_tiled_args.ready_*): one tile queue over all
-# stages, each tile waiting only for the row blocks it reads.  Opt-in (QG_DATAFLOW=1):
-# bit-exact, but measured slower (C2 0.088 vs 0.055 ms/epoch, C3 0.33 vs 0.23): each
-# persistent CTA runs its ~3 tiles back to back (no PDL prefetch, no overlap of one tile's
-# epilogue with the next tile's loads), which costs more than the stage overlap gains.
-DATAFLOW = os.environ.get("QG_DATAFLOW", "0") == "1"
 
 # An event the first adjacency-block launch must wait on (the e2e runner's side-stream
 # H2D of the schedule + blocks and their expansion); cleared once joined.
 PENDING_JOIN = None
-MAX_EPOCH_STAGES = 8
-
-# QG_A_BITS=1: adjacency blocks reach the GEMM packed (2 KB per 128x128 block) and are
-# expanded to the tensor-core byte layout in shared memory by otherwise idle warps: 8x
-# less A traffic and no 16 KB-per-block copy in HBM (C4: 12.1 vs 16.5 GB).  Off by
-# default: the copy -> expand -> MMA chain measured slower than streaming pre-expanded
-# blocks on B200 (C2 65 vs 55 us, C4 7.9 vs 7.3 ms, C5-16k 55% vs 69% of peak;
-# profiles/r01g_abits_ab.txt) -- the main loop is latency-, not L2-bandwidth-bound.
-A_BITS = os.environ.get("QG_A_BITS", "0") == "1"
 
 # 2-SM CTA pairs for large GEMM stages (QG_PAIR=0 disables)
 PAIR = os.environ.get("QG_PAIR", "1") != "0"
@@ -120,8 +100,6 @@ def _lib():
         L.qg_codes_to_tiles.restype = ctypes.c_int
         L.qg_tiles_to_codes.argtypes = [vp, i64, i64, i32, i64, vp, i64, vp]
         L.qg_tiles_to_codes.restype = ctypes.c_int
-        L.qg_tiled_epoch.argtypes = [ctypes.POINTER(TiledArgs), ctypes.c_int32, vp, vp]
-        L.qg_tiled_epoch.restype = ctypes.c_int
         L.qg_encode_linear_map.argtypes = [vp, i64, i32, vp]
         L.qg_encode_linear_map.restype = ctypes.c_int
         _SIGS_DONE = True
@@ -181,7 +159,7 @@ class BlockedAdjacency:
 
     @property
     def bytes(self) -> torch.Tensor:
-        """Pre-expanded 16 KB UMMA byte blocks (only when A_BITS is off)."""
+        """Pre-expanded 16 KB UMMA byte blocks."""
         if self._bytes is None:
             self._bytes = torch.empty((max(self.nblocks, 1), 16384), dtype=torch.uint8, device=self.packed.device)
             self.refresh()
@@ -189,7 +167,7 @@ class BlockedAdjacency:
 
     def operand(self) -> tuple:
         """(device pointer, a_bits) of the left operand the tiled GEMM reads."""
-        return (self.packed.data_ptr(), 1) if A_BITS else (self.bytes.data_ptr(), 0)
+        return (self.bytes.data_ptr(), 0)
 
     def refresh(self):
         """Re-gather + re-expand the blocks (and degrees) from the adjacency's current
@@ -333,15 +311,6 @@ def sm_count() -> int:
     return torch.cuda.get_device_properties(N.device()).multi_processor_count
 
 
-def choose_bn_fused(npad: int, row_blocks_total: int, cap: int) -> int:
-    """Persistent epoch kernel: at most ``cap`` (= SMs) tiles per stage, so every CTA
-    owns <= 1 tile per stage; the smallest N tile that keeps that maximises parallelism."""
-    bn = min(256, npad)
-    while bn > 32 and row_blocks_total * (npad // (bn // 2)) <= cap:
-        bn //= 2
-    return bn
-
-
 BN_MAX = int(os.environ.get("QG_BN_MAX", "256"))      # tuning experiments
 
 
@@ -361,7 +330,7 @@ def use_pair(b_npad: int, row_blocks_total: int, sizes, mode: int) -> bool:
     descriptors).  The fused-epilogue engine stages stay on single-CTA tiles: measured
     slower in pairs (C4 8.3 vs 7.4 ms/epoch, C3 0.34 vs 0.29 ms; the pair's tile is
     epilogue-bound and 2 CTAs/SM already overlap epilogue with main loop)."""
-    return (PAIR and mode == N.GEMM_I32 and sizes is not None and EPOCH is None and b_npad >= 64
+    return (PAIR and mode == N.GEMM_I32 and sizes is not None and b_npad >= 64
             and row_blocks_total * max(1, b_npad // 256) >= 2 * sm_count())
 
 
@@ -373,21 +342,16 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     rbs = [-(-s.m // TILE) for s in segs]
     pair = chain is None and use_pair(b_npad, sum(rbs), sizes, mode) and not a_bits
     if chain is not None:
-        if b_npad > 256 or a_bits or EPOCH is not None or (chain.split and b_npad < 64):
-            raise ValueError("chained stage needs one N tile <= 256 (two >= 32 when split), byte blocks, "
-                             "per-stage launches")
-        bn = b_npad // 2 if chain.split else b_npad
+        if b_npad > 256 or a_bits:
+            raise ValueError("chained stage needs one N tile <= 256 and byte blocks")
+        bn = b_npad
     elif pair:
         bn = max(64, min(256, b_npad))
     else:
-        bn = (choose_bn(b_npad, sum(rbs)) if EPOCH is None or DATAFLOW
-              else choose_bn_fused(b_npad, sum(rbs), sm_count()))
+        bn = choose_bn(b_npad, sum(rbs))
     n_tiles = b_npad // bn
     begin = 0
-    rb_base = 0
     for s, r in zip(segs, rbs):
-        s.rb_base = rb_base                          # dataflow epoch counters (same in every stage)
-        rb_base += r
         s.cta_begin = begin
         begin += (-(-r // 2) if pair else r) * n_tiles
     if pair:
@@ -415,11 +379,6 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     if a_blocks and PENDING_JOIN is not None:
         torch.cuda.current_stream().wait_event(PENDING_JOIN)
         PENDING_JOIN = None
-    if EPOCH is not None:
-        # deferred: flush_epoch() launches every recorded stage in ONE persistent kernel
-        EPOCH.append((args, work, table))
-        keep.append(args)
-        return
     global LAUNCHES
     LAUNCHES += 1
     from . import bitgemm
@@ -521,53 +480,13 @@ def entry_tiles(stacks, side: str, want_row_sums: bool, keep: list):
         begin += units if rows * cols else 0
         segs.append(seg)
         outs.append((tiles, pitch, rs))
-        keep.extend([tiles, rs])          # read later by a deferred (fused-epoch) launch
+        keep.extend([tiles, rs])
     if begin:
         table = SegTable(segs, EntrySeg)
         keep.append(table)
         N.check(N.lib().qg_entry_tiles(table.dev.data_ptr(), len(segs), stacks[0].bits, int(right), begin,
                                        N.stream()), "qg_entry_tiles")
     return outs
-
-
-def _segs_of(table):
-    """Host copies of a SegTable's segments."""
-    return table.segs
-
-
-def flush_epoch(stages: list, keep: list) -> None:
-    """Launch recorded stages as persistent epoch kernels (<= MAX_EPOCH_STAGES per launch):
-    one cooperative grid, a grid barrier between stages (include/qgtc_b200.h qg_tiled_epoch)."""
-    from . import bitgemm
-    for i in range(0, len(stages), MAX_EPOCH_STAGES):
-        chunk = stages[i:i + MAX_EPOCH_STAGES]
-        arr = (TiledArgs * len(chunk))(*[c[0] for c in chunk])
-        if DATAFLOW:
-            # per stage, one completion counter per 128-row block (zeroed per epoch)
-            nrb = max(1, max(sum(-(-sg.m // TILE) for sg in _segs_of(c[2])) for c in chunk))
-            ready = N.alloc((len(chunk), nrb), torch.int32, "volatile")
-            keep.append(ready)
-            for j, a in enumerate(arr):
-                a.ready_cur = ready[j].data_ptr()
-                if j > 0:
-                    a.ready_prev, a.expect_prev = ready[j - 1].data_ptr(), arr[j - 1].n_tiles
-        bar = N.alloc(1 + MAX_EPOCH_STAGES, torch.int32, "empty")   # zeroed by the call (memset node)
-        keep.extend([arr, bar])
-        if bitgemm.PHASE_HOOK is not None:
-            for a, (_, work, _) in zip(arr, chunk):
-                stamps = torch.zeros((a.total_ctas, 8), dtype=torch.int64, device=N.device())
-                a.phase_ns = stamps.data_ptr()
-                bitgemm.PHASE_HOOK.append((stamps, work))
-        if os.environ.get("QG_DEBUG_EPOCH"):
-            for a, (_, _, table) in zip(arr, chunk):
-                raw = table.dev.cpu().numpy().tobytes()
-                segs = (TSeg * a.nsegs).from_buffer_copy(raw)
-                print("  py stage segs=%x nsegs=%d total=%d bn=%d | seg0 a=%x b=%x m=%d r128=%d cta_begin=%d k=%d"
-                      % (a.segs, a.nsegs, a.total_ctas, a.bn, segs[0].a or 0, segs[0].b or 0, segs[0].m, segs[0].r128,
-                         segs[0].cta_begin, segs[0].k_tiles), flush=True)
-        global LAUNCHES
-        LAUNCHES += 1
-        N.check(_lib().qg_tiled_epoch(arr, len(chunk), bar.data_ptr(), N.stream()), "qg_tiled_epoch")
 
 
 # ------------------------------------------------- grouped block expansion
@@ -596,7 +515,7 @@ class GroupedRefresh:
         for b in self.blks:
             seg = BlockSeg()
             seg.packed, seg.blk_rb = b.packed.data_ptr(), b.blk_rb.data_ptr()
-            seg.bytes = None if A_BITS else b.bytes.data_ptr()
+            seg.bytes = b.bytes.data_ptr()
             seg.degrees, seg.rows, seg.block_begin = b.degrees.data_ptr(), b.m, begin
             begin += b.nblocks
             segs.append(seg)

@@ -6,7 +6,7 @@ import types
 
 import pytest
 
-from paper_2111_09547_b200 import engine, synth, tiled
+from paper_2111_09547_b200 import engine, synth
 
 
 def _run(**kw):
@@ -19,10 +19,10 @@ def _row_blocks(cfg):
 
 @pytest.fixture(autouse=True)
 def _defaults():
-    saved = (engine.CHAIN, engine.CHAIN_SPLIT, engine.SCREEN, tiled.A_BITS, tiled.EPOCH)
-    engine.CHAIN, engine.CHAIN_SPLIT, engine.SCREEN, tiled.A_BITS, tiled.EPOCH = True, False, False, False, None
+    saved = engine.CHAIN
+    engine.CHAIN = True
     yield
-    engine.CHAIN, engine.CHAIN_SPLIT, engine.SCREEN, tiled.A_BITS, tiled.EPOCH = saved
+    engine.CHAIN = saved
 
 
 def test_benchmark_configs_chain_as_measured():
@@ -37,9 +37,8 @@ def test_benchmark_configs_chain_as_measured():
     assert engine._chain_ok(_run(), c4.hidden, c4.hidden, _row_blocks(c4)) == 1
 
 
-def test_split_pairs_are_opt_in_and_need_a_two_way_split():
-    engine.CHAIN_SPLIT = True
-    assert engine._chain_ok(_run(), 64, 64, 79) == 2          # npad 64 split into 2 x 32
+def test_split_stages_chain_only_with_few_row_blocks():
+    assert engine._chain_ok(_run(), 64, 64, 79) == 0          # npad 64 split into 2 x 32
     assert engine._chain_ok(_run(), 32, 64, 79) == 1          # 32 columns: already one full-width tile
     assert engine._chain_ok(_run(), 256, 64, 50) == 0         # 4-way split, too many row blocks
     assert engine._chain_ok(_run(), 256, 64, 30) == 1         # 4-way split, few row blocks
@@ -50,7 +49,5 @@ def test_chain_is_off_whenever_its_preconditions_fail():
     assert engine._chain_ok(_run(tally=object()), 128, 64, 500) == 0  # tallies need the codes
     assert engine._chain_ok(_run(), 300, 64, 500) == 0               # stage-1 wider than one tile
     assert engine._chain_ok(_run(), 128, 300, 500) == 0              # stage-2 wider than one tile
-    engine.SCREEN = True
-    assert engine._chain_ok(_run(), 128, 64, 500) == 0
-    engine.SCREEN, engine.CHAIN = False, False
+    engine.CHAIN = False
     assert engine._chain_ok(_run(), 128, 64, 500) == 0

@@ -199,59 +199,6 @@ def test_bmm_reduced_equals_reduced_per_plane_bmm(bits):
     np.testing.assert_array_equal(got, dense.astype(np.int64) @ x.astype(np.int64))
 
 
-def _forward_screen(batches, model, screen: bool):
-    from paper_2111_09547_b200 import engine
-    old = engine.SCREEN
-    engine.SCREEN = screen
-    try:
-        return [o.cpu().numpy() for o in engine.model_forward_group(batches, model)]
-    finally:
-        engine.SCREEN = old
-
-
-@pytest.mark.parametrize("kind,bits", [("gin", 4), ("gin", 8), ("gcn", 4), ("gcn", 2)])
-def test_requant_screen_is_bit_identical_on_boundaries(kind, bits):
-    """Integer weights on unit-scale grids make every hidden pre-activation an exact
-    integer, i.e. every requant quotient sits ON a code boundary: the screen must send
-    all of them to the exact path.  Screen on == screen off == CPU oracle."""
-    from paper_2111_09547_b200 import engine
-    cfg = synth.GraphConfig("boundary", kind, 700, 6000, 4, 4, 40, 24, 7, 3, bits, bits)
-    batches, feats, xp = synth.planted_batches(cfg, seed=3)
-    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=3)
-    rng = np.random.default_rng(bits)
-    for ly in model.layers:
-        ly.weight = rng.integers(0, 1 << bits, ly.weight.shape).astype(np.float64)
-        ly.weight_params = bg.QuantParams(0.0, float(1 << bits), bits)      # scale 1: codes == weights
-        if ly.bias is not None:
-            ly.bias = rng.integers(-3, 4, ly.bias.shape).astype(np.float64)
-        for name in ("mid_params", "out_params"):
-            if getattr(ly, name) is not None:
-                setattr(ly, name, bg.QuantParams(0.0, float(1 << bits), bits))
-    model._prepared = None
-    on = _forward_screen(batches, model, True)
-    off = _forward_screen(batches, model, False)
-    b = batches[0]
-    a = b.adjacency
-    codes = O.quantize_codes(feats[0], xp.alpha_min, xp.alpha_max, xp.bits)
-    want = O.model_forward(a.words, a.dims(), codes, xp, model.layers)
-    np.testing.assert_array_equal(off[0], want)
-    np.testing.assert_array_equal(on[0], want)
-
-
-@pytest.mark.parametrize("name,bits", [("C2", 4), ("C2", 8), ("C3", 4), ("C1", 2)])
-def test_requant_screen_is_bit_identical_on_configs(name, bits):
-    """Calibrated (real-valued) grids at config shapes: screen on == screen off (the screen is
-    an opt-in path, QG_SCREEN=1; it must stay bit-exact)."""
-    cfg = synth.with_bits(synth.CONFIGS[name], bits)
-    ids = [0, 1, 2] if name == "C3" else None
-    batches, feats, _ = synth.planted_batches(cfg, seed=5, **({"batch_ids": ids} if ids else {}))
-    model = synth.calibrated_model(cfg, batches[0], feats[0], seed=5)
-    on = _forward_screen(batches, model, True)
-    off = _forward_screen(batches, model, False)
-    for x, y in zip(on, off):
-        np.testing.assert_array_equal(x, y)
-
-
 @pytest.mark.parametrize("pair", [True, False])
 def test_bmm_reduced_pair_path_large(pair):
     """The 2-SM (cta_group::2, TMA-signalled) pair path of bmm_reduced at a size that

@@ -185,8 +185,9 @@ def test_tiled_chain_argument_validation_needs_no_gpu():
     assert call(c_n=65) == N.QG_ERR_ARG                       # more columns than w_npad
     assert call(c_out_layout=1) == N.QG_ERR_ARG               # stage 2 writes right tiles or fp64
     assert call(c_out_layout=0) == N.QG_ERR_ARG               # fp64 output needs an OUT_REAL epilogue
-    assert call(n_tiles=2, b_npad=128) == N.QG_ERR_UNSUPPORTED  # one N tile unless split
-    assert call(c_split=1) == N.QG_ERR_UNSUPPORTED            # split needs n_tiles == 2
+    assert call(n_tiles=2, b_npad=128) == N.QG_ERR_UNSUPPORTED  # stage 1 is one N tile
+    assert call(c_reserved=1) == N.QG_ERR_UNSUPPORTED         # reserved field (removed split chain)
+    assert call(reserved3=1) == N.QG_ERR_UNSUPPORTED          # reserved field (removed dataflow epoch)
     assert call(mode=N.GEMM_I32) == N.QG_ERR_UNSUPPORTED      # stage 1 must requantize
     mean = (ctypes.c_double * 1)(0.0)
     epi2.bn_mean = ctypes.cast(mean, ctypes.c_void_p)         # BN without its other vectors
