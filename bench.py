@@ -575,6 +575,13 @@ def ours(args, world, rank):
         torch.cuda.empty_cache()
         extras["c2_sweep_ms_per_epoch_by_bits"] = c2_sweep(max(20, args.steps))
         extras["gemm_roofline_c5"] = c5_point(args.c5_n, 4, peak)
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from bitqnt_bench import run_bitqnt
+        hbm, hbm_src = hbm_peak_gbs()
+        extras["bitqnt_roofline"] = {
+            "bound": "hbm", "unit": "GB/s", "peak_source": hbm_src,
+            "work": "4*M*K fp32 in + s*Mpad*Kpad/8 plane bytes out + 8*M row-sum bytes per launch",
+            "C3": run_bitqnt(169343, 128, 4, hbm_peak=hbm), "C4": run_bitqnt(2449029, 100, 8, hbm_peak=hbm)}
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_one_core(cfg, model, logits_b0)
 

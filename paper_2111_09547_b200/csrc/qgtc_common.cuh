@@ -105,6 +105,22 @@ __device__ __forceinline__ R12 quantize_code_r12(double x, double amin, double i
   return o;
 }
 
+// Same decode with the tight near-integer test: flag only when the 40-bit fraction
+// (top 8 bits in hi, 32 in lo) is within one unit of an integer.  Inputs that are
+// exactly representable at low precision (fp32 features: x * 2^k has a short
+// fraction, so lo == 0 for almost every element) would trip the coarse lo-only test
+// of quantize_code_r12 on nearly every element.
+__device__ __forceinline__ R12 quantize_code_r12_tight(double x, double amin, double inv_scale, uint32_t maxv) {
+  const double r = __dadd_rn(__dmul_rn(__dsub_rn(x, amin), inv_scale), 0x1p12);
+  const uint32_t hi = (uint32_t)__double2hiint(r), lo = (uint32_t)__double2loint(r);
+  const int kc = (int)(hi >> 8) - 0x40B000;
+  const uint32_t f8 = hi & 0xFFu;
+  R12 o;
+  o.code = (uint32_t)min(max(kc, 0), (int)maxv);
+  o.flag = (hi >= 0x40C00000u) | (((f8 == 0u) & (lo <= 1u)) & (hi != 0x40B00000u)) | ((f8 == 0xFFu) & (lo == ~0u));
+  return o;
+}
+
 // Reference formulation (tests): floor of the IEEE quotient, clamped.
 __device__ __forceinline__ uint32_t quantize_code_ref(double x, double amin, double scale, uint32_t maxv) {
   const double v = floor(__ddiv_rn(__dsub_rn(x, amin), scale));

@@ -70,93 +70,99 @@ __global__ void __launch_bounds__(256) quantize_pack_col_kernel(
   }
 }
 
-// Row-wise, vectorised (the feature path, bitpack.py:181-191 + quantize.py:93-105).
-// CTA = 8 warps over a tile of 8 row groups (256 rows) x 128 columns.  Lane l owns
-// columns 4l..4l+3 of the tile: one 16-byte (fp32) / 2x16-byte (fp64) / 4-byte (u8)
-// load per row, so every warp row is a full 512 B (fp32) coalesced segment.  The
-// quantize is the exact division-free form (quantize_code_fast: RN(1/scale) product,
-// IEEE fallback only within 2^-40 of a code boundary).  Bits accumulate in registers
-// (word[p][j] bit i = plane p of row 32v+i, column 4l+j); the row sums come from one
-// redux.sync per row, kept by lane i and written once per (row, column tile).  The
-// plane words are staged in shared memory so the stores run along the row-group index
-// (8 consecutive words = 32 B per (plane, column)) instead of striding by the column
-// pitch.
+// Row-wise bit_qnt (the feature path, bitpack.py:181-191 + quantize.py:93-105).
+// CTA = 8 warps over a tile of 8 row groups (256 rows) x 32 columns.  Warp w owns row
+// group v0 + w, lane = column: every row step is one fully coalesced 128-byte warp load
+// (fp32), 8 rows are loaded ahead (independent loads in flight).  Requant: the exact
+// division-free form (quantize_code_r12_tight; IEEE fallback only within 2^-40 of a
+// code boundary).  The 8 codes of a column's 8-row step go into the bytes of a u64 and
+// one 8x8 bit transpose (transpose8x8) turns them into the 8 plane bytes of that step,
+// so the plane words (bit i = row 32v + i) are built in registers with no cross-lane
+// traffic.  Row sums: one redux.sync per row.  Plane words are staged in shared memory
+// so each (plane, column) is stored as 8 consecutive words (32 B) along the row-group
+// index instead of 4-byte stores one column pitch apart.
+// exact requant of one flagged element (+ the DataError position), kept out of line
 template <typename SrcT>
-__device__ __forceinline__ void load4(const SrcT* __restrict__ src, int64_t r, int64_t c, int64_t ld, int64_t cols,
-                                      bool vec, double (&x)[4]) {
-  const SrcT* p = src + r * ld + c;
-  if (vec && c + 3 < cols) {
-    if constexpr (sizeof(SrcT) == 4) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-    } else if constexpr (sizeof(SrcT) == 8) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-      x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
-    } else {
-      const uchar4 v = *reinterpret_cast<const uchar4*>(p);
-      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-    }
+static __device__ __noinline__ uint32_t requant_slow(SrcT x, double amin, double scale, double inv, uint32_t maxv,
+                                                     int64_t* status, int64_t flat) {
+  if constexpr (sizeof(SrcT) == 1) {
+    status_min(status, flat);
+    return (uint32_t)x & maxv;
   } else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) x[j] = c + j < cols ? (double)p[j] : 0.0;
+    const double xd = (double)x;
+    if (!isfinite(xd)) status_min(status, flat);
+    return quantize_code_fast(xd, amin, scale, inv, maxv);
   }
 }
 
-constexpr int kRowTileCols = 128, kRowTileGroups = 8, kRowStride = 132;
+constexpr int kRowTileCols = 32, kRowTileGroups = 8;
 
 template <typename SrcT, int BITS>
-__global__ void __launch_bounds__(256) quantize_pack_row_vec_kernel(
+__global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
     const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale, double inv,
     int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
-    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base, int vec, int single_tile) {
-  __shared__ __align__(16) uint32_t sw[BITS][kRowTileGroups][kRowStride];
+    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base, int single_tile) {
+  __shared__ uint32_t sw[BITS][kRowTileCols][kRowTileGroups + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wpc = prows >> 5;                          // words per column (row groups)
   const int64_t v0 = (int64_t)blockIdx.x * kRowTileGroups, v = v0 + warp;
-  const int64_t c0 = (int64_t)blockIdx.y * kRowTileCols, c = c0 + 4 * lane;
+  const int64_t c = (int64_t)blockIdx.y * kRowTileCols + lane;
+  const bool cok = c < cols;
   const uint32_t maxv = (1u << BITS) - 1u;
-  uint32_t word[BITS][4];
+  uint32_t word[BITS];
 #pragma unroll
-  for (int p = 0; p < BITS; ++p)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) word[p][j] = 0u;
+  for (int p = 0; p < BITS; ++p) word[p] = 0u;
   uint32_t my_sum = 0;                                     // lane i: row 32v + i
   if (v < wpc) {
-    for (int i = 0; i < 32; ++i) {
-      const int64_t r = v * 32 + i;
-      if (r >= rows) break;                                // warp-uniform
-      uint32_t q[4] = {0u, 0u, 0u, 0u};
-      if (c < cols) {
-        double x[4];
-        load4<SrcT>(src, r, c, ld, cols, vec != 0, x);
+    const int64_t rbase = v * 32;
+    const SrcT* colp = src + rbase * ld + c;
+    for (int i0 = 0; i0 < 32; i0 += 8) {
+      const int64_t left = rows - (rbase + i0);
+      const int nk = left <= 0 ? 0 : (left < 8 ? (int)left : 8);   // valid rows of this step
+      const SrcT* p0 = colp + (int64_t)i0 * ld;
+      SrcT x[8];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (c + j >= cols) continue;
-          if constexpr (sizeof(SrcT) == 1) {
-            uint32_t t = (uint32_t)x[j];
-            if (t > maxv) { status_min(status, status_base + r * cols + c + j); t &= maxv; }
-            q[j] = t;
-          } else {
-            if (!isfinite(x[j])) status_min(status, status_base + r * cols + c + j);
-            q[j] = quantize_code_fast(x[j], amin, scale, inv, maxv);
-          }
-        }
-        if (codes) {
-          if (vec && c + 3 < cols && (cols & 3) == 0)
-            *reinterpret_cast<uchar4*>(codes + r * cols + c) = make_uchar4(q[0], q[1], q[2], q[3]);
-          else
+      for (int k = 0; k < 8; ++k) x[k] = (cok && k < nk) ? p0[(int64_t)k * ld] : SrcT(0);
+      uint32_t q[8];
+      uint32_t fm = 0u;                                   // elements needing the exact path
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (c + j < cols) codes[r * cols + c + j] = (uint8_t)q[j];
+      for (int k = 0; k < 8; ++k) {
+        if constexpr (sizeof(SrcT) == 1) {
+          q[k] = (uint32_t)x[k];
+          fm |= (uint32_t)(q[k] > maxv) << k;
+        } else {
+          const R12 rq = quantize_code_r12_tight((double)x[k], amin, inv, maxv);
+          q[k] = rq.code;
+          fm |= (uint32_t)rq.flag << k;
         }
       }
+      if (fm && cok) {
+        // rare: near-boundary / out-of-range / non-finite elements (out of line)
 #pragma unroll
-      for (int p = 0; p < BITS; ++p)
+        for (int k = 0; k < 8; ++k)
+          if (((fm >> k) & 1u) && k < nk)
+            q[k] = requant_slow<SrcT>(x[k], amin, scale, inv, maxv, status,
+                                      status_base + (rbase + i0 + k) * cols + c);
+      }
+      uint32_t lo = 0u, hi = 0u;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) word[p][j] |= ((q[j] >> p) & 1u) << i;
-      const uint32_t s = __reduce_add_sync(QG_FULL, (q[0] + q[1]) + (q[2] + q[3]));
-      if (lane == i) my_sum = s;
+      for (int k = 0; k < 8; ++k) {
+        if (!(cok && k < nk)) q[k] = 0u;
+        if (k < 4) lo |= q[k] << (8 * k);
+        else hi |= q[k] << (8 * (k - 4));
+        const uint32_t sum = __reduce_add_sync(QG_FULL, q[k]);
+        if (lane == i0 + k) my_sum = sum;
+      }
+      if (codes && cok) {
+        uint8_t* cp = codes + (rbase + i0) * cols + c;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < nk) cp[(int64_t)k * cols] = (uint8_t)q[k];
+      }
+      // byte p of t = plane p of the 8 rows (bit k = row i0 + k)
+      const uint64_t t = transpose8x8(((uint64_t)hi << 32) | lo);
+#pragma unroll
+      for (int p = 0; p < BITS; ++p) word[p] |= (uint32_t)((t >> (8 * p)) & 0xFFu) << i0;
     }
     if (row_sums) {
       const int64_t r = v * 32 + lane;
@@ -167,15 +173,14 @@ __global__ void __launch_bounds__(256) quantize_pack_row_vec_kernel(
     }
   }
 #pragma unroll
-  for (int p = 0; p < BITS; ++p)
-    *reinterpret_cast<uint4*>(&sw[p][warp][4 * lane]) = make_uint4(word[p][0], word[p][1], word[p][2], word[p][3]);
+  for (int p = 0; p < BITS; ++p) sw[p][lane][warp] = word[p];
   __syncthreads();
   // plane p, column c0 + cc, row group v0 + w: word p * wpp + (c0 + cc) * wpc + v0 + w
-  const int64_t wpp = pcols * wpc;
+  const int64_t wpp = pcols * wpc, c0 = (int64_t)blockIdx.y * kRowTileCols;
   for (int idx = threadIdx.x; idx < BITS * kRowTileCols * kRowTileGroups; idx += blockDim.x) {
-    const int w = idx & 7, cc = (idx >> 3) & 127, p = idx >> 10;
+    const int w = idx & 7, cc = (idx >> 3) & 31, p = idx >> 8;
     const int64_t col = c0 + cc, vg = v0 + w;
-    if (col < pcols && vg < wpc) planes[p * wpp + col * wpc + vg] = sw[p][w][cc];
+    if (col < pcols && vg < wpc) planes[p * wpp + col * wpc + vg] = sw[p][cc][w];
   }
 }
 
@@ -212,14 +217,11 @@ int launch_quantize_pack(const SrcT* src, int64_t rows, int64_t cols, int64_t ld
       quantize_pack_col_kernel<SrcT, BITS><<<(unsigned)blocks, 256, 0, st>>>(
           src, rows, cols, ld, amin, scale, prows, pcols, planes, codes, row_sums, status, status_base);
     else {
-      // vectorised loads need an aligned base and a row pitch of whole vectors
-      const size_t vb = sizeof(SrcT) == 1 ? 4 : 16;
-      const int vec = (reinterpret_cast<uintptr_t>(src) % vb == 0) && ((ld * (int64_t)sizeof(SrcT)) % (int64_t)vb == 0);
       const dim3 grid((unsigned)(((prows >> 5) + kRowTileGroups - 1) / kRowTileGroups),
                       (unsigned)((pcols + kRowTileCols - 1) / kRowTileCols));
       quantize_pack_row_vec_kernel<SrcT, BITS><<<grid, 256, 0, st>>>(
           src, rows, cols, ld, amin, scale, 1.0 / scale, prows, pcols, planes, codes, row_sums, status, status_base,
-          vec, (int)(grid.y == 1));
+          (int)(grid.y == 1));
     }
   }
   if (col_sums && cols > 0 && rows > 0)
