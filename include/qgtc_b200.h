@@ -174,8 +174,10 @@ typedef struct {
   int64_t q_codes_ld;
   int32_t q_codes_colmajor;
   int32_t q_skip_planes;       /* 1: write only the code cache (planes built lazily) */
-  double reserved_d0;          /* reserved, 0 (round-1 affine requant screen, removed) */
-  double reserved_d1;
+  double screen_rmax;          /* tiled fast path: max code of the RIGHT operand (2^bits - 1)
+                                  enables the fp32 requant screen (0 = exact fp64 path for
+                                  every element); per-row acc bound = row_sums[r] * this   */
+  double reserved_d1;          /* reserved, 0                                          */
 } qg_epilogue;
 
 /*

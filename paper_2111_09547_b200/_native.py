@@ -55,7 +55,7 @@ class Epilogue(ctypes.Structure):
         ("q_prows", _i64), ("q_pcols", _i64),
         ("out_real", _vp), ("q_planes", _vp), ("q_row_sums", _vp), ("status", _vp),
         ("q_codes", _vp), ("q_codes_ld", _i64), ("q_codes_colmajor", ctypes.c_int32),
-        ("q_skip_planes", ctypes.c_int32), ("reserved_d0", _f64), ("reserved_d1", _f64),
+        ("q_skip_planes", ctypes.c_int32), ("screen_rmax", _f64), ("reserved_d1", _f64),
     ]
 
 

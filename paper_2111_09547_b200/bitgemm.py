@@ -14,6 +14,12 @@ the reference, bitgemm.py:10-16):
   (planes stacked along N, or recomposed into codes); ``CROSS_BIT`` re-expands
   it per plane (one plane per CTA).
 
+These variants apply to ``bmm_1bit_by_nbit`` (and the engine's aggregation
+stages).  ``gemm_sbit_by_tbit`` runs one kernel for every knob setting: its
+dense s-bit left operand has no zero-tile schedule worth running and its
+planes are recomposed into codes once, so ``jump`` / ``reuse`` select only the
+reference op counters it reports.
+
 Op counters are the reference's closed forms (bitgemm.py:335-370, 409-461)
 over the 8x128 tile flags, computed lazily on the device when read.
 """
@@ -276,6 +282,17 @@ def apply_epilogue(acc, epi: EpilogueSpec, *, out_orientation: str = ROW_WISE, o
     if t.dim() != 2:
         raise ValueError("accumulator must be 2-D")
     rows, cols = t.shape
+    if t.dtype != torch.int32 and t.numel():
+        # the kernel reads int32 accumulators: refuse values that would not survive the
+        # narrowing (the reference dequantizes acc.astype(float64), bitgemm.py:156-160)
+        lo, hi = torch.iinfo(torch.int32).min, torch.iinfo(torch.int32).max
+        if t.is_floating_point():
+            bad = ~torch.isfinite(t) | (t != torch.trunc(t)) | (t < lo) | (t > hi)
+        else:
+            bad = (t < lo) | (t > hi)
+        if bool(bad.any()):
+            raise ReductionOverflowError("accumulator values must be integers that fit int32 "
+                                         "(the device epilogue reads int32 accumulators)")
     plan = _build_epilogue(epi, rows, cols, out_orientation=out_orientation, out_pad_to=out_pad_to,
                            dev=t.device)
     t32 = t.to(torch.int32).contiguous()

@@ -28,6 +28,7 @@ namespace qg {
 
 struct TiledParams {
   alignas(64) CUtensorMap zero_map;   // pair mode: 16 KB zero block (rows of 128 B)
+  alignas(64) CUtensorMap w2_map;     // chained pair mode: stage-2 weights, boxes of bn2/2 rows of 128 B
   const qg_tseg* segs;
   int32_t nsegs;
   int32_t a_blocks;         // 1: left operand = adjacency blocks (schedule), 0: dense left slabs
@@ -43,6 +44,7 @@ struct TiledParams {
   int32_t pair;             // 1: CTA pairs (cluster of 2) run cta_group::2 MMAs, M = 256
   int32_t pair_swizzle;     // pair kernels: row-block pairs per N-major group (1 = plain order)
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
+  int32_t screen;           // fp32 requant screen enabled (QG_NO_SCREEN=1 disables)
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
   int32_t chain, bn2, k2, out_layout2;
@@ -74,6 +76,118 @@ static __device__ __noinline__ uint32_t requant_exact(double x, double amin, dou
   return quantize_code_fast(x, amin, scale, inv, maxv);
 }
 
+// ---------------------------------------------------------------- fp32 requant screen
+// For epilogues without batch norm the requantized code of an element is
+// clamp(floor(q), 0, maxv), q the reference's fp64 quotient RN(RN(x - amin) / scale) of
+// the dequantized (+bias, ReLU) value x.  In exact arithmetic over the fp64 constants
+// q ~ Y = alpha acc + beta_r + gamma_c (alpha = k_acc / scale > 0, beta_r = (rterm_r -
+// amin) / scale, gamma_c = (C_c + K + B_c) / scale).  beta_r and gamma_c are large and
+// cancel against alpha acc, so the screen shifts in INTEGERS first: acc' = acc - acc0_r -
+// acc0_c (acc0 = rint(-beta / alpha)), converts acc' to fp32 (exact below 2^24, else
+// relative 2^-24) and evaluates y = fma(acc', alpha, delta_r) + delta_c, |delta| <= alpha/2.
+// Then |y - q| <= 2^-24 (4 |Y| + 3 alpha) + 2^-40 < margin = 2^-21 (maxv + 3 + 2 alpha +
+// |q0|) wherever the code is decided (|Y| <= maxv + 2).  ReLU is max(q, q0) with q0 the
+// quotient of x = 0 (monotone, exact); floor(clamp(z, 0.5, maxv + 0.5)) ==
+// clamp(floor(z), 0, maxv).  An element whose clamped estimate lies within the margin
+// of an integer takes the exact fp64 path (per element, divergent; ~2.5e-4 of the
+// elements at 8 bits), so the codes are bit-identical to the reference's.
+struct ScreenRow {
+  bool on;          // screen usable for this tile (else every slice runs the fp64 path)
+  int32_t a0r;      // acc0_r
+  float dr;         // delta_r
+  float alpha;
+  float mrg;        // margin; -1: invalid row (never exact), +inf: always exact
+  float lo, hi;     // clamp bounds: max(q0, 0.5) (ReLU) or 0.5; maxv + 0.5
+  const int32_t* sA0;  // per column acc0_c (row-only stages: unused)
+  const float* sD;     // per column delta_c
+};
+
+// doubles of per-column constants one stage stages in shared memory: the fp64 terms
+// (C, B [, BN x5]) + the screen's acc0_c / delta_c; none for a row-only stage
+__host__ __device__ __forceinline__ int col_doubles(int bn, bool row_only, bool has_bn) {
+  if (row_only && !has_bn) return 0;
+  return has_bn ? 7 * bn : 3 * bn;
+}
+__device__ __forceinline__ bool epi_row_only(const qg_epilogue& E) { return !E.use_col && !E.use_const && !E.bias; }
+
+// per-column screen constants (staging warps; stages without batch norm); a column whose
+// shift does not fit turns the stage's screen off (*off)
+__device__ __forceinline__ void screen_col(const qg_epilogue& E, int i, double C, double B, int32_t* sA0, float* sD,
+                                           int* off) {
+  const double alpha = E.k_acc / E.q_scale;
+  const double K = E.use_const ? E.k_const : 0.0;
+  const double gam = ((C + K) + B) / E.q_scale;
+  const double a0 = rint(-gam / alpha);
+  if (!(fabs(a0) <= 0x1p29)) {
+    *off = 1;
+    sA0[i] = 0;
+    sD[i] = 0.0f;
+    return;
+  }
+  sA0[i] = (int32_t)a0;
+  sD[i] = (float)(gam + a0 * alpha);
+}
+
+// 8 codes of one slice through the screen; returns the mask of elements that need the
+// exact path
+template <bool PERCOL>
+__device__ __forceinline__ uint32_t screen8(const ScreenRow& S, const uint32_t (&v)[8], int cl8, uint32_t (&q)[8]) {
+  int32_t a0[8];
+  float dc[8];
+  if (PERCOL) {
+#pragma unroll
+    for (int j = 0; j < 8; j += 4) {
+      const int4 x = *reinterpret_cast<const int4*>(S.sA0 + cl8 + j);
+      const float4 z = *reinterpret_cast<const float4*>(S.sD + cl8 + j);
+      a0[j] = x.x; a0[j + 1] = x.y; a0[j + 2] = x.z; a0[j + 3] = x.w;
+      dc[j] = z.x; dc[j + 1] = z.y; dc[j + 2] = z.z; dc[j + 3] = z.w;
+    }
+  }
+  uint32_t bad = 0;
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    int32_t sh = (int32_t)v[jj] - S.a0r;
+    if (PERCOL) sh -= a0[jj];
+    float y = fmaf((float)sh, S.alpha, S.dr);
+    if (PERCOL) y += dc[jj];
+    y = fminf(fmaxf(y, S.lo), S.hi);
+    const float t = __fadd_rd(y, 12582912.0f);                        // 1.5 * 2^23 + floor(y)
+    const float r = __fsub_rn(__fadd_rn(y, 12582912.0f), 12582912.0f);   // round-to-nearest(y)
+    bad |= (fabsf(y - r) > S.mrg ? 0u : 1u) << jj;
+    q[jj] = __float_as_uint(t) & 0xFFu;
+  }
+  return bad;
+}
+
+// Per-column epilogue constants of one stage into shared memory (col_doubles layout):
+// C = RN(k_col * col_sum), B = bias [, BN mean / denom / gamma / beta / inv_denom], and the
+// screen's acc0_c / delta_c.  Columns n0 + i for i = t, t + nt, ... < bn.
+__device__ __forceinline__ void stage_cols(const qg_epilogue& E, double* sC, int bn, int64_t n0, int64_t n, int t,
+                                           int nt, int* off) {
+  if (!col_doubles(bn, epi_row_only(E), E.bn_mean != nullptr)) return;
+  for (int i = t; i < bn; i += nt) {
+    const int64_t c = n0 + i;
+    const bool ok = c < n;
+    // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
+    // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
+    // evaluates the reference's grouping without per-element branches
+    const double cC = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
+    const double cB = (ok && E.bias) ? E.bias[c] : 0.0;
+    sC[0 * bn + i] = cC;
+    sC[1 * bn + i] = cB;
+    if (E.bn_mean) {
+      sC[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
+      sC[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
+      sC[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
+      sC[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
+      sC[6 * bn + i] = ok ? E.bn_inv_denom[c] : 1.0;
+    } else {
+      screen_col(E, i, cC, cB, reinterpret_cast<int32_t*>(sC + 2 * bn), reinterpret_cast<float*>(sC + 2 * bn) + bn,
+                 off);
+    }
+  }
+}
+
 // Per-thread epilogue context: this lane owns one accumulator row (TMEM lane) and
 // walks 8-column slices first, first+2, ...
 struct EpiLane {
@@ -102,10 +216,28 @@ struct EpiLane {
 // Returns this lane's requantized code sum (packed output) for the row sums.
 // ST: 0 = this stage to global memory; 1 = chained stage 1, codes into the shared
 // memory operand of stage 2 (mid[k tile]); 2 = chained stage 2 (P.epi2, bn2, n2).
+// The exact fp64 requant of ONE element (no batch norm): the screen's rare fallback.
+struct ExactArgs {
+  double k_acc, kconst, q_amin, q_scale, q_inv;
+  uint32_t maxv;
+};
+template <int ACT, bool ROW_ONLY>
+static __device__ __noinline__ uint32_t exact_code(const ExactArgs A, const double* sC, const double* sB, int cl,
+                                                   uint32_t acc, double rterm, int64_t* status, int64_t flat) {
+  double x = __dadd_rn(__dmul_rn(A.k_acc, (double)(int32_t)acc), rterm);
+  if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), A.kconst), sB[cl]);
+  if (ACT == QG_ACT_RELU) {
+    const int hi = __double2hiint(x), m = ~(hi >> 31);
+    x = __hiloint2double(hi & m, __double2loint(x) & m);
+  }
+  const R12 c = quantize_code_r12(x, A.q_amin, A.q_inv, A.maxv);
+  return c.flag ? requant_exact(x, A.q_amin, A.q_scale, A.q_inv, A.maxv, status, flat) : c.code;
+}
+
 template <int ACT, bool HAS_BN, bool ROW_ONLY, int ST>
 __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
                                                const double* __restrict__ sCol, double rterm, uint8_t* mid0,
-                                               uint8_t* mid1) {
+                                               uint8_t* mid1, const ScreenRow& S) {
   const qg_epilogue& E = ST == 2 ? P.epi2 : P.epi;
   const int bn = ST == 2 ? P.bn2 : P.bn;
   const double* sC = sCol;
@@ -133,6 +265,26 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     const int cl8 = sl * 8;
     uint32_t v[8];
     L.load8(cl8, v);
+    const bool full = L.rvalid && cl8 + 8 <= L.nvalid;
+    uint32_t q[8];
+    bool screened = false;
+    if (ACT != QG_ACT_TANH && !HAS_BN && packed && S.on) {
+      screened = true;
+      uint32_t bad = screen8<!ROW_ONLY>(S, v, cl8, q);
+      if (!full) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (!(L.rvalid && cl8 + jj < L.nvalid)) { q[jj] = 0u; bad &= ~(1u << jj); }
+      }
+      if (bad) {
+        const ExactArgs A{k_acc, kconst, q_amin, q_scale, q_inv, maxv};
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if ((bad >> jj) & 1u)
+            q[jj] = exact_code<ACT, ROW_ONLY>(A, sC, sB, cl8 + jj, v[jj], rterm, status, L.myrow * pn + L.n0 + cl8 + jj);
+      }
+    }
+    if (!screened) {
     double real[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
@@ -165,9 +317,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     }
     // requant: branch-free candidates; one (rare, divergent) exact pass for ragged
     // edges, non-finite values or quotients within 2^-40 of a code boundary
-    const bool full = L.rvalid && cl8 + 8 <= L.nvalid;
     bool slow = !full;
-    uint32_t q[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
       const R12 c = quantize_code_r12(real[jj], q_amin, q_inv, maxv);
@@ -182,6 +332,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
                     ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, status, L.myrow * pn + L.n0 + cl8 + jj)
                     : 0u;
     }
+    }   // !screened
     const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
     const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
     rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
@@ -225,6 +376,7 @@ struct TileRing {
   uint64_t* done;
   unsigned long long* sRowSum;
   double* sRowTerm;
+  int* sOff;                  // [stage 1, stage 2]: a column's screen shift is out of range
   uint32_t tmem;
   int S;
   uint32_t it0;               // ring position (K tiles issued so far)
@@ -287,9 +439,46 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
     // one uniform dispatch per tile: the slice loop below is straight-line per variant
     const double rterm = rvalid ? R.sRowTerm[quad * 32 + lane] : 0.0;
     const bool row_only = !E.use_col && !E.use_const && !E.bias;
+    ScreenRow S;
+    S.on = false;
+    if (packed && P.screen && E.screen_rmax > 0.0 && E.act != QG_ACT_TANH && !E.bn_mean && !R.sOff[ST == 2]) {
+      // per-row acc bound (unsigned codes): left row sum x max right code; the integer
+      // shift acc - acc0_r - acc0_c must not overflow (acc < 2^30, |acc0| <= 2^29)
+      int64_t rs = 0;
+      bool known = true;
+      if (ST == 2) rs = (int64_t)R.sRowSum[quad * 32 + lane];
+      else if (G.row_sums) rs = rvalid ? G.row_sums[myrow] : 0;
+      else known = false;
+      const double accmax = (double)rs * E.screen_rmax;
+      const double alpha = E.k_acc / E.q_scale;
+      const double beta = (rterm - E.q_amin) / E.q_scale;
+      double a0 = rint(-beta / alpha);
+      const bool a0_ok = fabs(a0) <= 0x1p29;
+      if (!a0_ok) a0 = 0.0;
+      S.on = __all_sync(QG_FULL, known && accmax < 0x1p30) && alpha > 0.0 && alpha < 0x1p60;
+      if (S.on) {
+        const uint32_t maxv = (1u << E.q_bits) - 1u;
+        float lo = 0.5f;
+        double q0 = 0.0;
+        if (E.act == QG_ACT_RELU) {
+          // q0: the reference quotient of x = 0 (quantize.py:102-104), exact fp64
+          q0 = __ddiv_rn(__dsub_rn(0.0, E.q_amin), E.q_scale);
+          lo = fmaxf(lo, (float)q0);
+        }
+        const double margin = ((double)maxv + 3.0 + 2.0 * alpha + fabs(q0)) * 0x1p-21;
+        S.mrg = !rvalid ? -1.0f : (a0_ok && margin < 0.25) ? __double2float_ru(margin) : __int_as_float(0x7f800000);
+        S.a0r = (int32_t)a0;
+        S.dr = (float)(beta + a0 * alpha);
+        S.alpha = (float)alpha;
+        S.lo = lo;
+        S.hi = (float)maxv + 0.5f;
+        S.sA0 = reinterpret_cast<const int32_t*>(sCol + 2 * bn);
+        S.sD = reinterpret_cast<const float*>(sCol + 2 * bn) + bn;
+      }
+    }
     switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
 #define QG_EPI_CASE(i, A, B, Rw) \
-  case i: rsum = epi_slices<A, B, Rw, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
+  case i: rsum = epi_slices<A, B, Rw, ST>(P, G, L, sCol, rterm, mid0, mid1, S); break;
       QG_EPI_CASE(0, QG_ACT_NONE, false, false)
       QG_EPI_CASE(1, QG_ACT_NONE, false, true)
       QG_EPI_CASE(2, QG_ACT_NONE, true, false)
@@ -301,7 +490,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
       QG_EPI_CASE(8, QG_ACT_TANH, false, false)
       QG_EPI_CASE(9, QG_ACT_TANH, false, true)
       QG_EPI_CASE(10, QG_ACT_TANH, true, false)
-      default: rsum = epi_slices<QG_ACT_TANH, true, true, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
+      default: rsum = epi_slices<QG_ACT_TANH, true, true, ST>(P, G, L, sCol, rterm, mid0, mid1, S); break;
 #undef QG_EPI_CASE
     }
   }
@@ -348,7 +537,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const bool fused = P.mode == QG_GEMM_EPILOGUE;
   const qg_epilogue& E = P.epi;
   // chained stage 2: per-column constants after stage 1's
-  double* sCol2 = sCol + (E.bn_mean ? 7 : 2) * bn;
+  double* sCol2 = sCol + col_doubles(bn, epi_row_only(E), E.bn_mean != nullptr);
   if (tid < 128) R.sRowSum[tid] = 0ull;
   if (CHAIN && tid < 128) R.sRowSum[128 + tid] = 0ull;
   if (tid == 0) tstamp(P, tile, 1);
@@ -431,39 +620,8 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       const int64_t row = rb * 128 + t;
       R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
     }
-    for (int i = t; i < bn; i += (int)blockDim.x - 64) {
-      const int64_t c = n0 + i;
-      const bool ok = c < P.n;
-      // absent terms are +0.0: x + 0.0 == x bit for bit here (x is never -0: the first
-      // term k_acc*acc is >= +0 and RN sums that cancel give +0), so the dequant below
-      // evaluates the reference's grouping without per-element branches
-      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[c]) : 0.0;
-      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[c] : 0.0;
-      if (E.bn_mean) {
-        sCol[2 * bn + i] = ok ? E.bn_mean[c] : 0.0;
-        sCol[3 * bn + i] = ok ? E.bn_denom[c] : 1.0;
-        sCol[4 * bn + i] = ok ? E.bn_gamma[c] : 0.0;
-        sCol[5 * bn + i] = ok ? E.bn_beta[c] : 0.0;
-        sCol[6 * bn + i] = ok ? E.bn_inv_denom[c] : 1.0;
-      }
-    }
-    if (CHAIN) {
-      const qg_epilogue& E2 = P.epi2;
-      const int bn2 = P.bn2;
-      for (int i = t; i < bn2; i += (int)blockDim.x - 64) {
-        const int64_t c = i;
-        const bool ok = c < P.n2;
-        sCol2[0 * bn2 + i] = (ok && E2.use_col) ? __dmul_rn(E2.k_col, (double)E2.col_sums[c]) : 0.0;
-        sCol2[1 * bn2 + i] = (ok && E2.bias) ? E2.bias[c] : 0.0;
-        if (E2.bn_mean) {
-          sCol2[2 * bn2 + i] = ok ? E2.bn_mean[c] : 0.0;
-          sCol2[3 * bn2 + i] = ok ? E2.bn_denom[c] : 1.0;
-          sCol2[4 * bn2 + i] = ok ? E2.bn_gamma[c] : 0.0;
-          sCol2[5 * bn2 + i] = ok ? E2.bn_beta[c] : 0.0;
-          sCol2[6 * bn2 + i] = ok ? E2.bn_inv_denom[c] : 1.0;
-        }
-      }
-    }
+    stage_cols(E, sCol, bn, n0, P.n, t, (int)blockDim.x - 64, &R.sOff[0]);
+    if (CHAIN) stage_cols(P.epi2, sCol2, P.bn2, 0, P.n2, t, (int)blockDim.x - 64, &R.sOff[1]);
   }
   __syncwarp();
   // every thread is past the predecessor grid before any global write (nk == 0 tiles
@@ -578,7 +736,10 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];   // chained: [stage 1 | stage 2]
   __shared__ double sRowTerm[128];
+  __shared__ int sOff[2];
   TileRing R;
+  if (threadIdx.x < 2) sOff[threadIdx.x] = 0;
+  R.sOff = sOff;
   // schedule arrays and the segment table are static for the lifetime of a launch
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
@@ -620,6 +781,13 @@ __device__ __forceinline__ void tma_2d_pair(void* dst, const void* tmap, int32_t
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// wait on a local mbarrier whose arrivals come from the peer CTA (acquire at cluster scope)
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr), "r"(parity) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -667,14 +835,21 @@ __device__ __forceinline__ void pair_swizzle(int64_t local, int64_t nrbp, int n_
   rbp = g * gh + r % rows;
 }
 
-template <int TMEM_COLS>
+// CHAIN: the pair also runs the chained dense stage 2 (qg_chain) over its 256 rows.  Each
+// CTA's stage-1 epilogue writes its 128 rows of requantized codes into its own ring slots
+// (the stage-2 LEFT operand, UMMA K-major), fences them to the async proxy and arrives on
+// the leader's mid barrier; each CTA stages HALF of every weight tile (TMA, leader's full
+// barrier); the leader then issues the stage-2 cta_group::2 MMAs (M = 256, N = bn2) into
+// the same TMEM columns and both CTAs run epilogue 2 on their own rows.
+template <int TMEM_COLS, bool CHAIN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
     tc_pair_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ __align__(8) uint64_t full[8], empty[8], done, midbar;
   __shared__ uint32_t tmem_base_s;
-  __shared__ unsigned long long sRowSum[128];
+  __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];
   __shared__ double sRowTerm[128];
+  __shared__ int sOff[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -696,8 +871,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   pair_swizzle(local, (nrb + 1) >> 1, P.n_tiles, P.pair_swizzle, rbp, nt);
   const int64_t n0 = (int64_t)nt * bn;
   const int64_t rb = rbp * 2 + rank;                     // this CTA's row block (may be past the end)
-  const int64_t rb_other = rbp * 2 + (rank ^ 1);
-  const bool rb_ok = rb < nrb, other_ok = rb_other < nrb;
+  const bool rb_ok = rb < nrb;
 
   // K schedule of the pair (identical in both CTAs)
   UnionCursor U{};
@@ -718,9 +892,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   asm volatile("griddepcontrol.launch_dependents;");
 
   const uint32_t a_bytes = 16384u, bh_bytes = (uint32_t)bh * 128u;
-  const uint32_t stage_bytes = a_bytes + bh_bytes;
+  const uint32_t stage_bytes = a_bytes + (uint32_t)(P.slot_bn >> 1) * 128u;
   uint8_t* stage0 = smem;
+  const bool fused = P.mode == QG_GEMM_EPILOGUE;
+  const qg_epilogue& E = P.epi;
   double* sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);
+  double* sCol2 = sCol + (fused ? col_doubles(bn, epi_row_only(E), E.bn_mean != nullptr) : 0);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
                  "n"(TMEM_COLS));
@@ -729,11 +906,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   if (tid == 32) {
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     mbar_init(&done, 1);
+    mbar_init(&midbar, 2);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  const bool fused = P.mode == QG_GEMM_EPILOGUE;
-  const qg_epilogue& E = P.epi;
   if (tid < 128) sRowSum[tid] = 0ull;
+  if (CHAIN && tid < 128) sRowSum[128 + tid] = 0ull;
+  if (tid < 2) sOff[tid] = 0;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -743,6 +921,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   TileRing R;
   R.stage0 = stage0; R.sCol = sCol; R.full = full; R.empty = empty; R.done = &done;
   R.sRowSum = sRowSum; R.sRowTerm = sRowTerm; R.S = S; R.it0 = 0; R.ndone = 0; R.pdl_wait = false; R.tmem = tmem;
+  R.sOff = sOff;
+  const int k2 = CHAIN ? P.k2 : 0;
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer (both CTAs): own A block + own half of B ----------------
@@ -777,6 +957,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       tma_2d_pair(dst, amap, 0, (int32_t)arow, bar);
       tma_2d_pair(dst + a_bytes, G.tmap_b, 0, (int32_t)(((int64_t)kt * (P.b_npad << 7) >> 7) + b_row0), bar);
     }
+    if (CHAIN) {
+      // stage 2's weights: this CTA's half of every K tile, into the slots after stage 1's
+      const int bh2 = P.bn2 >> 1;
+      const uint32_t wh_bytes = (uint32_t)bh2 * 128u;
+      for (int j = 0; j < k2; ++j) {
+        const int g = nk + j, s = g % S;
+        if (g >= S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
+        if (rank == 0) mbar_expect_tx(&full[s], 2u * wh_bytes);
+        tma_2d_pair(stage0 + (size_t)s * stage_bytes + a_bytes, &P.w2_map, 0,
+                    (int32_t)((int64_t)j * P.w2_npad + (int64_t)rank * bh2), leader_full + (uint32_t)s * 8u);
+      }
+    }
   } else if (warp == 1 && lane == 0) {
     if (rank == 0) {
       // ---------------- MMA issuer (leader): both CTAs' stages, M = 256 ----------------
@@ -794,6 +986,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
         umma_commit_pair(&empty[s]);
       }
       if (nk > 0) umma_commit_pair(&done);
+      if (CHAIN) {
+        // both CTAs' epilogue 1 drained the accumulator and wrote their codes (mid barrier)
+        mbar_wait_cluster(smem_u32(&midbar), 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t idesc2 = (2u << 4) | ((uint32_t)(P.bn2 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+        for (int j = 0; j < k2; ++j) {
+          const int g = nk + j, s = g % S;
+          mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_i8_pair(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc2,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_pair(&empty[s]);
+        }
+        umma_commit_pair(&done);
+      }
     }
   } else if (warp >= 2 && fused) {
     const int t = tid - 64;
@@ -801,28 +1011,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       const int64_t row = rb * 128 + t;
       sRowTerm[t] = (E.use_row && rb_ok && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
     }
-    for (int i = t; i < bn; i += (int)blockDim.x - 64) {
-      const int64_t cc = n0 + i;
-      const bool ok = cc < P.n;
-      sCol[0 * bn + i] = (ok && E.use_col) ? __dmul_rn(E.k_col, (double)E.col_sums[cc]) : 0.0;
-      sCol[1 * bn + i] = (ok && E.bias) ? E.bias[cc] : 0.0;
-      if (E.bn_mean) {
-        sCol[2 * bn + i] = ok ? E.bn_mean[cc] : 0.0;
-        sCol[3 * bn + i] = ok ? E.bn_denom[cc] : 1.0;
-        sCol[4 * bn + i] = ok ? E.bn_gamma[cc] : 0.0;
-        sCol[5 * bn + i] = ok ? E.bn_beta[cc] : 0.0;
-        sCol[6 * bn + i] = ok ? E.bn_inv_denom[cc] : 1.0;
-      }
-    }
+    stage_cols(E, sCol, bn, n0, P.n, t, (int)blockDim.x - 64, &sOff[0]);
+    if (CHAIN) stage_cols(P.epi2, sCol2, P.bn2, 0, P.n2, t, (int)blockDim.x - 64, &sOff[1]);
   }
   __syncwarp();
+  uint32_t ndone = 0;
   if (nk > 0) {
     mbar_wait(smem_u32(&done), 0);
+    ndone = 1;
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
   __syncthreads();
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 3);
-  if (rb_ok) {
+  if (CHAIN) {
+    uint8_t* mid0 = stage0 + (size_t)(nk % S) * stage_bytes;
+    uint8_t* mid1 = stage0 + (size_t)((nk + 1) % S) * stage_bytes;
+    if (rb_ok) tile_epilogue<1>(P, G, R, (int64_t)blockIdx.x, rb, 0, nk, tmem, sCol, true, mid0, mid1);
+    // codes (generic proxy) -> visible to the leader's tensor core; TMEM reads retired
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid == 0) mbar_arrive_remote(mapa_cluster(smem_u32(&midbar), 0));
+    const qg_epilogue& E2 = P.epi2;
+    if (tid < 128) {
+      const int64_t row = rb * 128 + tid;
+      R.sRowTerm[tid] = (E2.use_row && rb_ok && row < G.m) ? __dmul_rn(E2.k_row, (double)sRowSum[tid]) : 0.0;
+    }
+    mbar_wait(smem_u32(&done), ndone & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    __syncthreads();                                     // stage-2 row terms visible
+    if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 7);
+    if (rb_ok) {
+      tile_epilogue<2>(P, G, R, (int64_t)blockIdx.x, rb, 0, k2, tmem, sCol2, true);
+      if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
+      if (E2.out_kind == QG_OUT_PLANES && G.q_row_sums) {
+        __syncthreads();
+        if (tid < 128 && rb * 128 + tid < G.m && sRowSum[128 + tid])
+          atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[128 + tid]);
+      }
+    }
+  } else if (rb_ok) {
     tile_epilogue<0>(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused);
     if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
     if (fused && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
@@ -831,7 +1059,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
         atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[tid]);
     }
   }
-  (void)other_ok;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   cluster_sync_all();                                    // both CTAs done with TMEM and the ring
@@ -1089,7 +1316,7 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) { rc = QG_ERR_SHAPE; return 0; }
   // reserved fields (round-1 opt-in variants, removed) must be zero
   if (a->a_bits || a->reserved1 || a->reserved2 || a->reserved3 ||
-      (a->epi && (a->epi->reserved_d0 != 0.0 || a->epi->reserved_d1 != 0.0)))
+      (a->epi && a->epi->reserved_d1 != 0.0))
     { rc = QG_ERR_UNSUPPORTED; return 0; }
   P = TiledParams{};
   P.segs = a->segs; P.nsegs = a->nsegs; P.a_blocks = a->a_blocks; P.b_npad = a->b_npad; P.n = a->n;
@@ -1101,11 +1328,16 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.total_ctas = a->total_ctas;
   P.pair = a->pair;
   P.slot_bn = P.bn;
-  size_t cols = (a->epi && a->epi->bn_mean ? 7 : 2) * (size_t)P.bn * 8;
+  // per-column constants: fp64 terms + the fp32 screen's acc0_c / delta_c (col_doubles)
+  const qg_epilogue* e1 = a->epi;
+  size_t cols = e1 ? (size_t)col_doubles(P.bn, !e1->use_col && !e1->use_const && !e1->bias, e1->bn_mean != nullptr) * 8
+                   : 0;
+  static const bool screen = getenv("QG_NO_SCREEN") == nullptr;
+  P.screen = screen ? 1 : 0;
   if (a->chain) {
     const qg_chain* c = a->chain;
     // stage 1: one N tile covering all its columns, packed codes
-    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != 1 || a->n > a->bn || a->pair || c->reserved ||
+    if (a->mode != QG_GEMM_EPILOGUE || a->n_tiles != 1 || a->n > a->bn || c->reserved ||
         a->epi->out_kind != QG_OUT_PLANES)
       { rc = QG_ERR_UNSUPPORTED; return 0; }
     if (!c->w || !c->epi || c->w_npad < 32 || c->w_npad > 256 || (c->w_npad & (c->w_npad - 1)) || c->n < 1 ||
@@ -1123,7 +1355,9 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
     P.w2_npad = c->w_npad;
     P.epi2 = *c->epi;
     P.slot_bn = std::max(P.bn, P.bn2);
-    cols += (c->epi->bn_mean ? 7 : 2) * (size_t)P.bn2 * 8;
+    if (c->epi->reserved_d1 != 0.0) { rc = QG_ERR_UNSUPPORTED; return 0; }
+    const qg_epilogue* e2 = c->epi;
+    cols += (size_t)col_doubles(P.bn2, !e2->use_col && !e2->use_const && !e2->bias, e2->bn_mean != nullptr) * 8;
   }
   return cols;
 }
@@ -1169,12 +1403,12 @@ extern "C" int qg_encode_linear_map(const void* base, int64_t bytes, int32_t box
   return r == CUDA_SUCCESS ? QG_OK : QG_ERR_ARG;
 }
 
-template <int COLS>
+template <int COLS, bool CHAIN>
 static void launch_pair(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
   static size_t attr_done = 0;
   if (smem > attr_done) {
-    cudaFuncSetAttribute(tc_pair_kernel<COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(tc_pair_kernel<COLS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(tc_pair_kernel<COLS, CHAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(tc_pair_kernel<COLS, CHAIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
     attr_done = smem;
   }
@@ -1189,7 +1423,7 @@ static void launch_pair(const TiledParams& P, unsigned grid, size_t smem, cudaSt
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, tc_pair_kernel<COLS>, P);
+  cudaLaunchKernelEx(&cfg, tc_pair_kernel<COLS, CHAIN>, P);
 }
 
 extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
@@ -1199,23 +1433,35 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   if (rc != QG_OK) return rc;
   if (P.pair) {
     // total_ctas = 2 x pairs; a stage holds the own A block + half of the B tile
-    if ((a->total_ctas & 1) || P.bn < 64) return QG_ERR_UNSUPPORTED;
+    if ((a->total_ctas & 1) || P.bn < 64 || (P.chain && P.bn2 < 32)) return QG_ERR_UNSUPPORTED;
     void* zero = nullptr;
     cudaGetSymbolAddress(&zero, g_zero_block);
     if (qg_encode_linear_map(zero, 16384, 128, &P.zero_map) != QG_OK) return QG_ERR_UNSUPPORTED;
+    if (P.chain &&
+        qg_encode_linear_map(P.w2, (int64_t)P.k2 * P.w2_npad * 128, P.bn2 >> 1, &P.w2_map) != QG_OK)
+      return QG_ERR_UNSUPPORTED;
     // 8 row-block pairs per N-major group: the ~148 pairs in flight then share A row
     // blocks and B column tiles in L2 (C5 16k: 73% -> 79% of the int8 peak)
     static const int swz = getenv("QG_PAIR_SWIZZLE") ? atoi(getenv("QG_PAIR_SWIZZLE")) : 8;
     P.pair_swizzle = swz < 1 ? 1 : swz;
-    const size_t stage = 16384 + (size_t)P.bn * 64;
+    const size_t stage = 16384 + (size_t)P.slot_bn * 64;
     cudaStream_t st = (cudaStream_t)stream;
-    P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (smem_budget() - cols) / stage));
+    P.stages = (int32_t)std::max<size_t>(P.chain ? 3 : 2, std::min<size_t>(8, (smem_budget() - cols) / stage));
     const size_t smem = (size_t)P.stages * stage + cols;
     const unsigned grid = (unsigned)a->total_ctas;
-    switch (P.bn) {
-      case 64: launch_pair<64>(P, grid, smem, st); break;
-      case 128: launch_pair<128>(P, grid, smem, st); break;
-      default: launch_pair<256>(P, grid, smem, st); break;
+    const int tcols = std::max(32, (int)P.slot_bn);
+    if (P.chain) {
+      switch (tcols) {
+        case 64: launch_pair<64, true>(P, grid, smem, st); break;
+        case 128: launch_pair<128, true>(P, grid, smem, st); break;
+        default: launch_pair<256, true>(P, grid, smem, st); break;
+      }
+    } else {
+      switch (tcols) {
+        case 64: launch_pair<64, false>(P, grid, smem, st); break;
+        case 128: launch_pair<128, false>(P, grid, smem, st); break;
+        default: launch_pair<256, false>(P, grid, smem, st); break;
+      }
     }
     return tstatus();
   }

@@ -334,6 +334,17 @@ def use_pair(b_npad: int, row_blocks_total: int, sizes, mode: int) -> bool:
             and row_blocks_total * max(1, b_npad // 256) >= 2 * sm_count())
 
 
+PAIR_CHAIN = os.environ.get("QG_PAIR_CHAIN", "0") != "0"
+
+
+def use_pair_chain(b_npad: int, w_npad: int, row_blocks_total: int, sizes) -> bool:
+    """Chained aggregate -> update stages on 2-SM CTA pairs (tc_pair_kernel<.., CHAIN>):
+    each CTA streams half of every B / weight tile, so a K tile costs 16 KB + bn*64 B of
+    L2 traffic per CTA instead of 16 KB + bn*128 B.  Needs >= 2 pairs per SM of work."""
+    return (PAIR_CHAIN and sizes is not None and b_npad >= 64 and w_npad >= 32
+            and row_blocks_total >= 2 * sm_count())
+
+
 def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: int, out_npad: int, epi_struct,
            keep: list, work: float = 0.0, a_bits: bool = False, sizes=None, chain: Chain | None = None):
     """One grouped tiled GEMM over ``segs`` (TSeg list with row_blocks set in .m).
@@ -345,6 +356,7 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
         if b_npad > 256 or a_bits:
             raise ValueError("chained stage needs one N tile <= 256 and byte blocks")
         bn = b_npad
+        pair = use_pair_chain(b_npad, chain.w_npad, sum(rbs), sizes)
     elif pair:
         bn = max(64, min(256, b_npad))
     else:
