@@ -432,6 +432,16 @@ int qg_bmm_counters(int64_t rt, int64_t ct, int64_t zero_tiles, int32_t s, int64
 int qg_gemm_counters(int64_t rt, int64_t ct, const int64_t* plane_zero_tiles, int32_t s, int32_t t,
                      int64_t n_chunks, int32_t jump, int32_t cross_tile, qg_counters* out);
 
+/*
+ * Host partitioner (no device work).  Replaces partition() (graph.py:190-229, the
+ * balanced BFS-grown greedy METIS stand-in): identical decisions for the same seed
+ * (Python random.Random(seed).randrange reproduced).  Input: CSR of the undirected,
+ * sorted, self-loop-free neighbour lists (Graph.neighbors, graph.py:73-81).
+ * part_of: int64 [n], written.  QG_ERR_ARG unless 1 <= num_parts <= n.
+ */
+int qg_partition_bfs(int64_t n, const int64_t* indptr, const int64_t* nbrs, int64_t num_parts, int64_t seed,
+                     int64_t* part_of);
+
 #ifdef __cplusplus
 }
 #endif

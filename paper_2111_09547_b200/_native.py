@@ -35,7 +35,7 @@ EXPORTS = ("qg_version", "qg_status_reset", "qg_quantize_pack", "qg_pack_planes"
            "qg_test_requant", "qg_tiled_gemm", "qg_block_prepare", "qg_codes_to_tiles",
            "qg_tiles_to_codes", "qg_entry_tiles",
            "qg_block_prepare_grouped", "qg_bmm_1xs", "qg_gemm_sxt", "qg_batch_h2d", "qg_bmm_counters",
-           "qg_gemm_counters", "qg_encode_linear_map", "qg_slab_reset")
+           "qg_gemm_counters", "qg_encode_linear_map", "qg_slab_reset", "qg_partition_bfs")
 
 _vp, _i64, _i32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
 
@@ -112,6 +112,7 @@ def lib() -> ctypes.CDLL:
             "qg_batch_h2d": ([_vp, _i64, _vp, _vp], ctypes.c_int),
             "qg_bmm_counters": ([_i64, _i64, _i64, _i32, _i64, _i32, _i32, _vp], ctypes.c_int),
             "qg_gemm_counters": ([_i64, _i64, _vp, _i32, _i32, _i64, _i32, _i32, _vp], ctypes.c_int),
+            "qg_partition_bfs": ([_i64, _vp, _vp, _i64, _i64, _vp], ctypes.c_int),
         }
         for name, (argt, rest) in sigs.items():
             fn = getattr(L, name)

@@ -1,9 +1,11 @@
-"""Block-diagonal subgraph batches and their single-transfer compound buffer.
+"""Graph IO, partitioning, block-diagonal subgraph batches and their
+single-transfer compound buffer (mirror of graph.py).
 
-Mirror of the batch side of graph.py (graph.py:265-440).  Graph IO and the
-BFS partitioner (graph.py:85-262) are host preprocessing outside the
-reference's timed region and out of this package's scope: partitions are
-supplied as ``PartitionAssignment`` (the METIS-import path, graph.py:232-256).
+Graph IO (graph.py:85-156) and partition import/export (graph.py:232-262) are
+host file formats, kept here with the reference's formats and error messages.
+The balanced BFS partitioner (graph.py:190-229) runs natively
+(``qg_partition_bfs``, csrc/qgtc_partition.cu): same assignment for the same
+seed, O(E log E) instead of the reference's per-step frontier scan.
 
 Batch construction runs on the GPU: kept intra-part edges are written
 straight into packed adjacency words (``qg_edges_to_bits``; no dense
@@ -28,6 +30,9 @@ from .quantize import QuantParams, quantize_pack_device
 
 BUFFER_MAGIC = b"QGTB"
 _BUFFER_HEADER = struct.Struct("<4sHIIBddBQQ")
+GRAPH_MAGIC = b"QGTG"
+_GRAPH_HEADER = struct.Struct("<4sHIQ")
+BALANCE_SLACK = 0.10
 
 
 @dataclass(eq=False)
@@ -93,6 +98,140 @@ class PartitionAssignment:
             self._csr = (order, starts)
         order, starts = self._csr
         return order[starts[part]:starts[part + 1]]
+
+
+# ------------------------------------------------------------------ graph IO
+def load_graph(path, fmt: str = "edge-list-text") -> Graph:
+    """Read a graph (graph.py:85-92): text lines ``src dst`` with an optional
+    ``# nodes N`` header, or the binary QGTG image."""
+    readers = {"edge-list-text": _read_text_graph, "binary": _read_binary_graph}
+    if fmt not in readers:
+        raise ValueError(f"unknown graph format {fmt!r}")
+    return readers[fmt](path)
+
+
+def _read_text_graph(path) -> Graph:
+    # formats and messages of graph.py:95-125; a header bounds only the lines after it
+    declared = None
+    src, dst = [], []
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            tok = raw.split()
+            if not tok:
+                continue
+            if tok[0].startswith("#"):
+                head = raw.strip()[1:].split()
+                if len(head) != 2 or head[0] != "nodes" or not head[1].isdigit():
+                    raise FormatError(f"{path}:{lineno}: unrecognized header {raw.strip()!r}")
+                declared = int(head[1])
+                continue
+            if len(tok) != 2:
+                raise FormatError(f"{path}:{lineno}: expected 'src dst', got {raw.strip()!r}")
+            try:
+                a, b = int(tok[0]), int(tok[1])
+            except ValueError:
+                raise FormatError(f"{path}:{lineno}: non-integer endpoint") from None
+            if min(a, b) < 0:
+                raise FormatError(f"{path}:{lineno}: negative node index")
+            if declared is not None and max(a, b) >= declared:
+                raise FormatError(f"{path}:{lineno}: index exceeds declared node count {declared}")
+            src.append(a)
+            dst.append(b)
+    edges = np.stack([np.asarray(src, dtype=np.int64), np.asarray(dst, dtype=np.int64)], axis=1)
+    n = declared if declared is not None else (int(edges.max()) + 1 if len(edges) else 0)
+    return Graph(num_nodes=n, edges=edges)
+
+
+def _read_binary_graph(path) -> Graph:
+    data = open(path, "rb").read()
+    if len(data) < _GRAPH_HEADER.size:
+        raise FormatError("graph payload shorter than header")
+    magic, version, n, m = _GRAPH_HEADER.unpack_from(data)
+    if magic != GRAPH_MAGIC:
+        raise FormatError(f"bad graph magic {magic!r}")
+    if version != 1:
+        raise FormatError(f"unsupported graph version {version}")
+    if len(data) != _GRAPH_HEADER.size + 8 * m:
+        raise FormatError(f"graph payload length {len(data)} != expected {_GRAPH_HEADER.size + 8 * m}")
+    pairs = np.frombuffer(data, dtype="<u4", count=2 * m, offset=_GRAPH_HEADER.size)
+    return Graph(num_nodes=n, edges=pairs.astype(np.int64).reshape(-1, 2))
+
+
+def save_graph(g: Graph, path, fmt: str = "edge-list-text") -> None:
+    """Write a graph in either format (graph.py:128-141)."""
+    if fmt == "edge-list-text":
+        body = "\n".join(f"{a} {b}" for a, b in g.edges.tolist())
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write(f"# nodes {g.num_nodes}\n" + (body + "\n" if body else ""))
+    elif fmt == "binary":
+        with open(path, "wb") as fh:
+            fh.write(_GRAPH_HEADER.pack(GRAPH_MAGIC, 1, g.num_nodes, g.num_edges))
+            fh.write(np.ascontiguousarray(g.edges, dtype="<u4").tobytes())
+    else:
+        raise ValueError(f"unknown graph format {fmt!r}")
+
+
+# ------------------------------------------------------------- partitioning
+def edge_cut(g: Graph, assign: PartitionAssignment) -> int:
+    """Distinct undirected edges whose endpoints sit in different parts (graph.py:178-187)."""
+    if not len(g.edges):
+        return 0
+    lo, hi = g.edges.min(axis=1), g.edges.max(axis=1)
+    und = np.unique(lo * np.int64(g.num_nodes) + hi)
+    a, b = und // g.num_nodes, und % g.num_nodes
+    return int(np.count_nonzero(assign.part_of[a] != assign.part_of[b]))
+
+
+def partition(g: Graph, num_parts: int, seed: int = 0) -> PartitionAssignment:
+    """Balanced BFS-grown greedy partition (graph.py:190-229) on the native host
+    partitioner: identical part_of to the reference for the same seed."""
+    n = g.num_nodes
+    if not 1 <= num_parts <= n:
+        raise ValueError(f"num_parts must be in [1, {n}], got {num_parts}")
+    e = g.edges[g.edges[:, 0] != g.edges[:, 1]] if len(g.edges) else g.edges.reshape(0, 2)
+    both = np.unique(np.concatenate([e, e[:, ::-1]]), axis=0) if len(e) else e
+    indptr = np.searchsorted(both[:, 0], np.arange(n + 1)).astype(np.int64)
+    nbrs = np.ascontiguousarray(both[:, 1], dtype=np.int64)
+    part_of = np.empty(n, dtype=np.int64)
+    rc = N.lib().qg_partition_bfs(n, indptr.ctypes.data, nbrs.ctypes.data if len(nbrs) else None,
+                                  int(num_parts), int(seed), part_of.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"qg_partition_bfs failed ({rc})")
+    assign = PartitionAssignment(num_parts=num_parts, part_of=part_of)
+    assign.edge_cut = edge_cut(g, assign)
+    return assign
+
+
+def import_partition(path, num_nodes: int | None = None, num_parts: int | None = None) -> PartitionAssignment:
+    """One part index per line, e.g. METIS output (graph.py:232-256)."""
+    parts = []
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            t = raw.strip()
+            if t:
+                try:
+                    parts.append(int(t))
+                except ValueError:
+                    raise FormatError(f"{path}:{lineno}: not an integer") from None
+    if num_nodes is not None and len(parts) != num_nodes:
+        raise ValueError(f"expected {num_nodes} lines, found {len(parts)}")
+    if not parts:
+        raise ValueError("empty partition file")
+    arr = np.asarray(parts, dtype=np.int64)
+    if arr.min() < 0:
+        raise ValueError("negative part index")
+    count = int(arr.max()) + 1
+    if num_parts is not None:
+        if count > num_parts:
+            raise ValueError(f"part index {count - 1} >= num_parts {num_parts}")
+        count = num_parts
+    return PartitionAssignment(num_parts=count, part_of=arr)
+
+
+def export_partition(assign: PartitionAssignment, path) -> None:
+    """Inverse of import_partition (graph.py:259-262)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("".join(f"{p}\n" for p in assign.part_of.tolist()))
 
 
 class SubgraphBatch:

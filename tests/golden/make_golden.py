@@ -301,6 +301,31 @@ def binding_cases(bg, bb, rng):
     return d
 
 
+def partition_cases(bg, rng):
+    """Reference partition() (graph.py:190-229) + edge_cut on random and planted graphs."""
+    d = {}
+    cases = []
+    for _ in range(10):
+        n = int(rng.integers(8, 300))
+        cases.append((n, rng.integers(0, n, (int(rng.integers(0, 4 * n)), 2))))
+    edges, _, _ = _planted_graph(rng, 600, 6, 4, 1)
+    cases.append((600, edges))
+    cases.append((5, np.zeros((0, 2), dtype=np.int64)))               # edgeless: seeds only
+    for i, (n, e) in enumerate(cases):
+        g = bg.Graph(n, e)
+        d[f"g{i}_n"] = np.array(n)
+        d[f"g{i}_edges"] = g.edges
+        for parts in (1, 2, 5):
+            for seed in (0, 7, 2 ** 33 + 5):
+                if parts > n:
+                    continue
+                a = bg.partition(g, parts, seed=seed)
+                d[f"g{i}_p{parts}_s{seed}"] = a.part_of
+                d[f"g{i}_p{parts}_s{seed}_cut"] = np.array(a.edge_cut)
+    d["n"] = np.array(len(cases))
+    return d
+
+
 def main():
     bg, bb = _load_reference()
     rng = np.random.default_rng(20261017)
@@ -313,6 +338,10 @@ def main():
     d = binding_cases(bg, bb, rng)
     np.savez_compressed(os.path.join(OUT, "bindings.npz"), **d)
     print("bindings", len(d), "arrays")
+    # own generator: the fixtures above regenerate unchanged
+    d = partition_cases(bg, np.random.default_rng(20261018))
+    np.savez_compressed(os.path.join(OUT, "partition.npz"), **d)
+    print("partition", len(d), "arrays")
 
 
 if __name__ == "__main__":
