@@ -798,7 +798,7 @@ extern "C" int qg_test_requant(const double* x, int64_t n, double amin, double s
   return launch_status_g();
 }
 
-extern "C" int qg_version(void) { return 29; }  // == number of exported entry points
+extern "C" int qg_version(void) { return 30; }  // == number of exported entry points
 
 // ---------------------------------------------------------------------------
 // Reference-shaped entry points over qg_bitgemm / cudaMemcpyAsync,
