@@ -292,6 +292,7 @@ def kernel_roofline(model, batches, reps=20):
     r = EpochRunner(model, batches, rescan=False).capture(stamps=True)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     spans, ops, launches, step_ms = 0.0, 0.0, 0, 0.0
+    per = None
     with torch.cuda.stream(r.stream):
         for i in range(reps + 3):
             flush.zero_()
@@ -303,11 +304,15 @@ def kernel_roofline(model, batches, reps=20):
             if i < 3:
                 continue
             ks = r.kernel_spans()
+            per = [[0.0, w] for _, w in ks] if per is None else per
+            for j, (t, _) in enumerate(ks):
+                per[j][0] += t
             spans += sum(t for t, _ in ks)
             ops += sum(w for _, w in ks)
             launches += len(ks)
             step_ms += s.elapsed_time(e)
     del r
+    kernel_roofline.per_launch = [(t / reps, w) for t, w in (per or [])]
     return spans / reps, ops / reps, launches / reps, step_ms / reps
 
 
@@ -464,11 +469,18 @@ def c2_sweep(steps):
 def c5_point(n, bits, peak):
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from c5_sweep import run_point
-    c5 = run_point(n, 0.1, bits, reps=10, int8_peak=peak)
+    c5 = run_point(n, 0.1, bits, reps=10, int8_peak=peak, packed=True)
     c5.update({"bound": "tensor", "peak": peak, "unit": "TOPS",
                "kernel": "tc_pair_kernel (2-SM cluster, tcgen05.mma.cta_group::2.kind::i8 M=256, TMA)",
                "config": "C5: A Bernoulli(0.1) 1-bit x X uniform codes, reduce_bitplanes(bmm_1bit_by_nbit) "
-                         "in one launch, CUDA-graph replays timed with CUDA events"})
+                         "in one launch, CUDA-graph replays timed with CUDA events; *_from_packed adds the "
+                         "operand preparation from packed inputs (zero-tile scan + block expansion of A, "
+                         "X planes -> tiled codes), timed separately with CUDA events"})
+    # block-diagonal A (16 diagonal blocks): zero-tile jumping skips 15/16 of the tiles
+    bd = run_point(n, 0.1, bits, reps=10, int8_peak=peak, diag_blocks=16, packed=True)
+    c5["block_diagonal_16"] = {k: bd[k] for k in ("ms", "alg_tops", "eff_tops", "frac", "nonzero_blocks",
+                                                  "total_blocks", "parity_sampled_rows", "ms_from_packed",
+                                                  "frac_from_packed")}
     return c5
 
 
@@ -613,7 +625,10 @@ def ours(args, world, rank):
                                   "after an L2 flush; CUDA events around each replay give stamped_step_ms",
                      "launches_per_epoch": gemm_launches, "kernel_ms_per_epoch": round(gemm_ms, 5),
                      "stamped_step_ms": round(stamped_step_ms, 5),
-                     "kernel_share_of_step": round(gemm_ms / stamped_step_ms, 3)},
+                     "kernel_share_of_step": round(gemm_ms / stamped_step_ms, 3),
+                     "per_launch": [{"ms": round(t, 5), "tops": round(w / (t * 1e-3) / 1e12, 1) if t else None,
+                                     "frac": round(w / (t * 1e-3) / 1e12 / peak, 4) if t else None}
+                                    for t, w in getattr(kernel_roofline, "per_launch", [])]},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_ms, 5), "unit": "ms/epoch", "h2d_bytes_per_step": e2e_h2d,
                 "d2h_bytes_per_step": e2e_d2h, "wall_ms_per_step": round(e2e_wall / args.steps, 5),

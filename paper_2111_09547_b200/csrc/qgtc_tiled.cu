@@ -128,37 +128,6 @@ __device__ __forceinline__ void screen_col(const qg_epilogue& E, int i, double C
   sD[i] = (float)(gam + a0 * alpha);
 }
 
-// 8 codes of one slice through the screen; returns the mask of elements that need the
-// exact path
-template <bool PERCOL>
-__device__ __forceinline__ uint32_t screen8(const ScreenRow& S, const uint32_t (&v)[8], int cl8, uint32_t (&q)[8]) {
-  int32_t a0[8];
-  float dc[8];
-  if (PERCOL) {
-#pragma unroll
-    for (int j = 0; j < 8; j += 4) {
-      const int4 x = *reinterpret_cast<const int4*>(S.sA0 + cl8 + j);
-      const float4 z = *reinterpret_cast<const float4*>(S.sD + cl8 + j);
-      a0[j] = x.x; a0[j + 1] = x.y; a0[j + 2] = x.z; a0[j + 3] = x.w;
-      dc[j] = z.x; dc[j + 1] = z.y; dc[j + 2] = z.z; dc[j + 3] = z.w;
-    }
-  }
-  uint32_t bad = 0;
-#pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    int32_t sh = (int32_t)v[jj] - S.a0r;
-    if (PERCOL) sh -= a0[jj];
-    float y = fmaf((float)sh, S.alpha, S.dr);
-    if (PERCOL) y += dc[jj];
-    y = fminf(fmaxf(y, S.lo), S.hi);
-    const float t = __fadd_rd(y, 12582912.0f);                        // 1.5 * 2^23 + floor(y)
-    const float r = __fsub_rn(__fadd_rn(y, 12582912.0f), 12582912.0f);   // round-to-nearest(y)
-    bad |= (fabsf(y - r) > S.mrg ? 0u : 1u) << jj;
-    q[jj] = __float_as_uint(t) & 0xFFu;
-  }
-  return bad;
-}
-
 // Per-column epilogue constants of one stage into shared memory (col_doubles layout):
 // C = RN(k_col * col_sum), B = bias [, BN mean / denom / gamma / beta / inv_denom], and the
 // screen's acc0_c / delta_c.  Columns n0 + i for i = t, t + nt, ... < bn.
@@ -234,10 +203,145 @@ static __device__ __noinline__ uint32_t exact_code(const ExactArgs A, const doub
   return c.flag ? requant_exact(x, A.q_amin, A.q_scale, A.q_inv, A.maxv, status, flat) : c.code;
 }
 
+// The screened epilogue (ScreenRow) of this lane's slices, lean: per element one integer
+// shift, one I2FP, 2 FFMA/FADD, a clamp, the floor and the margin test; bytes packed with
+// PRMT, row sums with DP4A, one store per slice (8 byte stores for right-tiled outputs).
+// Slices with a flagged element, ragged columns or rows past m are deferred to a second,
+// warp-uniform pass (TMEM reloaded) that evaluates the exact fp64 path -- kept out of the
+// main loop so its registers do not burden it.
+// LAYOUT: 0 = chained stage 1 into the stage-2 operand in shared memory (mid0 / mid1),
+// 1 = next LEFT operand (left-tiled codes), 2 = next RIGHT operand (right-tiled codes).
+template <bool ROW_ONLY, int ST, int LAYOUT>
+__device__ __forceinline__ void epi_store(const EpiLane& L, uint8_t* q_codes, int64_t r128, int64_t rbase, int lrow,
+                                          uint8_t* mid0, uint8_t* mid1, int cl8, uint2 w, bool full) {
+  const int64_t c = L.n0 + cl8;
+  if (LAYOUT == 0) {
+    uint8_t* dst = ((c >> 7) ? mid1 : mid0) + (lrow >> 3) * 1024 + ((c & 127) >> 4) * 128 + (lrow & 7) * 16 + (c & 15);
+    *reinterpret_cast<uint2*>(dst) = w;
+  } else if (L.rvalid) {
+    if (LAYOUT == 1) {
+      *reinterpret_cast<uint2*>(q_codes + (c >> 7) * (r128 << 7) + rbase + ((c & 127) >> 4) * 128 + (c & 15)) = w;
+    } else {
+      uint8_t* base = q_codes + rbase + (c >> 3) * 1024;
+      if (full) {
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          base[jj * 16] = (uint8_t)(w.x >> (8 * jj));
+          base[(jj + 4) * 16] = (uint8_t)(w.y >> (8 * jj));
+        }
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (cl8 + jj < L.nvalid) base[jj * 16] = (uint8_t)((jj < 4 ? w.x : w.y) >> (8 * (jj & 3)));
+      }
+    }
+  }
+}
+
+template <bool ROW_ONLY, int ST, int LAYOUT>
+__device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
+                                             const double* __restrict__ sCol, double rterm, uint8_t* mid0,
+                                             uint8_t* mid1, const ScreenRow& S) {
+  const int bn = ST == 2 ? P.bn2 : P.bn;
+  uint8_t* const q_codes = G.q_codes;
+  const int64_t myrow = L.myrow;
+  const int lrow = (int)(myrow & 127);
+  int64_t rbase = 0;
+  if (LAYOUT == 1) rbase = (myrow >> 3) * 1024 + (myrow & 7) * 16;
+  if (LAYOUT == 2) {
+    const int64_t npad = ST == 2 ? P.out_npad2 : P.out_npad;
+    rbase = (myrow >> 7) * (npad << 7) + ((myrow & 127) >> 4) * 128 + (myrow & 15);
+  }
+  const int64_t r128 = G.r128;
+  const float C = 12582912.0f, lo = S.lo, hi = S.hi, alpha = S.alpha, dr = S.dr, mrg = S.mrg, mhi = 1.0f - S.mrg;
+  const int32_t a0r = S.a0r;
+  const int nval = L.rvalid ? L.nvalid : 0;
+  uint32_t rsum = 0, deferred = 0;
+  int k = 0;
+  for (int sl = L.first; sl < L.nslices; sl += L.step, ++k) {
+    const int cl8 = sl * 8;
+    uint32_t v[8];
+    L.load8(cl8, v);
+    int32_t a0[8];
+    float dc[8];
+    if (!ROW_ONLY) {
+      const int4 x0 = *reinterpret_cast<const int4*>(S.sA0 + cl8);
+      const int4 x1 = *reinterpret_cast<const int4*>(S.sA0 + cl8 + 4);
+      const float4 z0 = *reinterpret_cast<const float4*>(S.sD + cl8);
+      const float4 z1 = *reinterpret_cast<const float4*>(S.sD + cl8 + 4);
+      a0[0] = x0.x; a0[1] = x0.y; a0[2] = x0.z; a0[3] = x0.w; a0[4] = x1.x; a0[5] = x1.y; a0[6] = x1.z; a0[7] = x1.w;
+      dc[0] = z0.x; dc[1] = z0.y; dc[2] = z0.z; dc[3] = z0.w; dc[4] = z1.x; dc[5] = z1.y; dc[6] = z1.z; dc[7] = z1.w;
+    }
+    uint32_t t[8];
+    bool bad = cl8 + 8 > nval;                               // ragged slice or row past m
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int32_t sh = ROW_ONLY ? (int32_t)v[jj] - a0r : (int32_t)v[jj] - a0r - a0[jj];
+      float y = fmaf((float)sh, alpha, dr);
+      if (!ROW_ONLY) y += dc[jj];
+      y = fminf(fmaxf(y, lo), hi);
+      const float f = __fadd_rd(y, C);                     // 1.5 * 2^23 + floor(y)
+      const float d = y - (f - C);                          // y - floor(y), exact
+      bad |= (d < mrg) | (d > mhi);
+      t[jj] = __float_as_uint(f);
+    }
+    if (bad) {
+      deferred |= 1u << k;
+      continue;
+    }
+    uint2 w;
+    w.x = __byte_perm(__byte_perm(t[0], t[1], 0x0040), __byte_perm(t[2], t[3], 0x0040), 0x5410);
+    w.y = __byte_perm(__byte_perm(t[4], t[5], 0x0040), __byte_perm(t[6], t[7], 0x0040), 0x5410);
+    rsum = __dp4a(w.x, 0x01010101u, rsum);
+    rsum = __dp4a(w.y, 0x01010101u, rsum);
+    epi_store<ROW_ONLY, ST, LAYOUT>(L, q_codes, r128, rbase, lrow, mid0, mid1, cl8, w, true);
+  }
+  // ---- deferred slices: exact fp64 path (warp-uniform walk: tcgen05.ld is collective)
+  const uint32_t any = __reduce_or_sync(QG_FULL, deferred);
+  if (any) {
+    const qg_epilogue& E = ST == 2 ? P.epi2 : P.epi;
+    const double k_acc = E.k_acc, kconst = E.use_const ? E.k_const : 0.0;
+    const double q_amin = E.q_amin, q_scale = E.q_scale, q_inv = E.q_inv_scale;
+    const uint32_t maxv = (1u << E.q_bits) - 1u;
+    const bool relu = E.act == QG_ACT_RELU;
+    const double* sC = sCol;
+    const double* sB = sCol + bn;
+    const int64_t pn = ST == 2 ? P.n2 : P.n;
+    k = 0;
+    for (int sl = L.first; sl < L.nslices; sl += L.step, ++k) {
+      if (!((any >> k) & 1u)) continue;
+      const int cl8 = sl * 8;
+      uint32_t v[8];
+      L.load8(cl8, v);
+      if (!((deferred >> k) & 1u)) continue;
+      uint32_t q[8];
+      for (int jj = 0; jj < 8; ++jj) {
+        q[jj] = 0u;
+        if (cl8 + jj >= nval) continue;                    // padding column / row past m: code 0
+        const int cl = cl8 + jj;
+        double x = __dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm);
+        if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), kconst), sB[cl]);
+        if (relu) {
+          const int h = __double2hiint(x), m = ~(h >> 31);
+          x = __hiloint2double(h & m, __double2loint(x) & m);
+        }
+        const R12 c = quantize_code_r12(x, q_amin, q_inv, maxv);
+        q[jj] = c.flag ? requant_exact(x, q_amin, q_scale, q_inv, maxv, G.status, myrow * pn + L.n0 + cl) : c.code;
+      }
+      const uint2 w = make_uint2(q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24),
+                                 q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24));
+      rsum = __dp4a(w.x, 0x01010101u, rsum);
+      rsum = __dp4a(w.y, 0x01010101u, rsum);
+      epi_store<ROW_ONLY, ST, LAYOUT>(L, q_codes, r128, rbase, lrow, mid0, mid1, cl8, w, cl8 + 8 <= nval);
+    }
+  }
+  return rsum;
+}
+
 template <int ACT, bool HAS_BN, bool ROW_ONLY, int ST>
 __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
                                                const double* __restrict__ sCol, double rterm, uint8_t* mid0,
-                                               uint8_t* mid1, const ScreenRow& S) {
+                                               uint8_t* mid1) {
   const qg_epilogue& E = ST == 2 ? P.epi2 : P.epi;
   const int bn = ST == 2 ? P.bn2 : P.bn;
   const double* sC = sCol;
@@ -267,24 +371,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     L.load8(cl8, v);
     const bool full = L.rvalid && cl8 + 8 <= L.nvalid;
     uint32_t q[8];
-    bool screened = false;
-    if (ACT != QG_ACT_TANH && !HAS_BN && packed && S.on) {
-      screened = true;
-      uint32_t bad = screen8<!ROW_ONLY>(S, v, cl8, q);
-      if (!full) {
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if (!(L.rvalid && cl8 + jj < L.nvalid)) { q[jj] = 0u; bad &= ~(1u << jj); }
-      }
-      if (bad) {
-        const ExactArgs A{k_acc, kconst, q_amin, q_scale, q_inv, maxv};
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)
-          if ((bad >> jj) & 1u)
-            q[jj] = exact_code<ACT, ROW_ONLY>(A, sC, sB, cl8 + jj, v[jj], rterm, status, L.myrow * pn + L.n0 + cl8 + jj);
-      }
-    }
-    if (!screened) {
+    {
     double real[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
@@ -332,7 +419,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
                     ? requant_exact(real[jj], q_amin, q_scale, q_inv, maxv, status, L.myrow * pn + L.n0 + cl8 + jj)
                     : 0u;
     }
-    }   // !screened
+    }
     const uint32_t lo = q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24);
     const uint32_t hi = q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24);
     rsum += ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
@@ -476,9 +563,22 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
         S.sD = reinterpret_cast<const float*>(sCol + 2 * bn) + bn;
       }
     }
+    const int out_layout = ST == 2 ? P.out_layout2 : P.out_layout;
+    if (S.on && (ST == 1 || out_layout == 1 || out_layout == 2)) {
+      if (ST == 1) {
+        rsum = row_only ? epi_fast<true, ST, 0>(P, G, L, sCol, rterm, mid0, mid1, S)
+                        : epi_fast<false, ST, 0>(P, G, L, sCol, rterm, mid0, mid1, S);
+      } else if (out_layout == 1) {
+        rsum = row_only ? epi_fast<true, ST, 1>(P, G, L, sCol, rterm, mid0, mid1, S)
+                        : epi_fast<false, ST, 1>(P, G, L, sCol, rterm, mid0, mid1, S);
+      } else {
+        rsum = row_only ? epi_fast<true, ST, 2>(P, G, L, sCol, rterm, mid0, mid1, S)
+                        : epi_fast<false, ST, 2>(P, G, L, sCol, rterm, mid0, mid1, S);
+      }
+    } else
     switch ((E.act * 2 + (E.bn_mean != nullptr ? 1 : 0)) * 2 + (row_only ? 1 : 0)) {
 #define QG_EPI_CASE(i, A, B, Rw) \
-  case i: rsum = epi_slices<A, B, Rw, ST>(P, G, L, sCol, rterm, mid0, mid1, S); break;
+  case i: rsum = epi_slices<A, B, Rw, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
       QG_EPI_CASE(0, QG_ACT_NONE, false, false)
       QG_EPI_CASE(1, QG_ACT_NONE, false, true)
       QG_EPI_CASE(2, QG_ACT_NONE, true, false)
@@ -490,7 +590,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
       QG_EPI_CASE(8, QG_ACT_TANH, false, false)
       QG_EPI_CASE(9, QG_ACT_TANH, false, true)
       QG_EPI_CASE(10, QG_ACT_TANH, true, false)
-      default: rsum = epi_slices<QG_ACT_TANH, true, true, ST>(P, G, L, sCol, rterm, mid0, mid1, S); break;
+      default: rsum = epi_slices<QG_ACT_TANH, true, true, ST>(P, G, L, sCol, rterm, mid0, mid1); break;
 #undef QG_EPI_CASE
     }
   }
@@ -923,6 +1023,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   R.sRowSum = sRowSum; R.sRowTerm = sRowTerm; R.S = S; R.it0 = 0; R.ndone = 0; R.pdl_wait = false; R.tmem = tmem;
   R.sOff = sOff;
   const int k2 = CHAIN ? P.k2 : 0;
+  if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 1);
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer (both CTAs): own A block + own half of B ----------------
@@ -976,7 +1077,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       for (int it = 0; it < nk; ++it) {
         const int s = it % S;
         mbar_wait(smem_u32(&full[s]), (it / S) & 1);
-        if (it == 0) tstamp(P, (int64_t)blockIdx.x, 2);
+        if (it == 0) { tstamp(P, (int64_t)blockIdx.x, 2); tstamp(P, (int64_t)blockIdx.x + 1, 2); }
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
 #pragma unroll
@@ -986,24 +1087,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
         umma_commit_pair(&empty[s]);
       }
       if (nk > 0) umma_commit_pair(&done);
-      if (CHAIN) {
-        // both CTAs' epilogue 1 drained the accumulator and wrote their codes (mid barrier)
-        mbar_wait_cluster(smem_u32(&midbar), 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t idesc2 = (2u << 4) | ((uint32_t)(P.bn2 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-        for (int j = 0; j < k2; ++j) {
-          const int g = nk + j, s = g % S;
-          mbar_wait(smem_u32(&full[s]), (g / S) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_i8_pair(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc2,
-                         (j > 0 || kk > 0) ? 1u : 0u);
-          umma_commit_pair(&empty[s]);
-        }
-        umma_commit_pair(&done);
-      }
     }
   } else if (warp >= 2 && fused) {
     const int t = tid - 64;
@@ -1026,12 +1109,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   if (CHAIN) {
     uint8_t* mid0 = stage0 + (size_t)(nk % S) * stage_bytes;
     uint8_t* mid1 = stage0 + (size_t)((nk + 1) % S) * stage_bytes;
+    if (nk == 0 && tid == 0) tstamp(P, (int64_t)blockIdx.x, 2);
     if (rb_ok) tile_epilogue<1>(P, G, R, (int64_t)blockIdx.x, rb, 0, nk, tmem, sCol, true, mid0, mid1);
     // codes (generic proxy) -> visible to the leader's tensor core; TMEM reads retired
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (tid == 0) mbar_arrive_remote(mapa_cluster(smem_u32(&midbar), 0));
+    if (rank == 0 && warp == 1 && lane == 0) {
+      // ---- stage-2 MMAs (leader): both CTAs' epilogue 1 drained the accumulator and
+      // wrote their codes (mid barrier); the weight halves land on full[]
+      mbar_wait_cluster(smem_u32(&midbar), 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t idesc2 = (2u << 4) | ((uint32_t)(P.bn2 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      for (int j = 0; j < k2; ++j) {
+        const int g = nk + j, s = g % S;
+        mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_i8_pair(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc2,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit_pair(&empty[s]);
+      }
+      umma_commit_pair(&done);
+    }
+    __syncwarp();
     const qg_epilogue& E2 = P.epi2;
     if (tid < 128) {
       const int64_t row = rb * 128 + tid;
@@ -1051,6 +1155,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       }
     }
   } else if (rb_ok) {
+    if (nk == 0 && tid == 0) tstamp(P, (int64_t)blockIdx.x, 2);
     tile_epilogue<0>(P, G, R, (int64_t)blockIdx.x, rb, n0, nk, tmem, sCol, fused);
     if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
     if (fused && E.out_kind == QG_OUT_PLANES && G.q_row_sums) {
@@ -1059,6 +1164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
         atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), sRowSum[tid]);
     }
   }
+  if (!rb_ok && tid == 0) tstamp(P, (int64_t)blockIdx.x, 4);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   cluster_sync_all();                                    // both CTAs done with TMEM and the ring
