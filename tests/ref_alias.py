@@ -26,7 +26,8 @@ def _install():
     from paper_2111_09547_b200 import bindings as our_bindings
 
     sys.modules["bitgnn"] = ours
-    for sub in ("bitgemm", "bitpack", "engine", "errors", "graph", "quantize"):
+    import paper_2111_09547_b200.cli  # noqa: F401  (bitgnn.cli: the bench CLI on the B200 path)
+    for sub in ("bitgemm", "bitpack", "engine", "errors", "graph", "quantize", "cli"):
         sys.modules[f"bitgnn.{sub}"] = getattr(ours, sub)
     sys.modules["bitgnn_bindings"] = our_bindings
 

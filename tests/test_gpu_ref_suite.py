@@ -7,8 +7,8 @@ path) for those tests.  One pytest subprocess per reference test file; each
 must pass except the entries of ``NOT_APPLICABLE`` (reason stated there and in
 DESIGN.md section 2).
 
-``test_cli.py`` is not run: the reference CLI (cli.py) is out of scope
-(bench.py replaces it).
+``test_cli.py`` runs against ``paper_2111_09547_b200.cli`` (the bench CLI on the
+B200 path: native partitioner, GPU batches, tiled forward).
 """
 
 from __future__ import annotations
@@ -23,7 +23,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITE = os.path.join(ROOT, "oracle", "_ref", "ref_tests")
 FILES = ["test_quantize.py", "test_bitpack.py", "test_bitgemm.py", "test_engine.py", "test_graph.py",
-         "test_acceptance.py", "test_bindings.py"]
+         "test_acceptance.py", "test_bindings.py", "test_cli.py"]
 
 # node id -> why it cannot hold for this design (measured evidence in DESIGN.md section 2)
 NOT_APPLICABLE: dict[str, str] = {}
