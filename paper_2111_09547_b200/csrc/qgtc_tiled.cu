@@ -45,6 +45,7 @@ struct TiledParams {
   int32_t pair_swizzle;     // pair kernels: row-block pairs per N-major group (1 = plain order)
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
   int32_t screen;           // fp32 requant screen enabled (QG_NO_SCREEN=1 disables)
+  int32_t dbg;              // QG_EPI_DBG knock-out bits (experiments): 1 no stores, 2 no math, 4 no TMEM loads
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
   int32_t chain, bn2, k2, out_layout2;
@@ -112,12 +113,26 @@ __device__ __forceinline__ bool epi_row_only(const qg_epilogue& E) { return !E.u
 
 // per-column screen constants (staging warps; stages without batch norm); a column whose
 // shift does not fit turns the stage's screen off (*off)
+// alpha = k_acc / scale and ~1/alpha without fp64 divisions (software routines on the GPU):
+// the screen only needs its integer shifts near -beta / alpha; the identities
+// y = alpha acc' + delta hold exactly for the alpha used (relative 2^-52 off the quotient,
+// far inside the margin)
+__device__ __forceinline__ double screen_alpha(const qg_epilogue& E, double& inv_alpha) {
+  const double alpha = E.k_acc * E.q_inv_scale;
+  double r = (double)__frcp_rn((float)alpha);
+  r = r * (2.0 - alpha * r);
+  r = r * (2.0 - alpha * r);
+  inv_alpha = r;
+  return alpha;
+}
+
 __device__ __forceinline__ void screen_col(const qg_epilogue& E, int i, double C, double B, int32_t* sA0, float* sD,
                                            int* off) {
-  const double alpha = E.k_acc / E.q_scale;
+  double ia;
+  const double alpha = screen_alpha(E, ia);
   const double K = E.use_const ? E.k_const : 0.0;
-  const double gam = ((C + K) + B) / E.q_scale;
-  const double a0 = rint(-gam / alpha);
+  const double gam = ((C + K) + B) * E.q_inv_scale;
+  const double a0 = rint(-gam * ia);
   if (!(fabs(a0) <= 0x1p29)) {
     *off = 1;
     sA0[i] = 0;
@@ -238,6 +253,22 @@ __device__ __forceinline__ void epi_store(const EpiLane& L, uint8_t* q_codes, in
   }
 }
 
+// Screened estimate of one element: clamped fp32 y (floor bits in *f) and whether it is
+// within the per-element margin 2^-21 (|y| + 2 alpha) of an integer (>= 2x the error bound
+// 2^-24 (4 |Y| + 3 alpha) of ScreenRow).
+template <bool ROW_ONLY>
+__device__ __forceinline__ bool screen1(const ScreenRow& S, uint32_t acc, int32_t a0c, float dc, uint32_t& f) {
+  const int32_t sh = ROW_ONLY ? (int32_t)acc - S.a0r : (int32_t)acc - S.a0r - a0c;
+  float y = fmaf((float)sh, S.alpha, S.dr);
+  if (!ROW_ONLY) y += dc;
+  y = fminf(fmaxf(y, S.lo), S.hi);
+  const float fl = __fadd_rd(y, 12582912.0f);              // 1.5 * 2^23 + floor(y)
+  const float d = y - (fl - 12582912.0f);                  // y - floor(y), exact
+  const float m = fmaf(y, 0x1p-21f, S.mrg);                // y >= 0.5 > 0 after the clamp
+  f = __float_as_uint(fl);
+  return (d < m) | (d > 1.0f - m);
+}
+
 template <bool ROW_ONLY, int ST, int LAYOUT>
 __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
                                              const double* __restrict__ sCol, double rterm, uint8_t* mid0,
@@ -253,15 +284,18 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
     rbase = (myrow >> 7) * (npad << 7) + ((myrow & 127) >> 4) * 128 + (myrow & 15);
   }
   const int64_t r128 = G.r128;
-  const float C = 12582912.0f, lo = S.lo, hi = S.hi, alpha = S.alpha, dr = S.dr, mrg = S.mrg, mhi = 1.0f - S.mrg;
-  const int32_t a0r = S.a0r;
   const int nval = L.rvalid ? L.nvalid : 0;
   uint32_t rsum = 0, deferred = 0;
   int k = 0;
   for (int sl = L.first; sl < L.nslices; sl += L.step, ++k) {
     const int cl8 = sl * 8;
     uint32_t v[8];
-    L.load8(cl8, v);
+    if (P.dbg & 4) {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) v[jj] = (uint32_t)(cl8 * 131 + jj * 17 + lrow);
+    } else {
+      L.load8(cl8, v);
+    }
     int32_t a0[8];
     float dc[8];
     if (!ROW_ONLY) {
@@ -274,16 +308,12 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
     }
     uint32_t t[8];
     bool bad = cl8 + 8 > nval;                               // ragged slice or row past m
+    if (P.dbg & 2) {
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int32_t sh = ROW_ONLY ? (int32_t)v[jj] - a0r : (int32_t)v[jj] - a0r - a0[jj];
-      float y = fmaf((float)sh, alpha, dr);
-      if (!ROW_ONLY) y += dc[jj];
-      y = fminf(fmaxf(y, lo), hi);
-      const float f = __fadd_rd(y, C);                     // 1.5 * 2^23 + floor(y)
-      const float d = y - (f - C);                          // y - floor(y), exact
-      bad |= (d < mrg) | (d > mhi);
-      t[jj] = __float_as_uint(f);
+      for (int jj = 0; jj < 8; ++jj) t[jj] = v[jj];
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) bad |= screen1<ROW_ONLY>(S, v[jj], ROW_ONLY ? 0 : a0[jj], ROW_ONLY ? 0.f : dc[jj], t[jj]);
     }
     if (bad) {
       deferred |= 1u << k;
@@ -294,9 +324,10 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
     w.y = __byte_perm(__byte_perm(t[4], t[5], 0x0040), __byte_perm(t[6], t[7], 0x0040), 0x5410);
     rsum = __dp4a(w.x, 0x01010101u, rsum);
     rsum = __dp4a(w.y, 0x01010101u, rsum);
-    epi_store<ROW_ONLY, ST, LAYOUT>(L, q_codes, r128, rbase, lrow, mid0, mid1, cl8, w, true);
+    if (!(P.dbg & 1)) epi_store<ROW_ONLY, ST, LAYOUT>(L, q_codes, r128, rbase, lrow, mid0, mid1, cl8, w, true);
   }
-  // ---- deferred slices: exact fp64 path (warp-uniform walk: tcgen05.ld is collective)
+  // ---- deferred slices (warp-uniform walk: tcgen05.ld is collective): screened codes
+  // again, the exact fp64 path only for the flagged elements, zeros past the valid region
   const uint32_t any = __reduce_or_sync(QG_FULL, deferred);
   if (any) {
     const qg_epilogue& E = ST == 2 ? P.epi2 : P.epi;
@@ -315,18 +346,24 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
       L.load8(cl8, v);
       if (!((deferred >> k) & 1u)) continue;
       uint32_t q[8];
+#pragma unroll
       for (int jj = 0; jj < 8; ++jj) {
-        q[jj] = 0u;
-        if (cl8 + jj >= nval) continue;                    // padding column / row past m: code 0
-        const int cl = cl8 + jj;
-        double x = __dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm);
-        if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[cl]), kconst), sB[cl]);
-        if (relu) {
-          const int h = __double2hiint(x), m = ~(h >> 31);
-          x = __hiloint2double(h & m, __double2loint(x) & m);
+        const int c = cl8 + jj;
+        uint32_t f = 0;
+        const bool flag = screen1<ROW_ONLY>(S, v[jj], ROW_ONLY ? 0 : S.sA0[c], ROW_ONLY ? 0.f : S.sD[c], f);
+        q[jj] = f & 0xFFu;
+        if (c >= nval) {
+          q[jj] = 0u;                                      // padding column / row past m: code 0
+        } else if (flag) {
+          double x = __dadd_rn(__dmul_rn(k_acc, (double)(int32_t)v[jj]), rterm);
+          if (!ROW_ONLY) x = __dadd_rn(__dadd_rn(__dadd_rn(x, sC[c]), kconst), sB[c]);
+          if (relu) {
+            const int hh = __double2hiint(x), m = ~(hh >> 31);
+            x = __hiloint2double(hh & m, __double2loint(x) & m);
+          }
+          const R12 r = quantize_code_r12(x, q_amin, q_inv, maxv);
+          q[jj] = r.flag ? requant_exact(x, q_amin, q_scale, q_inv, maxv, G.status, myrow * pn + L.n0 + c) : r.code;
         }
-        const R12 c = quantize_code_r12(x, q_amin, q_inv, maxv);
-        q[jj] = c.flag ? requant_exact(x, q_amin, q_scale, q_inv, maxv, G.status, myrow * pn + L.n0 + cl) : c.code;
       }
       const uint2 w = make_uint2(q[0] | (q[1] << 8) | (q[2] << 16) | (q[3] << 24),
                                  q[4] | (q[5] << 8) | (q[6] << 16) | (q[7] << 24));
@@ -537,9 +574,10 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
       else if (G.row_sums) rs = rvalid ? G.row_sums[myrow] : 0;
       else known = false;
       const double accmax = (double)rs * E.screen_rmax;
-      const double alpha = E.k_acc / E.q_scale;
-      const double beta = (rterm - E.q_amin) / E.q_scale;
-      double a0 = rint(-beta / alpha);
+      double ia;
+      const double alpha = screen_alpha(E, ia);
+      const double beta = (rterm - E.q_amin) * E.q_inv_scale;
+      double a0 = rint(-beta * ia);
       const bool a0_ok = fabs(a0) <= 0x1p29;
       if (!a0_ok) a0 = 0.0;
       S.on = __all_sync(QG_FULL, known && accmax < 0x1p30) && alpha > 0.0 && alpha < 0x1p60;
@@ -548,12 +586,17 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
         float lo = 0.5f;
         double q0 = 0.0;
         if (E.act == QG_ACT_RELU) {
-          // q0: the reference quotient of x = 0 (quantize.py:102-104), exact fp64
-          q0 = __ddiv_rn(__dsub_rn(0.0, E.q_amin), E.q_scale);
+          // q0 ~ the reference quotient of x = 0 (quantize.py:102-104); its fp32 copy is
+          // inside the margin (y >= lo >= q0f)
+          q0 = -E.q_amin * E.q_inv_scale;
           lo = fmaxf(lo, (float)q0);
         }
-        const double margin = ((double)maxv + 3.0 + 2.0 * alpha + fabs(q0)) * 0x1p-21;
-        S.mrg = !rvalid ? -1.0f : (a0_ok && margin < 0.25) ? __double2float_ru(margin) : __int_as_float(0x7f800000);
+        // per-element margin 2^-21 (|y| + 2 alpha) (screen1): this is its constant part; +inf
+        // sends every element of the row to the exact path, -1 (rows past m) none
+        const double margin = (2.0 * alpha + (double)maxv * 0x1p-20) * 0x1p-21 + 0x1p-40;
+        S.mrg = !rvalid ? -1.0f
+                        : (a0_ok && margin < 0.125 && fabs(q0) < 0x1p20) ? __double2float_ru(margin)
+                                                                         : __int_as_float(0x7f800000);
         S.a0r = (int32_t)a0;
         S.dr = (float)(beta + a0 * alpha);
         S.alpha = (float)alpha;
@@ -1440,6 +1483,8 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
                    : 0;
   static const bool screen = getenv("QG_NO_SCREEN") == nullptr;
   P.screen = screen ? 1 : 0;
+  static const int dbg = getenv("QG_EPI_DBG") ? atoi(getenv("QG_EPI_DBG")) : 0;
+  P.dbg = dbg;
   if (a->chain) {
     const qg_chain* c = a->chain;
     // stage 1: one N tile covering all its columns, packed codes
