@@ -45,6 +45,7 @@ struct TiledParams {
   int32_t pair_swizzle;     // pair kernels: row-block pairs per N-major group (1 = plain order)
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
   int32_t screen;           // fp32 requant screen enabled (QG_NO_SCREEN=1 disables)
+  int32_t a_bits;           // a_blocks: the adjacency ships as PACKED 2 KB blocks, expanded in smem
   int32_t dbg;              // QG_EPI_DBG knock-out bits (experiments): 1 no stores, 2 no math, 4 no TMEM loads
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
@@ -108,6 +109,12 @@ struct ScreenRow {
 __host__ __device__ __forceinline__ int col_doubles(int bn, bool row_only, bool has_bn) {
   if (row_only && !has_bn) return 0;
   return has_bn ? 7 * bn : 3 * bn;
+}
+// bytes of one ring slot of the single-CTA kernel (a_bits adds the 2 KB packed block,
+// slots 1 KB aligned for the UMMA descriptors)
+__host__ __device__ __forceinline__ uint32_t tiled_stage_bytes(int slot_bn, int a_bits) {
+  const uint32_t b = 16384u + (uint32_t)slot_bn * 128u;
+  return a_bits ? ((b + 2048u + 1023u) & ~1023u) : b;
 }
 __device__ __forceinline__ bool epi_row_only(const qg_epilogue& E) { return !E.use_col && !E.use_const && !E.bias; }
 
@@ -497,6 +504,7 @@ struct TileRing {
   double* sCol;               // per-column epilogue constants
   uint64_t* full;
   uint64_t* empty;
+  uint64_t* aready;           // a_bits: the expanded A operand of a ring slot is ready
   uint64_t* done;
   unsigned long long* sRowSum;
   double* sRowTerm;
@@ -663,9 +671,11 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const int64_t n0 = (int64_t)nt * bn;
 
   // stage = [A: 16 KB UMMA bytes][B: bn x 128 B]
+  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B][a_bits: 2 KB packed bit block]
   const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u, slot_b = (uint32_t)P.slot_bn * 128u;
   uint8_t* stage0 = R.stage0;
-  const uint32_t stage_bytes = a_bytes + slot_b;
+  const bool abits = P.a_blocks && P.a_bits;
+  const uint32_t stage_bytes = tiled_stage_bytes(P.slot_bn, P.a_bits);
   double* sCol = R.sCol;
   uint64_t* full = R.full;
   uint64_t* empty = R.empty;
@@ -698,9 +708,16 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       for (int it = 0; it < pre; ++it) {
         uint8_t* dst = dst0 + (size_t)((it0 + it) % S) * stage_bytes;
         uint64_t* fb = &full[(it0 + it) % S];
-        mbar_expect_tx(fb, a_bytes + b_bytes);
-        if (P.a_blocks) bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
-        else bulk_g2s(dst + a_bytes, bbase + (int64_t)it * (P.b_npad << 7), b_bytes, fb);
+        if (abits) {
+          mbar_expect_tx(fb, 2048u + b_bytes);
+          bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
+        } else if (P.a_blocks) {
+          mbar_expect_tx(fb, a_bytes + b_bytes);
+          bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
+        } else {
+          mbar_expect_tx(fb, a_bytes + b_bytes);
+          bulk_g2s(dst + a_bytes, bbase + (int64_t)it * (P.b_npad << 7), b_bytes, fb);
+        }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = 0; it < pre; ++it) {
@@ -720,10 +737,17 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       int kt;
       const uint8_t* asrc;
       uint8_t* dst = stage0 + (size_t)s * stage_bytes;
-      if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
-      else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
-      mbar_expect_tx(&full[s], a_bytes + b_bytes);
-      bulk_g2s(dst, asrc, a_bytes, &full[s]);
+      if (abits) {
+        // 2 KB packed block -> staging; the expander warps build the 16 KB operand
+        kt = G.blk_kt[kbase + it];
+        mbar_expect_tx(&full[s], 2048u + b_bytes);
+        bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
+      } else {
+        if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
+        else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
+        mbar_expect_tx(&full[s], a_bytes + b_bytes);
+        bulk_g2s(dst, asrc, a_bytes, &full[s]);
+      }
       bulk_g2s(dst + a_bytes, bbase + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
     }
     if (CHAIN) {
@@ -744,7 +768,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     for (int it = 0; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
-      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+      mbar_wait(smem_u32(abits ? &R.aready[s] : &full[s]), (g / S) & 1);
       if (it == 0) tstamp(P, tile, 2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
@@ -765,6 +789,30 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     }
     stage_cols(E, sCol, bn, n0, P.n, t, (int)blockDim.x - 64, &R.sOff[0]);
     if (CHAIN) stage_cols(P.epi2, sCol2, P.bn2, 0, P.n2, t, (int)blockDim.x - 64, &R.sOff[1]);
+  }
+  if (abits && warp >= 2) {
+    // expander warps: packed 128x128 bit block -> UMMA K-major 0/1 bytes (16 KB) per ring
+    // slot, one 16-byte store per (row, 16-bit K-core); unit u = (row/8, K-core, row%8) is
+    // the core-matrix order, so consecutive lanes store consecutive 16 B
+    const int et = tid - 64, nt = (int)blockDim.x - 64;
+    for (int it = 0; it < nk; ++it) {
+      const uint32_t g = it0 + (uint32_t)it;
+      const int s = (int)(g % (uint32_t)S);
+      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+      uint8_t* slot = stage0 + (size_t)s * stage_bytes;
+      const uint32_t* bits = reinterpret_cast<const uint32_t*>(slot + a_bytes + slot_b);
+      for (int u = et; u < 1024; u += nt) {
+        const int r = ((u >> 6) << 3) | (u & 7), c = (u >> 3) & 7;
+        const uint32_t x = bits[r * 4 + (c >> 1)] >> ((c & 1) * 16);
+        *reinterpret_cast<uint4*>(slot + u * 16) =
+            make_uint4(expand_nibble(x & 0xFu), expand_nibble((x >> 4) & 0xFu), expand_nibble((x >> 8) & 0xFu),
+                       expand_nibble((x >> 12) & 0xFu));
+      }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.aready[s]);
+    }
   }
   __syncwarp();
   // every thread is past the predecessor grid before any global write (nk == 0 tiles
@@ -843,6 +891,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
 // CTA setup: TMEM allocation, ring barriers.
 template <int TMEM_COLS>
 __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                            uint64_t* aready,
                                             uint64_t* done, uint32_t* tmem_base_s, unsigned long long* sRowSum,
                                             double* sRowTerm, int S, uint32_t stage_bytes_max) {
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -856,10 +905,13 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
+    // aready: one arrival per expander warp (warps 2..)
+    for (int i = 0; i < S; ++i) mbar_init(&aready[i], (blockDim.x >> 5) - 2);
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   R.stage0 = smem;
+  R.aready = aready;
   R.sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes_max);
   R.full = full;
   R.empty = empty;
@@ -875,7 +927,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
 template <int TMEM_COLS, int MINB, int NT, bool CHAIN = false>
 __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], done;
+  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];   // chained: [stage 1 | stage 2]
   __shared__ double sRowTerm[128];
@@ -886,8 +938,8 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   // schedule arrays and the segment table are static for the lifetime of a launch
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
-  tiled_setup<TMEM_COLS>(R, smem, full, empty, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
-                         16384u + (uint32_t)P.slot_bn * 128u);
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
+                         tiled_stage_bytes(P.slot_bn, P.a_bits));
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -1464,7 +1516,7 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
     { rc = QG_ERR_ARG; return 0; }
   if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) { rc = QG_ERR_SHAPE; return 0; }
   // reserved fields (round-1 opt-in variants, removed) must be zero
-  if (a->a_bits || a->reserved1 || a->reserved2 || a->reserved3 ||
+  if ((a->a_bits && (!a->a_blocks || a->pair)) || a->reserved1 || a->reserved2 || a->reserved3 ||
       (a->epi && a->epi->reserved_d1 != 0.0))
     { rc = QG_ERR_UNSUPPORTED; return 0; }
   P = TiledParams{};
@@ -1476,6 +1528,7 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.phase_ns = a->phase_ns;
   P.total_ctas = a->total_ctas;
   P.pair = a->pair;
+  P.a_bits = a->a_blocks ? a->a_bits : 0;
   P.slot_bn = P.bn;
   // per-column constants: fp64 terms + the fp32 screen's acc0_c / delta_c (col_doubles)
   const qg_epilogue* e1 = a->epi;
@@ -1616,7 +1669,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     }
     return tstatus();
   }
-  const size_t stage = 16384 + (size_t)P.slot_bn * 128;
+  const size_t stage = tiled_stage_bytes(P.slot_bn, P.a_bits);
   // Occupancy: 2 CTAs/SM by default (one CTA's fp64 epilogue overlaps the other's main
   // loop).  Stages with N tiles <= 128 and >= 3 CTAs per SM of work run 3 CTAs/SM
   // (80-register variant, 72 KB ring, 3 x <= 128 TMEM columns): more warps hide the

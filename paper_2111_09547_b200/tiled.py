@@ -166,7 +166,11 @@ class BlockedAdjacency:
         return self._bytes
 
     def operand(self) -> tuple:
-        """(device pointer, a_bits) of the left operand the tiled GEMM reads."""
+        """(device pointer, a_bits) of the left operand the tiled GEMM reads: the packed
+        2 KB blocks (expanded in shared memory by the GEMM, QG_A_BITS=1) or the
+        pre-expanded 16 KB byte blocks."""
+        if A_BITS:
+            return (self.packed.data_ptr(), 1)
         return (self.bytes.data_ptr(), 0)
 
     def refresh(self):
@@ -336,6 +340,11 @@ def use_pair(b_npad: int, row_blocks_total: int, sizes, mode: int) -> bool:
 
 PAIR_CHAIN = os.environ.get("QG_PAIR_CHAIN", "0") != "0"
 
+# QG_A_BITS=1: adjacency blocks reach the tiled GEMM packed (2 KB per non-zero 128x128
+# block instead of 16 KB of 0/1 bytes) and the otherwise idle epilogue warps expand them
+# into the ring slot during the main loop: 8x less adjacency traffic from HBM / L2.
+A_BITS = os.environ.get("QG_A_BITS", "0") == "1"
+
 
 def use_pair_chain(b_npad: int, w_npad: int, row_blocks_total: int, sizes) -> bool:
     """Chained aggregate -> update stages on 2-SM CTA pairs (tc_pair_kernel<.., CHAIN>):
@@ -353,10 +362,10 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     rbs = [-(-s.m // TILE) for s in segs]
     pair = chain is None and use_pair(b_npad, sum(rbs), sizes, mode) and not a_bits
     if chain is not None:
-        if b_npad > 256 or a_bits:
-            raise ValueError("chained stage needs one N tile <= 256 and byte blocks")
+        if b_npad > 256:
+            raise ValueError("chained stage needs one N tile <= 256")
         bn = b_npad
-        pair = use_pair_chain(b_npad, chain.w_npad, sum(rbs), sizes)
+        pair = use_pair_chain(b_npad, chain.w_npad, sum(rbs), sizes) and not a_bits
     elif pair:
         bn = max(64, min(256, b_npad))
     else:
