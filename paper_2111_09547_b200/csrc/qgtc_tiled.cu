@@ -55,6 +55,20 @@ struct TiledParams {
   qg_epilogue epi2;
 };
 
+// Segment of a work item: the last segment with cta_begin <= w (cta_begin ascending).
+// Warp-cooperative: every lane tests its own segments with independent loads (one L2
+// round trip per 32 segments instead of a dependent binary search).
+__device__ __forceinline__ int find_seg(const qg_tseg* segs, int nsegs, int64_t w) {
+  const int lane = threadIdx.x & 31;
+  int cnt = 0;
+  for (int base = 0; base < nsegs; base += 32) {
+    const int i = base + lane;
+    const bool le = i < nsegs && segs[i].cta_begin <= w;
+    cnt += __popc(__ballot_sync(0xffffffffu, le));
+  }
+  return cnt - 1;
+}
+
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
   if (P.phase_ns) {
     uint64_t t;
@@ -508,6 +522,7 @@ struct TileRing {
   uint64_t* done;
   unsigned long long* sRowSum;
   double* sRowTerm;
+  int64_t* sRowIn;            // the stage's left-operand row sums (staged with the row terms)
   int* sOff;                  // [stage 1, stage 2]: a column's screen shift is out of range
   uint32_t tmem;
   int S;
@@ -579,7 +594,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
       int64_t rs = 0;
       bool known = true;
       if (ST == 2) rs = (int64_t)R.sRowSum[quad * 32 + lane];
-      else if (G.row_sums) rs = rvalid ? G.row_sums[myrow] : 0;
+      else if (G.row_sums) rs = R.sRowIn ? R.sRowIn[quad * 32 + lane] : (rvalid ? G.row_sums[myrow] : 0);
       else known = false;
       const double accmax = (double)rs * E.screen_rmax;
       double ia;
@@ -659,12 +674,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   if (tid == 0) tstamp(P, tile, 0);
 
   // ---- segment lookup (uniform): last segment with cta_begin <= tile
-  int lo = 0, hi = P.nsegs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (P.segs[mid].cta_begin <= tile) lo = mid; else hi = mid - 1;
-  }
-  const qg_tseg& G = P.segs[lo];
+  const qg_tseg& G = P.segs[find_seg(P.segs, P.nsegs, tile)];
   const int64_t local = tile - G.cta_begin;
   const int64_t rb = local / P.n_tiles;
   const int nt = (int)(local % P.n_tiles);
@@ -785,7 +795,9 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     if (R.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (t < 128) {
       const int64_t row = rb * 128 + t;
-      R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
+      const int64_t rsin = (G.row_sums && row < G.m) ? G.row_sums[row] : 0;
+      if (R.sRowIn) R.sRowIn[t] = rsin;
+      R.sRowTerm[t] = (E.use_row && row < G.m) ? __dmul_rn(E.k_row, (double)rsin) : 0.0;
     }
     stage_cols(E, sCol, bn, n0, P.n, t, (int)blockDim.x - 64, &R.sOff[0]);
     if (CHAIN) stage_cols(P.epi2, sCol2, P.bn2, 0, P.n2, t, (int)blockDim.x - 64, &R.sOff[1]);
@@ -931,10 +943,13 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];   // chained: [stage 1 | stage 2]
   __shared__ double sRowTerm[128];
+  // staged input row sums; the 3-CTA/SM variant keeps its static footprint (reads global)
+  __shared__ int64_t sRowIn[MINB >= 3 ? 1 : 128];
   __shared__ int sOff[2];
   TileRing R;
   if (threadIdx.x < 2) sOff[threadIdx.x] = 0;
   R.sOff = sOff;
+  R.sRowIn = MINB >= 3 ? nullptr : sRowIn;
   // schedule arrays and the segment table are static for the lifetime of a launch
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
@@ -1044,6 +1059,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];
   __shared__ double sRowTerm[128];
+  __shared__ int64_t sRowIn[128];
   __shared__ int sOff[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t rank;
@@ -1053,12 +1069,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 0);
 
   // ---- work item of the pair: (segment, row-block pair, N tile); cta_begin counts PAIRS
-  int lo = 0, hi = P.nsegs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (P.segs[mid].cta_begin <= pair) lo = mid; else hi = mid - 1;
-  }
-  const qg_tseg& G = P.segs[lo];
+  const qg_tseg& G = P.segs[find_seg(P.segs, P.nsegs, pair)];
   const int64_t local = pair - G.cta_begin;
   const int64_t nrb = G.r128 >> 7;
   int64_t rbp;
@@ -1107,7 +1118,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   if (tid < 128) sRowSum[tid] = 0ull;
   if (CHAIN && tid < 128) sRowSum[128 + tid] = 0ull;
   if (tid < 2) sOff[tid] = 0;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // PDL: the setup above and the STATIC operands below (adjacency / left blocks, column
+  // constants) overlap the predecessor grid's tail; its OUTPUTS (the B operand, row sums)
+  // are read only after griddepcontrol.wait (per role)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   cluster_sync_all();                                    // barriers of both CTAs initialised
@@ -1117,6 +1130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   R.stage0 = stage0; R.sCol = sCol; R.full = full; R.empty = empty; R.done = &done;
   R.sRowSum = sRowSum; R.sRowTerm = sRowTerm; R.S = S; R.it0 = 0; R.ndone = 0; R.pdl_wait = false; R.tmem = tmem;
   R.sOff = sOff;
+  R.sRowIn = sRowIn;
   const int k2 = CHAIN ? P.k2 : 0;
   if (tid == 0) tstamp(P, (int64_t)blockIdx.x, 1);
 
@@ -1128,6 +1142,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
     const int64_t b_row0 = ((n0 + (int64_t)rank * bh) >> 3) * 8;      // 128-byte rows
     UnionCursor c = U;
     int i_me = 0;
+    // the first ring-full: A (static) before the predecessor finishes, B after
+    const int pre = nk < S ? nk : S;
+    int kts[8];
     for (int it = 0; it < nk; ++it) {
       const int s = it % S;
       if (it >= S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
@@ -1151,6 +1168,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
       if (rank == 0) mbar_expect_tx(&full[s], 2u * (a_bytes + bh_bytes));
       const uint32_t bar = leader_full + (uint32_t)s * 8u;
       tma_2d_pair(dst, amap, 0, (int32_t)arow, bar);
+      if (it < pre) {
+        kts[it] = kt;
+        if (it == pre - 1) {
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          for (int j = 0; j < pre; ++j)
+            tma_2d_pair(stage0 + (size_t)j * stage_bytes + a_bytes, G.tmap_b, 0,
+                        (int32_t)(((int64_t)kts[j] * (P.b_npad << 7) >> 7) + b_row0),
+                        leader_full + (uint32_t)j * 8u);
+        }
+        continue;
+      }
       tma_2d_pair(dst + a_bytes, G.tmap_b, 0, (int32_t)(((int64_t)kt * (P.b_npad << 7) >> 7) + b_row0), bar);
     }
     if (CHAIN) {
@@ -1185,14 +1213,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
     }
   } else if (warp >= 2 && fused) {
     const int t = tid - 64;
-    if (t < 128) {
-      const int64_t row = rb * 128 + t;
-      sRowTerm[t] = (E.use_row && rb_ok && row < G.m) ? __dmul_rn(E.k_row, (double)G.row_sums[row]) : 0.0;
-    }
     stage_cols(E, sCol, bn, n0, P.n, t, (int)blockDim.x - 64, &sOff[0]);
     if (CHAIN) stage_cols(P.epi2, sCol2, P.bn2, 0, P.n2, t, (int)blockDim.x - 64, &sOff[1]);
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // row sums: predecessor outputs
+    if (t < 128) {
+      const int64_t row = rb * 128 + t;
+      const int64_t rsin = (G.row_sums && rb_ok && row < G.m) ? G.row_sums[row] : 0;
+      sRowIn[t] = rsin;
+      sRowTerm[t] = (E.use_row && rb_ok && row < G.m) ? __dmul_rn(E.k_row, (double)rsin) : 0.0;
+    }
   }
   __syncwarp();
+  // every thread is past the predecessor grid before any global write
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint32_t ndone = 0;
   if (nk > 0) {
     mbar_wait(smem_u32(&done), 0);
@@ -1695,7 +1728,11 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     // the split-N stages it replaces and two epilogues per tile: with fewer tiles than
     // SMs, 16 warps (1 CTA/SM) split the epilogue slices 4 ways
     const bool wide16 = a->total_ctas <= (int64_t)sms;
-    if (wide16) {
+    static const bool chain_wide = getenv("QG_CHAIN_WIDE") != nullptr && atoi(getenv("QG_CHAIN_WIDE")) != 0;
+    if (!wide16 && chain_wide && tcols == 256) {
+      // 12 warps: 3 warp groups split the two epilogues' slices (opt-in, measured)
+      launch_tiled<256, 2, 384, true>(P, grid, smem, st);
+    } else if (wide16) {
       switch (tcols) {
         case 32: launch_tiled<32, 1, 512, true>(P, grid, smem, st); break;
         case 64: launch_tiled<64, 1, 512, true>(P, grid, smem, st); break;

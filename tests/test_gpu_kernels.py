@@ -199,17 +199,20 @@ def test_bmm_reduced_equals_reduced_per_plane_bmm(bits):
     np.testing.assert_array_equal(got, dense.astype(np.int64) @ x.astype(np.int64))
 
 
-@pytest.mark.parametrize("pair", [True, False])
-def test_bmm_reduced_pair_path_large(pair):
+@pytest.mark.parametrize("pair,m", [(True, 4000), (False, 4000), (True, 2900)])
+def test_bmm_reduced_pair_path_large(pair, m):
     """The 2-SM (cta_group::2, TMA-signalled) pair path of bmm_reduced at a size that
     selects it: block-sparse A with empty row blocks (union schedule + zero blocks) and
-    an odd number of row blocks; result == dense product, and == the single-CTA path."""
+    an odd number of row blocks; result == dense product, and == the single-CTA path.
+    m = 4000: 32 row blocks = two full N-major groups of 8 pairs; m = 2900: 23 row blocks
+    = 12 pairs, a short last group and a pair with one row block past the end."""
     from paper_2111_09547_b200 import tiled
     g = torch.Generator(device="cuda").manual_seed(3)
-    m, k, n, bits = 4000, 2500, 4096, 5
+    k, n, bits = 2500, 4096, 5
     dense = (torch.rand((m, k), generator=g, device="cuda") < 0.02).to(torch.uint8)
     dense[:1000, 1200:] = 0
-    dense[2600:3000] = 0                                  # empty row blocks
+    dense[2600:3000] = 0                                  # empty row blocks (m = 4000)
+    dense[2000:2300] = 0 if m < 4000 else dense[2000:2300]
     dense[3000:, :600] = 0
     codes = torch.randint(0, 1 << bits, (k, n), generator=g, device="cuda", dtype=torch.uint8)
     a = bg.pack_colwise(dense)

@@ -1,0 +1,29 @@
+"""The measured opt-in kernel paths stay bit-exact: the config-scale parity suite
+(test_gpu_config_parity.py, logits vs the real reference) re-run in a subprocess with
+each switch set (the switches are read once at import / first launch).
+
+* QG_PAIR_CHAIN=1: chained aggregate -> update stages on the 2-SM pair kernel;
+* QG_A_BITS=1: packed 2 KB adjacency blocks expanded in shared memory by the GEMM;
+* QG_NO_SCREEN=1: every requant element on the exact fp64 path.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("switch", ["QG_PAIR_CHAIN", "QG_A_BITS", "QG_NO_SCREEN"])
+def test_optin_path_config_parity(switch):
+    env = dict(os.environ)
+    env[switch] = "1"
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_config_parity.py"),
+                        "-x", "-q", "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
