@@ -197,6 +197,7 @@ __device__ __forceinline__ void stage_cols(const qg_epilogue& E, double* sC, int
 // walks 8-column slices first, first+2, ...
 struct EpiLane {
   uint32_t tmem_row;
+  double* stage_real;         // fp64 outputs staged in shared memory (tile-local rows), or NULL
   bool has_acc, rvalid;
   int first, step, nslices, nvalid;   // this lane's slices: first, first + step, ...
   int64_t myrow, n0;
@@ -453,7 +454,7 @@ __device__ __forceinline__ uint32_t epi_slices(const TiledParams& P, const qg_ts
     }
     if (!packed) {
       if (L.rvalid) {
-        double* dst = out_real + L.myrow * pn + L.n0;
+        double* dst = L.stage_real ? L.stage_real + (int64_t)lrow * pn : out_real + L.myrow * pn + L.n0;
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj)
           if (cl8 + jj < L.nvalid) dst[cl8 + jj] = real[jj];
@@ -528,6 +529,7 @@ struct TileRing {
   int S;
   uint32_t it0;               // ring position (K tiles issued so far)
   uint32_t ndone;             // accumulator phases completed so far
+  uint32_t ring_bytes;        // bytes of the ring (free for output staging after the last MMA)
   bool pdl_wait;              // griddepcontrol.wait still pending (PDL-launched single tile)
 };
 
@@ -554,6 +556,12 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   const int nslices = (ncols_cta + 7) >> 3;
   const bool packed = fused && E.out_kind == QG_OUT_PLANES;
   EpiLane L;
+  L.stage_real = nullptr;
+  // fp64 outputs of a tile that spans all output columns form ONE contiguous block of
+  // rows in out_real: stage them in the (now idle) ring and store them coalesced
+  const bool stage_out = fused && E.out_kind == QG_OUT_REAL && n0 == 0 && pn <= bn &&
+                         (uint64_t)128 * (uint64_t)pn * 8u <= R.ring_bytes;
+  if (stage_out) L.stage_real = reinterpret_cast<double*>(R.stage0);
   L.tmem_row = tmem + ((uint32_t)(quad * 32) << 16);
   L.has_acc = nk > 0;
   L.first = half;
@@ -663,6 +671,15 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
   // chained stage 2 accumulates into the second half of sRowSum
   if (packed && (ST == 1 || G.q_row_sums) && rsum)
     atomicAdd(&R.sRowSum[(ST == 2 ? 128 : 0) + quad * 32 + lane], (unsigned long long)rsum);
+  if (stage_out) {
+    // the tile's rows [rb*128, min(m, rb*128 + 128)) x pn doubles, contiguous in out_real
+    __syncthreads();
+    const int64_t rows = G.m - rb * 128 < 128 ? G.m - rb * 128 : 128;
+    // consecutive threads -> consecutive doubles (segment bases are only 8-byte aligned)
+    const int64_t total = rows * pn;
+    double* dst = G.out_real + rb * 128 * pn;
+    for (int64_t i = tid; i < total; i += blockDim.x) dst[i] = L.stage_real[i];
+  }
 }
 
 // One work item: (segment, 128-row block, N tile) -> fused GEMM tile.  Ends with a
@@ -931,6 +948,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.sRowSum = sRowSum;
   R.sRowTerm = sRowTerm;
   R.S = S;
+  R.ring_bytes = (uint32_t)S * stage_bytes_max;
   R.it0 = 0;
   R.ndone = 0;
   R.pdl_wait = false;
@@ -1129,6 +1147,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTThreads)
   TileRing R;
   R.stage0 = stage0; R.sCol = sCol; R.full = full; R.empty = empty; R.done = &done;
   R.sRowSum = sRowSum; R.sRowTerm = sRowTerm; R.S = S; R.it0 = 0; R.ndone = 0; R.pdl_wait = false; R.tmem = tmem;
+  R.ring_bytes = (uint32_t)S * stage_bytes;
   R.sOff = sOff;
   R.sRowIn = sRowIn;
   const int k2 = CHAIN ? P.k2 : 0;
