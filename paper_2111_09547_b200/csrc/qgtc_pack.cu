@@ -113,6 +113,12 @@ __global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
 #pragma unroll
   for (int p = 0; p < BITS; ++p) word[p] = 0u;
   uint32_t my_sum = 0;                                     // lane i: row 32v + i
+  // fp32 sources: an fp32 screen y = fma(x, RN32(1/scale), RN32(-amin/scale)) with
+  // |y - q| <= 2^-24 (2|y| + 2|c|) against the reference quotient q = RN(RN(x - amin) /
+  // scale) (x is exact in fp64); elements within 2^-21 (|y| + |c|) of a code boundary,
+  // and non-finite ones, take the exact fp64 path (requant_slow)
+  const float inv32 = (float)inv, c32 = (float)(-amin * inv);
+  const float mc = fabsf(c32) * 0x1p-21f + 0x1p-40f, hic = (float)maxv + 0.5f;
   if (v < wpc) {
     const int64_t rbase = v * 32;
     const SrcT* colp = src + rbase * ld + c;
@@ -130,6 +136,14 @@ __global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
         if constexpr (sizeof(SrcT) == 1) {
           q[k] = (uint32_t)x[k];
           fm |= (uint32_t)(q[k] > maxv) << k;
+        } else if constexpr (sizeof(SrcT) == 4) {
+          const float y = fmaf((float)x[k], inv32, c32);
+          const float yc = fminf(fmaxf(y, 0.5f), hic);
+          const float f = __fadd_rd(yc, 12582912.0f);      // 1.5 * 2^23 + floor(yc)
+          const float d = yc - (f - 12582912.0f);
+          const float m = fmaf(yc, 0x1p-21f, mc);
+          q[k] = __float_as_uint(f) & 0x1FFu;
+          fm |= (uint32_t)((d < m) | (d > 1.0f - m) | !(fabsf((float)x[k]) <= 3.4028234663852886e38f)) << k;
         } else {
           const R12 rq = quantize_code_r12_tight((double)x[k], amin, inv, maxv);
           q[k] = rq.code;
@@ -150,8 +164,13 @@ __global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
         if (!(cok && k < nk)) q[k] = 0u;
         if (k < 4) lo |= q[k] << (8 * k);
         else hi |= q[k] << (8 * (k - 4));
-        const uint32_t sum = __reduce_add_sync(QG_FULL, q[k]);
-        if (lane == i0 + k) my_sum = sum;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        // rows i0 + k and i0 + k + 1 in the two 16-bit halves (sum <= 32 * 255 < 2^16)
+        const uint32_t sum = __reduce_add_sync(QG_FULL, q[k] | (q[k + 1] << 16));
+        if (lane == i0 + k) my_sum = sum & 0xFFFFu;
+        if (lane == i0 + k + 1) my_sum = sum >> 16;
       }
       if (codes && cok) {
         uint8_t* cp = codes + (rbase + i0) * cols + c;

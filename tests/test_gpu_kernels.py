@@ -147,6 +147,33 @@ def test_quantize_pack_large_matches_oracle():
             np.testing.assert_array_equal(np.stack([q.words for q in st.planes]), w)
 
 
+@pytest.mark.parametrize("bits,amin,amax", [(8, 0.0, 1.0), (4, -0.5, 1.5), (2, -3.0, 1.0), (8, -1e-3, 3e-3),
+                                            (7, 100.0, 228.0)])
+def test_bitqnt_fp32_screen_matches_oracle(bits, amin, amax):
+    """The row-wise bit_qnt kernel's fp32 screen (fp32 sources) against the fp64
+    reference quotient: random values, values exactly on and one float ulp around every
+    code boundary (the exact path), out-of-range values; planes and row sums."""
+    from paper_2111_09547_b200 import _native as N
+    from paper_2111_09547_b200.quantize import quantize_pack_device
+    rng = np.random.default_rng(bits)
+    scale = (amax - amin) / (1 << bits)
+    rows, cols = 3001, 100
+    x = rng.uniform(amin - 0.2 * (amax - amin), amax + 0.2 * (amax - amin), (rows, cols)).astype(np.float32)
+    k = np.arange(-1, (1 << bits) + 2, dtype=np.float64)
+    edge = (amin + k * scale).astype(np.float32)
+    edge = np.concatenate([edge, np.nextafter(edge, np.float32(np.inf)), np.nextafter(edge, np.float32(-np.inf))])
+    flat = x.reshape(-1)
+    flat[:len(edge)] = edge
+    rng.shuffle(flat)
+    x = flat.reshape(rows, cols)
+    p = bg.QuantParams(amin, amax, bits)
+    r = quantize_pack_device(x, p, N.ROW_WISE_ID, 8, row_sums=True)
+    codes = O.quantize_codes(x.astype(np.float64), amin, amax, bits)
+    w, _, _ = O.pack_stack(O.planes_of(codes, bits), O.ROW, 8)
+    np.testing.assert_array_equal(r["planes"].cpu().numpy().view(np.uint32).reshape(w.shape), w)
+    np.testing.assert_array_equal(r["row_sums"].cpu().numpy(), codes.astype(np.int64).sum(axis=1))
+
+
 def test_empty_and_degenerate_shapes():
     a = bg.pack_colwise(np.zeros((0, 5), np.uint8))
     assert a.padded_rows == 0 and len(a.words) == 0
