@@ -353,7 +353,9 @@ int qg_tiles_to_codes(const uint8_t* tiles, int64_t rows, int64_t cols, int righ
  * of the first GEMM, one launch for all batches.  right = 0: left-tiled M x K
  * (GIN update, X as rows x features; optional int64 row code sums, ZEROED by the
  * caller); right = 1: right-tiled K x N (GCN aggregation, pitch = padded N).
- * A work unit is 32 rows x 128 columns; block_begin = first unit of the segment. */
+ * A work unit is 32 * words_per_unit rows (words_per_unit = 8 or 1: 32-byte plane loads
+ * for large inputs, more units for small ones) x 128 columns; unit_begin = first unit of
+ * the segment. */
 typedef struct {
   const uint32_t* words;       /* (bits, pad128(rows)/32 * pc) row-wise plane words   */
   uint8_t* tiles;              /* tiled u8 output                                    */
@@ -364,8 +366,8 @@ typedef struct {
   int64_t unit_begin;          /* first work unit of this segment                    */
 } qg_entry_seg;
 
-int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t nplanes, int32_t right, int64_t total_units,
-                   void* stream);
+int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t nplanes, int32_t right,
+                   int32_t words_per_unit, int64_t total_units, void* stream);
 
 /* Shifted reduction sum_p acc[p] << p (int64 in) narrowed to int32 with an
  * overflow flag.  Replaces reduce_bitplanes (bitgemm.py:291-298). */

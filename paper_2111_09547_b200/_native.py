@@ -107,7 +107,7 @@ def lib() -> ctypes.CDLL:
             "qg_test_requant": ([_vp, _i64, _f64, _f64, _f64, _i32, _vp, _vp, _vp], ctypes.c_int),
             "qg_planes_to_codes": ([_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i64, _i32, _vp, _vp],
                                    ctypes.c_int),
-            "qg_entry_tiles": ([_vp, _i32, _i32, _i32, _i64, _vp], ctypes.c_int),
+            "qg_entry_tiles": ([_vp, _i32, _i32, _i32, _i32, _i64, _vp], ctypes.c_int),
             "qg_block_prepare_grouped": ([_vp, _i32, _i64, _vp], ctypes.c_int),
             "qg_batch_h2d": ([_vp, _i64, _vp, _vp], ctypes.c_int),
             "qg_bmm_counters": ([_i64, _i64, _i64, _i32, _i64, _i32, _i32, _vp], ctypes.c_int),

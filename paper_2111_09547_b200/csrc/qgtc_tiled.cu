@@ -1424,19 +1424,21 @@ __global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t
   codes[r * ld + c] = tiles[off];
 }
 
-// Grouped entry conversion: row-wise feature planes -> tiled u8 codes.  Unit =
-// 32 rows (one plane word per column) x 128 columns; thread t < 128 owns column
-// c0 + t and expands its s plane words into 32 code bytes (bit i of plane p ->
-// bit p of byte i).  Right-tiled (K = rows): the 32 bytes are two 16-byte K-cores
-// of column c -> two vector stores.  Left-tiled (K = columns): transpose through
-// shared memory, then every thread stores one 16-byte K-core of one row; row code
-// sums reduce over the unit's 128 columns before one atomic per row.
+// Grouped entry conversion: row-wise feature planes of all batches -> tiled u8 codes.  Unit =
+// 256 rows (8 plane words per column) x 128 columns; thread t < 128 owns column c0 + t and
+// reads, per plane, its 8 consecutive row words with two 16-byte loads (one 32-B sector),
+// then expands them into 256 code bytes (bit i of plane p -> bit p of byte i).
+// Right-tiled (K = rows): every 32 rows of column c are two 16-byte K-cores -> direct
+// vector stores.  Left-tiled (K = columns): transpose through shared memory, then every
+// thread stores 16-byte K-cores of rows; row code sums reduce over the unit's 128 columns
+// before one atomic per row.
+template <int kEntryWords>                              // row words (x 32 rows) per unit: 8 or 1
 __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
                                                           int nplanes, int right) {
   // the first GEMM (PDL-launched) may start its prologue + static-operand prefetch now;
   // it reads this kernel's output only after griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
-  __shared__ __align__(16) uint8_t tile[32][128 + 16];
+  __shared__ __align__(16) uint8_t tile[32 * kEntryWords][128 + 16];
   int lo = 0, hi = nsegs - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -1449,47 +1451,73 @@ __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __
   const int64_t u = (int64_t)blockIdx.x - G.unit_begin;
   const int64_t wpl = G.pr >> 5;                          // words per column of one plane
   const int64_t ncg = right ? (G.pitch + 127) >> 7 : (G.pc + 127) >> 7;
-  const int64_t v = u / ncg, cg = u % ncg;                // 32-row group, 128-column group
+  const int64_t vb = (u / ncg) * kEntryWords, cg = u % ncg;   // first row word, 128-column group
   const int t = threadIdx.x;
   const int64_t wpp = wpl * G.pc;
-  uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t c = cg * 128 + (t & 127);
+  const int nw = (int)(wpl - vb < kEntryWords ? wpl - vb : kEntryWords);   // valid row words
+  uint32_t w[8][kEntryWords];                              // [plane][row word]
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+#pragma unroll
+    for (int j = 0; j < kEntryWords; ++j) w[p][j] = 0u;
   if (t < 128 && c < G.pc) {
-    for (int p = 0; p < nplanes; ++p) {
-      const uint32_t x = __ldg(G.words + p * wpp + c * wpl + v);
+    const uint32_t* col = G.words + c * wpl + vb;          // 16-byte aligned: wpl % 4 == 0, vb % 8 == 0
 #pragma unroll
-      for (int q = 0; q < 8; ++q) o[q] |= expand_nibble((x >> (4 * q)) & 0xFu) << p;
+    for (int p = 0; p < 8; ++p) {
+      if (p < nplanes) {
+        const uint32_t* src = col + p * wpp;
+        if (kEntryWords == 8 && nw == 8) {
+          const uint4 a = __ldg(reinterpret_cast<const uint4*>(src));
+          const uint4 b = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+          w[p][0] = a.x; w[p][1] = a.y; w[p][2] = a.z; w[p][3] = a.w;
+          w[p][4 % kEntryWords] = b.x; w[p][5 % kEntryWords] = b.y; w[p][6 % kEntryWords] = b.z;
+          w[p][7 % kEntryWords] = b.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < kEntryWords; ++j) w[p][j] = j < nw ? __ldg(src + j) : 0u;
+        }
+      }
     }
   }
-  if (right) {
-    if (t < 128 && c < G.pitch) {
-      const int64_t k0 = v * 32;
-      *reinterpret_cast<uint4*>(G.tiles + right_tile_off(k0, c, G.pitch)) = make_uint4(o[0], o[1], o[2], o[3]);
-      *reinterpret_cast<uint4*>(G.tiles + right_tile_off(k0 + 16, c, G.pitch)) = make_uint4(o[4], o[5], o[6], o[7]);
-    }
-    return;
-  }
-  if (t < 128) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) tile[i][t] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+  for (int j = 0; j < kEntryWords; ++j) {
+    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};               // 32 code bytes: rows 32(vb + j) ..
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] |= expand_nibble((w[p][j] >> (4 * q)) & 0xFu) << p;
+    if (right) {
+      if (t < 128 && c < G.pitch && j < nw) {
+        const int64_t k0 = (vb + j) * 32;
+        *reinterpret_cast<uint4*>(G.tiles + right_tile_off(k0, c, G.pitch)) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(G.tiles + right_tile_off(k0 + 16, c, G.pitch)) =
+            make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    } else if (t < 128) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) tile[32 * j + i][t] = (uint8_t)(o[i >> 2] >> (8 * (i & 3)));
+    }
   }
+  if (right) return;
   __syncthreads();
-  // 32 rows x 8 K-cores = 256 16-byte stores
-  const int r = t >> 3, core = t & 7;
-  const int64_t row = v * 32 + r, k = cg * 128 + core * 16;
-  const uint4 q = *reinterpret_cast<const uint4*>(&tile[r][core * 16]);
-  if (row < G.pitch) *reinterpret_cast<uint4*>(G.tiles + left_tile_off(row, k, G.pitch)) = q;
-  if (G.row_sums) {
-    const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
-    uint32_t sum = 0;
+  // 256 rows x 8 K-cores = 2048 16-byte stores, 8 per thread; the 8 cores of a row are 8
+  // consecutive lanes (row sums reduce over them)
+  for (int idx = t; idx < 32 * kEntryWords * 8; idx += 256) {
+    const int r = idx >> 3, core = idx & 7;
+    const int64_t row = vb * 32 + r, k = cg * 128 + core * 16;
+    const uint4 q = *reinterpret_cast<const uint4*>(&tile[r][core * 16]);
+    if (row < G.pitch) *reinterpret_cast<uint4*>(G.tiles + left_tile_off(row, k, G.pitch)) = q;
+    if (G.row_sums) {
+      const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+      uint32_t sum = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      sum += (w4[i] & 0xFFu) + ((w4[i] >> 8) & 0xFFu) + ((w4[i] >> 16) & 0xFFu) + (w4[i] >> 24);
-    // the 8 cores of a row are 8 consecutive lanes
+      for (int i = 0; i < 4; ++i) sum = __dp4a(w4[i], 0x01010101u, sum);
 #pragma unroll
-    for (int off = 4; off > 0; off >>= 1) sum += __shfl_xor_sync(QG_FULL, sum, off);
-    if (core == 0 && row < G.rows && sum)
-      atomicAdd(reinterpret_cast<unsigned long long*>(G.row_sums + row), (unsigned long long)sum);
+      for (int off = 4; off > 0; off >>= 1) sum += __shfl_xor_sync(QG_FULL, sum, off);
+      if (core == 0 && row < G.rows && sum)
+        atomicAdd(reinterpret_cast<unsigned long long*>(G.row_sums + row), (unsigned long long)sum);
+    }
   }
 }
 
@@ -1498,8 +1526,10 @@ __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __
 using namespace qg;
 
 extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t nplanes, int32_t right,
-                              int64_t total_units, void* stream) {
-  if (!segs || nsegs < 1 || nplanes < 1 || nplanes > 8 || total_units < 0) return QG_ERR_ARG;
+                              int32_t words_per_unit, int64_t total_units, void* stream) {
+  if (!segs || nsegs < 1 || nplanes < 1 || nplanes > 8 || total_units < 0 ||
+      (words_per_unit != 1 && words_per_unit != 8))
+    return QG_ERR_ARG;
   if (total_units == 0) return QG_OK;
   // programmatic dependent launch: the launch overlaps the predecessor's tail (the slab
   // reset of a captured epoch); the kernel waits before reading any predecessor output
@@ -1513,7 +1543,8 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, entry_tiles_kernel, segs, (int)nsegs, (int)nplanes, (int)right);
+  if (words_per_unit == 8) cudaLaunchKernelEx(&cfg, entry_tiles_kernel<8>, segs, (int)nsegs, (int)nplanes, (int)right);
+  else cudaLaunchKernelEx(&cfg, entry_tiles_kernel<1>, segs, (int)nsegs, (int)nplanes, (int)right);
   return cudaGetLastError() == cudaSuccess ? QG_OK : QG_ERR_CUDA;
 }
 

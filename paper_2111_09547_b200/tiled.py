@@ -483,16 +483,21 @@ def entry_tiles(stacks, side: str, want_row_sums: bool, keep: list):
         return None
     right = side == "right"
     segs, outs, begin = [], [], 0
+    # work unit rows: 256 (8 plane words, one 32-byte sector per plane and column) when
+    # that still gives >= 2 units per SM, else 32 (small inputs want more CTAs)
+    big = sum((-(-s.dims()[2] // 256)) * (-(-(npad_of(s.dims()[1]) if right else s.dims()[3]) // 128))
+              for s in stacks) >= 2 * sm_count()
+    urows = 256 if big else 32
     for s in stacks:
         rows, cols, pr, pc = s.dims()
         if right:
             pitch = npad_of(cols)
             tiles = N.alloc(max(pad128(rows) * pitch, 16), torch.uint8, "static")
-            units = (pr // 32) * (-(-pitch // 128))
+            units = (-(-pr // urows)) * (-(-pitch // 128))
         else:
             pitch = pad128(rows)
             tiles = N.alloc(max(pad128(cols) * pitch, 16), torch.uint8, "static")
-            units = (pr // 32) * (-(-pc // 128))
+            units = (-(-pr // urows)) * (-(-pc // 128))
         rs = N.alloc(rows, torch.int64, "volatile") if (want_row_sums and not right) else None
         seg = EntrySeg()
         seg.words, seg.tiles, seg.row_sums = s.dwords.data_ptr(), tiles.data_ptr(), (rs.data_ptr() if rs is not None
@@ -505,8 +510,8 @@ def entry_tiles(stacks, side: str, want_row_sums: bool, keep: list):
     if begin:
         table = SegTable(segs, EntrySeg)
         keep.append(table)
-        N.check(N.lib().qg_entry_tiles(table.dev.data_ptr(), len(segs), stacks[0].bits, int(right), begin,
-                                       N.stream()), "qg_entry_tiles")
+        N.check(N.lib().qg_entry_tiles(table.dev.data_ptr(), len(segs), stacks[0].bits, int(right), urows // 32,
+                                       begin, N.stream()), "qg_entry_tiles")
     return outs
 
 
