@@ -58,15 +58,19 @@ struct TiledParams {
 // Segment of a work item: the last segment with cta_begin <= w (cta_begin ascending).
 // Warp-cooperative: every lane tests its own segments with independent loads (one L2
 // round trip per 32 segments instead of a dependent binary search).
-__device__ __forceinline__ int find_seg(const qg_tseg* segs, int nsegs, int64_t w) {
+template <typename Seg, typename Begin>
+__device__ __forceinline__ int find_seg_by(const Seg* segs, int nsegs, int64_t w, Begin begin) {
   const int lane = threadIdx.x & 31;
   int cnt = 0;
   for (int base = 0; base < nsegs; base += 32) {
     const int i = base + lane;
-    const bool le = i < nsegs && segs[i].cta_begin <= w;
+    const bool le = i < nsegs && begin(segs[i]) <= w;
     cnt += __popc(__ballot_sync(0xffffffffu, le));
   }
   return cnt - 1;
+}
+__device__ __forceinline__ int find_seg(const qg_tseg* segs, int nsegs, int64_t w) {
+  return find_seg_by(segs, nsegs, w, [](const qg_tseg& g) { return g.cta_begin; });
 }
 
 static __device__ __forceinline__ void tstamp(const TiledParams& P, int64_t tile, int k) {
@@ -1375,12 +1379,7 @@ __global__ void __launch_bounds__(256) block_expand_grouped_kernel(const qg_bloc
   asm volatile("griddepcontrol.launch_dependents;");
   const int64_t gb = blockIdx.x;
   if (gb >= total_blocks) return;
-  int lo = 0, hi = nsegs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].block_begin <= gb) lo = mid; else hi = mid - 1;
-  }
-  const qg_block_seg& S = segs[lo];
+  const qg_block_seg& S = segs[find_seg_by(segs, nsegs, gb, [](const qg_block_seg& g) { return g.block_begin; })];
   const int64_t b = gb - S.block_begin;
   const int t = threadIdx.x, r = t & 127, h = t >> 7;
   const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(S.packed) + b * 128 + r);
@@ -1439,12 +1438,8 @@ __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __
   // it reads this kernel's output only after griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
   __shared__ __align__(16) uint8_t tile[32 * kEntryWords][128 + 16];
-  int lo = 0, hi = nsegs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].unit_begin <= (int64_t)blockIdx.x) lo = mid; else hi = mid - 1;
-  }
-  const qg_entry_seg& G = segs[lo];
+  const qg_entry_seg& G =
+      segs[find_seg_by(segs, nsegs, (int64_t)blockIdx.x, [](const qg_entry_seg& g) { return g.unit_begin; })];
   // PDL-launched: everything above read only the (static) segment table; the planes and
   // the zeroed row sums come from the stream predecessor
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1482,11 +1477,20 @@ __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __
   }
 #pragma unroll
   for (int j = 0; j < kEntryWords; ++j) {
-    uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};               // 32 code bytes: rows 32(vb + j) ..
+    // 32 code bytes (rows 32(vb + j) ..): for each 8-row group g gather byte g of the 8
+    // plane words (byte p = plane p, PRMT) and transpose the 8x8 bit matrix -- byte i of the
+    // result holds bit p of row 8g + i for every plane p, i.e. the code of row 8g + i
+    uint32_t o[8];
 #pragma unroll
-    for (int p = 0; p < 8; ++p)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) o[q] |= expand_nibble((w[p][j] >> (4 * q)) & 0xFu) << p;
+    for (int g = 0; g < 4; ++g) {
+      const uint32_t sel = (uint32_t)g | ((uint32_t)(g + 4) << 4);      // [a.byte g, b.byte g]
+      const uint32_t p01 = __byte_perm(w[0][j], w[1][j], sel), p23 = __byte_perm(w[2][j], w[3][j], sel);
+      const uint32_t p45 = __byte_perm(w[4][j], w[5][j], sel), p67 = __byte_perm(w[6][j], w[7][j], sel);
+      const uint64_t x = ((uint64_t)__byte_perm(p45, p67, 0x5410) << 32) | __byte_perm(p01, p23, 0x5410);
+      const uint64_t tt = transpose8x8(x);
+      o[2 * g] = (uint32_t)tt;
+      o[2 * g + 1] = (uint32_t)(tt >> 32);
+    }
     if (right) {
       if (t < 128 && c < G.pitch && j < nw) {
         const int64_t k0 = (vb + j) * 32;
