@@ -45,7 +45,9 @@ struct TiledParams {
   int32_t pair_swizzle;     // pair kernels: row-block pairs per N-major group (1 = plain order)
   int32_t slot_bn;          // ring slot B capacity in columns: max(bn, bn2)
   int32_t screen;           // fp32 requant screen enabled (QG_NO_SCREEN=1 disables)
-  int32_t a_bits;           // a_blocks: the adjacency ships as PACKED 2 KB blocks, expanded in smem
+  int32_t a_bits;           // a_blocks: the adjacency ships as PACKED 2 KB blocks, expanded in smem (1)
+                            // or into tensor memory (2)
+  int32_t a_slots, a_col0;  // a_bits 2: TMEM A ring slots (32 columns each) and its first column
   int32_t dbg;              // QG_EPI_DBG knock-out bits (experiments): 1 no stores, 2 no math, 4 no TMEM loads
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
@@ -131,6 +133,7 @@ __host__ __device__ __forceinline__ int col_doubles(int bn, bool row_only, bool 
 // bytes of one ring slot of the single-CTA kernel (a_bits adds the 2 KB packed block,
 // slots 1 KB aligned for the UMMA descriptors)
 __host__ __device__ __forceinline__ uint32_t tiled_stage_bytes(int slot_bn, int a_bits) {
+  if (a_bits == 2) return ((uint32_t)slot_bn * 128u + 2048u + 1023u) & ~1023u;   // no A bytes in smem
   const uint32_t b = 16384u + (uint32_t)slot_bn * 128u;
   return a_bits ? ((b + 2048u + 1023u) & ~1023u) : b;
 }
@@ -524,6 +527,7 @@ struct TileRing {
   uint64_t* full;
   uint64_t* empty;
   uint64_t* aready;           // a_bits: the expanded A operand of a ring slot is ready
+  uint64_t* aempty;           // a_bits 2: the MMAs reading a TMEM A slot completed
   uint64_t* done;
   unsigned long long* sRowSum;
   double* sRowTerm;
@@ -701,11 +705,15 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const int nt = (int)(local % P.n_tiles);
   const int64_t n0 = (int64_t)nt * bn;
 
-  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B]
-  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B][a_bits: 2 KB packed bit block]
-  const uint32_t a_bytes = 16384u, b_bytes = (uint32_t)bn * 128u, slot_b = (uint32_t)P.slot_bn * 128u;
+  // stage = [A: 16 KB UMMA bytes][B: bn x 128 B]                       (bytes)
+  //         [A: 16 KB UMMA bytes][B: bn x 128 B][2 KB packed bit block] (a_bits 1: A expanded in smem)
+  //         [B: bn x 128 B][2 KB packed bit block]                       (a_bits 2: A expanded into TMEM)
+  const uint32_t b_bytes = (uint32_t)bn * 128u, slot_b = (uint32_t)P.slot_bn * 128u;
   uint8_t* stage0 = R.stage0;
-  const bool abits = P.a_blocks && P.a_bits;
+  const bool ats = P.a_blocks && P.a_bits == 2;            // A operand from tensor memory
+  const bool abits = P.a_blocks && P.a_bits == 1;
+  const uint32_t a_bytes = ats ? 0u : 16384u;              // offset of B in a slot
+  const uint32_t bits_off = a_bytes + slot_b;              // offset of the packed bits
   const uint32_t stage_bytes = tiled_stage_bytes(P.slot_bn, P.a_bits);
   double* sCol = R.sCol;
   uint64_t* full = R.full;
@@ -739,12 +747,12 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       for (int it = 0; it < pre; ++it) {
         uint8_t* dst = dst0 + (size_t)((it0 + it) % S) * stage_bytes;
         uint64_t* fb = &full[(it0 + it) % S];
-        if (abits) {
+        if (abits || ats) {
           mbar_expect_tx(fb, 2048u + b_bytes);
-          bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
+          bulk_g2s(dst + bits_off, G.a + (int64_t)(kbase + it) * 2048, 2048u, fb);
         } else if (P.a_blocks) {
-          mbar_expect_tx(fb, a_bytes + b_bytes);
-          bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, a_bytes, fb);
+          mbar_expect_tx(fb, 16384u + b_bytes);
+          bulk_g2s(dst, G.a + (int64_t)(kbase + it) * 16384, 16384u, fb);
         } else {
           mbar_expect_tx(fb, a_bytes + b_bytes);
           bulk_g2s(dst + a_bytes, bbase + (int64_t)it * (P.b_npad << 7), b_bytes, fb);
@@ -768,11 +776,11 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       int kt;
       const uint8_t* asrc;
       uint8_t* dst = stage0 + (size_t)s * stage_bytes;
-      if (abits) {
-        // 2 KB packed block -> staging; the expander warps build the 16 KB operand
+      if (abits || ats) {
+        // 2 KB packed block -> staging; the expander warps build the operand (smem or TMEM)
         kt = G.blk_kt[kbase + it];
         mbar_expect_tx(&full[s], 2048u + b_bytes);
-        bulk_g2s(dst + a_bytes + slot_b, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
+        bulk_g2s(dst + bits_off, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
       } else {
         if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
         else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
@@ -799,13 +807,24 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
     for (int it = 0; it < nk; ++it) {
       const uint32_t g = it0 + (uint32_t)it;
       const int s = (int)(g % (uint32_t)S);
-      mbar_wait(smem_u32(abits ? &R.aready[s] : &full[s]), (g / S) & 1);
+      mbar_wait(smem_u32((abits || ats) ? &R.aready[s] : &full[s]), (g / S) & 1);
       if (it == 0) tstamp(P, tile, 2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = smem_u32(stage0 + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+      if (ats) {
+        // A from the TMEM ring slot g % a_slots (lane = row, 4 K bytes per column): 8 columns
+        // per K = 32
+        const uint32_t sa = g % (uint32_t)P.a_slots;
+        const uint32_t at = tmem + (uint32_t)P.a_col0 + 32u * sa;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_i8(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)
+          umma_i8_ts(tmem, at + 8u * (uint32_t)kk, umma_desc(b0 + kk * 256u), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&R.aempty[sa]);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_i8(tmem, umma_desc(a0 + kk * 256u), umma_desc(b0 + kk * 256u), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+      }
       umma_commit(&empty[s]);
     }
     if (nk > 0) umma_commit(R.done);
@@ -843,6 +862,31 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       }
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.aready[s]);
+    }
+  }
+  if (ats && warp >= 4 && warp < 8) {
+    // A into TENSOR MEMORY: warp w (lanes 32 (w % 4) ..) expands its 32 rows -- thread =
+    // row, 128 bits -> 128 bytes of 0/1 = 32 TMEM columns -- with one tcgen05.st per K
+    // tile; no shared-memory traffic for A beyond the 2 KB of bits
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t SA = (uint32_t)P.a_slots;
+    for (int it = 0; it < nk; ++it) {
+      const uint32_t g = it0 + (uint32_t)it;
+      const int s = (int)(g % (uint32_t)S);
+      const uint32_t sa = g % SA;
+      mbar_wait(smem_u32(&full[s]), (g / S) & 1);
+      if (g >= SA) mbar_wait(smem_u32(&R.aempty[sa]), ((g / SA) - 1) & 1);   // slot read by the MMA
+      const uint4 b4 = *reinterpret_cast<const uint4*>(stage0 + (size_t)s * stage_bytes + bits_off + r * 16);
+      const uint32_t wv[4] = {b4.x, b4.y, b4.z, b4.w};
+      uint32_t x[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) x[c] = expand_nibble((wv[c >> 3] >> (4 * (c & 7))) & 0xFu);
+      tmem_st32(tmem + lane_base + (uint32_t)P.a_col0 + 32u * sa, x);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(&R.aready[s]);
     }
@@ -924,7 +968,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
 // CTA setup: TMEM allocation, ring barriers.
 template <int TMEM_COLS>
 __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t* full, uint64_t* empty,
-                                            uint64_t* aready,
+                                            uint64_t* aready, uint64_t* aempty, bool a_tmem,
                                             uint64_t* done, uint32_t* tmem_base_s, unsigned long long* sRowSum,
                                             double* sRowTerm, int S, uint32_t stage_bytes_max) {
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -938,13 +982,15 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    // aready: one arrival per expander warp (warps 2..)
-    for (int i = 0; i < S; ++i) mbar_init(&aready[i], (blockDim.x >> 5) - 2);
+    // aready: one arrival per expander warp (warps 2.. for smem expansion, 4..7 for TMEM)
+    for (int i = 0; i < S; ++i) mbar_init(&aready[i], a_tmem ? 4u : (blockDim.x >> 5) - 2);
+    for (int i = 0; i < 4; ++i) mbar_init(&aempty[i], 1);
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   R.stage0 = smem;
   R.aready = aready;
+  R.aempty = aempty;
   R.sCol = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes_max);
   R.full = full;
   R.empty = empty;
@@ -961,7 +1007,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
 template <int TMEM_COLS, int MINB, int NT, bool CHAIN = false>
 __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constant__ TiledParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], done;
+  __shared__ __align__(8) uint64_t full[8], empty[8], aready[8], aempty[4], done;
   __shared__ uint32_t tmem_base_s;
   __shared__ unsigned long long sRowSum[CHAIN ? 256 : 128];   // chained: [stage 1 | stage 2]
   __shared__ double sRowTerm[128];
@@ -975,7 +1021,7 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   // schedule arrays and the segment table are static for the lifetime of a launch
   // sequence; only predecessor OUTPUTS need griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
-  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
+  tiled_setup<TMEM_COLS>(R, smem, full, empty, aready, aempty, P.a_blocks && P.a_bits == 2, &done, &tmem_base_s, sRowSum, sRowTerm, P.stages,
                          tiled_stage_bytes(P.slot_bn, P.a_bits));
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -1603,7 +1649,8 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
     { rc = QG_ERR_ARG; return 0; }
   if (a->b_npad % 8 || a->b_npad < (int64_t)a->n_tiles * a->bn) { rc = QG_ERR_SHAPE; return 0; }
   // reserved fields (round-1 opt-in variants, removed) must be zero
-  if ((a->a_bits && (!a->a_blocks || a->pair)) || a->reserved1 || a->reserved2 || a->reserved3 ||
+  if ((a->a_bits && (!a->a_blocks || a->pair)) || a->a_bits < 0 || a->a_bits > 2 ||
+      (a->a_bits == 2 && (a->chain || a->bn > 128)) || a->reserved1 || a->reserved2 || a->reserved3 ||
       (a->epi && a->epi->reserved_d1 != 0.0))
     { rc = QG_ERR_UNSUPPORTED; return 0; }
   P = TiledParams{};
@@ -1770,13 +1817,26 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   static const bool env_budget = getenv("QG_TILED_SMEM_KB") != nullptr;
   // TMEM columns: the widest accumulator (stage 1 or the chained stage 2)
   const int tcols = std::max(32, (int)P.slot_bn);     // TMEM allocations are >= 32 columns
-  const bool three = !env_budget && !P.chain && tcols <= 128 && a->total_ctas >= 3 * (int64_t)sms;
+  const bool three = !env_budget && !P.chain && tcols <= 128 && a->total_ctas >= 3 * (int64_t)sms &&
+                     (P.a_bits != 2 || P.bn <= 64);
   static const bool wide = getenv("QG_WIDE") == nullptr || atoi(getenv("QG_WIDE")) != 0;
   const size_t budget = three ? 72 * 1024 : smem_budget();
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned grid = (unsigned)a->total_ctas;
+  if (P.a_bits == 2) {
+    // A in tensor memory: the accumulator at columns [0, bn), the A ring of 32-column slots
+    // after it -- 3 CTAs/SM: 128 columns (bn <= 64, 2 slots); else 256 columns (4 slots)
+    if (three) {
+      P.a_col0 = 64; P.a_slots = 2;
+      launch_tiled<128, 3>(P, grid, smem, st);
+    } else {
+      P.a_col0 = 128; P.a_slots = 4;
+      launch_tiled<256, 2>(P, grid, smem, st);
+    }
+    return tstatus();
+  }
   if (P.chain) {
     // chained aggregate -> update: one tile per CTA.  A chained stage has half the CTAs of
     // the split-N stages it replaces and two epilogues per tile: with fewer tiles than

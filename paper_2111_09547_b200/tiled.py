@@ -345,6 +345,13 @@ PAIR_CHAIN = os.environ.get("QG_PAIR_CHAIN", "0") != "0"
 # into the ring slot during the main loop: 8x less adjacency traffic from HBM / L2.
 A_BITS = os.environ.get("QG_A_BITS", "0") == "1"
 
+# A in tensor memory (default; QG_A_TMEM=0 disables) for large non-chained adjacency
+# stages with N tiles <= 128 columns, where TMEM has room beside the accumulator: the
+# packed 2 KB blocks are expanded by four warps straight into TENSOR MEMORY (tcgen05.st)
+# and the MMAs read A from there (tcgen05.mma [d], [a], b): 8x less adjacency traffic and
+# no shared-memory traffic for A.
+A_TMEM = os.environ.get("QG_A_TMEM", "1") != "0"
+
 
 def use_pair_chain(b_npad: int, w_npad: int, row_blocks_total: int, sizes) -> bool:
     """Chained aggregate -> update stages on 2-SM CTA pairs (tc_pair_kernel<.., CHAIN>):
@@ -387,7 +394,7 @@ def launch(segs, *, a_blocks: bool, b_npad: int, n: int, mode: int, out_layout: 
     args.segs, args.nsegs, args.a_blocks, args.total_ctas = table.dev.data_ptr(), table.n, int(a_blocks), begin
     args.b_npad, args.n, args.bn, args.n_tiles = b_npad, n, bn, n_tiles
     args.mode, args.out_layout, args.out_npad = mode, out_layout, out_npad
-    args.a_bits = int(bool(a_blocks and a_bits))
+    args.a_bits = int(a_bits) if a_blocks else 0
     args.pair = int(pair)
     if epi_struct is not None:
         args.epi = ctypes.pointer(epi_struct)
