@@ -48,6 +48,8 @@ struct TiledParams {
   int32_t a_bits;           // a_blocks: the adjacency ships as PACKED 2 KB blocks, expanded in smem (1)
                             // or into tensor memory (2)
   int32_t a_slots, a_col0;  // a_bits 2: TMEM A ring slots (32 columns each) and its first column
+  int32_t persist;          // CTAs loop over work items (grid = resident CTAs); the producer
+                            // prefetches the next item's first K tiles during the epilogue
   int32_t dbg;              // QG_EPI_DBG knock-out bits (experiments): 1 no stores, 2 no math, 4 no TMEM loads
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
@@ -539,6 +541,7 @@ struct TileRing {
   uint32_t ndone;             // accumulator phases completed so far
   uint32_t ring_bytes;        // bytes of the ring (free for output staging after the last MMA)
   bool pdl_wait;              // griddepcontrol.wait still pending (PDL-launched single tile)
+  int pref;                   // producer: K tiles of the CURRENT tile already issued (persistent prefetch)
 };
 
 // Epilogue of one 128-row x bn tile held in this CTA's TMEM: 8-column slices over all
@@ -704,6 +707,13 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
   const int64_t rb = local / P.n_tiles;
   const int nt = (int)(local % P.n_tiles);
   const int64_t n0 = (int64_t)nt * bn;
+  // persistent: the next work item of this CTA (warp-cooperative lookup, all threads)
+  const int64_t next = tile + (int64_t)gridDim.x;
+  const bool has_next = P.persist && next < P.total_ctas;
+  const qg_tseg& Gn = P.segs[has_next ? find_seg(P.segs, P.nsegs, next) : 0];
+  const int64_t localn = has_next ? next - Gn.cta_begin : 0;
+  const int64_t rbn = localn / P.n_tiles;
+  const int64_t n0n = (int64_t)(localn % P.n_tiles) * bn;
 
   // stage = [A: 16 KB UMMA bytes][B: bn x 128 B]                       (bytes)
   //         [A: 16 KB UMMA bytes][B: bn x 128 B][2 KB packed bit block] (a_bits 1: A expanded in smem)
@@ -769,8 +779,8 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       }
       it_begin = pre;
     }
-    for (int it = it_begin; it < nk; ++it) {
-      const uint32_t g = it0 + (uint32_t)it;
+    // one K tile `it` of work item (Gx, rbx, n0x, kbasex) into ring position g
+    auto issue = [&](const qg_tseg& Gx, int64_t rbx, int64_t n0x, int kbasex, int it, uint32_t g) {
       const int s = (int)(g % (uint32_t)S);
       if (g >= (uint32_t)S) mbar_wait(smem_u32(&empty[s]), ((g / S) - 1) & 1);
       int kt;
@@ -778,16 +788,29 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
       uint8_t* dst = stage0 + (size_t)s * stage_bytes;
       if (abits || ats) {
         // 2 KB packed block -> staging; the expander warps build the operand (smem or TMEM)
-        kt = G.blk_kt[kbase + it];
+        kt = Gx.blk_kt[kbasex + it];
         mbar_expect_tx(&full[s], 2048u + b_bytes);
-        bulk_g2s(dst + bits_off, G.a + (int64_t)(kbase + it) * 2048, 2048u, &full[s]);
+        bulk_g2s(dst + bits_off, Gx.a + (int64_t)(kbasex + it) * 2048, 2048u, &full[s]);
       } else {
-        if (P.a_blocks) { kt = G.blk_kt[kbase + it]; asrc = G.a + (int64_t)(kbase + it) * 16384; }
-        else { kt = it; asrc = G.a + (int64_t)kt * (G.r128 << 7) + rb * 16384; }
+        if (P.a_blocks) { kt = Gx.blk_kt[kbasex + it]; asrc = Gx.a + (int64_t)(kbasex + it) * 16384; }
+        else { kt = it; asrc = Gx.a + (int64_t)kt * (Gx.r128 << 7) + rbx * 16384; }
         mbar_expect_tx(&full[s], a_bytes + b_bytes);
         bulk_g2s(dst, asrc, a_bytes, &full[s]);
       }
-      bulk_g2s(dst + a_bytes, bbase + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
+      bulk_g2s(dst + a_bytes, Gx.b + (n0x >> 3) * 1024 + (int64_t)kt * (P.b_npad << 7), b_bytes, &full[s]);
+    };
+    if (R.pref > it_begin) it_begin = R.pref;            // issued during the previous item's epilogue
+    R.pref = 0;
+    for (int it = it_begin; it < nk; ++it) issue(G, rb, n0, kbase, it, it0 + (uint32_t)it);
+    if (!CHAIN && has_next) {
+      // persistent: the next work item's first ring-full, behind this item's K tiles (the
+      // slots free up as this item's MMAs retire; no dependence on the epilogue)
+      int nnk, nkb = 0;
+      if (P.a_blocks) { nnk = Gn.blk_count[rbn]; nkb = Gn.blk_base[rbn]; }
+      else nnk = Gn.k_tiles;
+      const int pre = nnk < S ? nnk : S;
+      for (int j = 0; j < pre; ++j) issue(Gn, rbn, n0n, nkb, j, it0 + (uint32_t)nk + (uint32_t)j);
+      R.pref = pre;
     }
     if (CHAIN) {
       // stage 2's (static) right operand, one K tile per ring position after stage 1's;
@@ -959,6 +982,7 @@ __device__ __forceinline__ void tiled_tile(const TiledParams& P, int64_t tile, T
         atomicAdd(reinterpret_cast<unsigned long long*>(G.q_row_sums + rb * 128 + tid), R.sRowSum[tid]);
     }
   }
+  if (tid < 2) R.sOff[tid] = 0;                          // next work item re-derives its screen flags
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -1002,6 +1026,7 @@ __device__ __forceinline__ void tiled_setup(TileRing& R, uint8_t* smem, uint64_t
   R.it0 = 0;
   R.ndone = 0;
   R.pdl_wait = false;
+  R.pref = 0;
 }
 
 template <int TMEM_COLS, int MINB, int NT, bool CHAIN = false>
@@ -1030,7 +1055,10 @@ __global__ void __launch_bounds__(NT, MINB) tc_tiled_kernel(const __grid_constan
   // the predecessor grid's outputs (activations, row sums) are read only after
   // griddepcontrol.wait, issued per role inside the tile (static operands prefetch first)
   R.pdl_wait = true;
-  tiled_tile<TMEM_COLS, CHAIN>(P, (int64_t)blockIdx.x, R);
+  for (int64_t tile = blockIdx.x; tile < P.total_ctas; tile += gridDim.x) {
+    tiled_tile<TMEM_COLS, CHAIN>(P, tile, R);
+    if (!P.persist) break;
+  }
   if ((threadIdx.x >> 5) == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(R.tmem), "n"(TMEM_COLS));
 }
@@ -1618,6 +1646,16 @@ static void tiled_attr(size_t bytes) {
 template <int COLS, int MINB, int NT = kTThreads, bool CHAIN = false>
 static void launch_tiled(const TiledParams& P, unsigned grid, size_t smem, cudaStream_t st) {
   tiled_attr<COLS, MINB, NT, CHAIN>(smem);
+  if (P.persist) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const unsigned resident = (unsigned)(sms * MINB);
+    if (grid > resident) grid = resident;
+  }
   static const bool pdl = getenv("QG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1672,6 +1710,8 @@ static size_t tiled_params(const qg_tiled_args* a, TiledParams& P, int& rc) {
   P.screen = screen ? 1 : 0;
   static const int dbg = getenv("QG_EPI_DBG") ? atoi(getenv("QG_EPI_DBG")) : 0;
   P.dbg = dbg;
+  static const bool persist = getenv("QG_PERSIST") != nullptr && atoi(getenv("QG_PERSIST")) != 0;
+  P.persist = persist ? 1 : 0;
   if (a->chain) {
     const qg_chain* c = a->chain;
     // stage 1: one N tile covering all its columns, packed codes
