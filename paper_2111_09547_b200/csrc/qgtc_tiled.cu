@@ -1881,7 +1881,8 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
     // chained aggregate -> update: one tile per CTA.  A chained stage has half the CTAs of
     // the split-N stages it replaces and two epilogues per tile: with fewer tiles than
     // SMs, 16 warps (1 CTA/SM) split the epilogue slices 4 ways
-    const bool wide16 = a->total_ctas <= (int64_t)sms;
+    static const bool force16 = getenv("QG_CHAIN_16W") != nullptr && atoi(getenv("QG_CHAIN_16W")) != 0;
+    const bool wide16 = a->total_ctas <= (int64_t)sms || force16;
     static const bool chain_wide = getenv("QG_CHAIN_WIDE") != nullptr && atoi(getenv("QG_CHAIN_WIDE")) != 0;
     if (!wide16 && chain_wide && tcols == 256) {
       // 12 warps: 3 warp groups split the two epilogues' slices (opt-in, measured)
