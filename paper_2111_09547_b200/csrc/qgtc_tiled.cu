@@ -622,7 +622,11 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
       double a0 = rint(-beta * ia);
       const bool a0_ok = fabs(a0) <= 0x1p29;
       if (!a0_ok) a0 = 0.0;
-      S.on = __all_sync(QG_FULL, known && accmax < 0x1p30) && alpha > 0.0 && alpha < 0x1p60;
+      // CTA-uniform (the staged code stores below rely on it); a warp whose rows could
+      // overflow the integer shift (acc >= 2^30) or lack row sums sends every element to
+      // the exact path instead (margin +inf)
+      const bool warp_ok = __all_sync(QG_FULL, known && accmax < 0x1p30);
+      S.on = alpha > 0.0 && alpha < 0x1p60;
       if (S.on) {
         const uint32_t maxv = (1u << E.q_bits) - 1u;
         float lo = 0.5f;
@@ -637,8 +641,8 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
         // sends every element of the row to the exact path, -1 (rows past m) none
         const double margin = (2.0 * alpha + (double)maxv * 0x1p-20) * 0x1p-21 + 0x1p-40;
         S.mrg = !rvalid ? -1.0f
-                        : (a0_ok && margin < 0.125 && fabs(q0) < 0x1p20) ? __double2float_ru(margin)
-                                                                         : __int_as_float(0x7f800000);
+                        : (warp_ok && a0_ok && margin < 0.125 && fabs(q0) < 0x1p20) ? __double2float_ru(margin)
+                                                                                    : __int_as_float(0x7f800000);
         S.a0r = (int32_t)a0;
         S.dr = (float)(beta + a0 * alpha);
         S.alpha = (float)alpha;
