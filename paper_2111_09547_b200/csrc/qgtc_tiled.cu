@@ -300,6 +300,65 @@ __device__ __forceinline__ bool screen1(const ScreenRow& S, uint32_t acc, int32_
   return (d < m) | (d > 1.0f - m);
 }
 
+// Two elements of screen1 with the fp32 adds/FMAs in packed f32x2 form (FFMA2 / FADD2: one
+// issue slot per pair; lane-wise the same IEEE operations and roundings as screen1, so the
+// estimates, floors and flags are bit-identical to it -- the deferred pass re-derives them
+// with screen1).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2add_rm(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+template <bool ROW_ONLY>
+__device__ __forceinline__ bool screen2(const ScreenRow& S, uint32_t acc0, uint32_t acc1, int32_t a0c0, int32_t a0c1,
+                                        float dc0, float dc1, uint32_t& f0, uint32_t& f1) {
+  const int32_t sh0 = ROW_ONLY ? (int32_t)acc0 - S.a0r : (int32_t)acc0 - S.a0r - a0c0;
+  const int32_t sh1 = ROW_ONLY ? (int32_t)acc1 - S.a0r : (int32_t)acc1 - S.a0r - a0c1;
+  uint64_t y = f2fma(f2pack((float)sh0, (float)sh1), f2pack(S.alpha, S.alpha), f2pack(S.dr, S.dr));
+  if (!ROW_ONLY) y = f2add(y, f2pack(dc0, dc1));
+  float y0, y1;
+  f2unpack(y, y0, y1);
+  y0 = fminf(fmaxf(y0, S.lo), S.hi);
+  y1 = fminf(fmaxf(y1, S.lo), S.hi);
+  y = f2pack(y0, y1);
+  const uint64_t C = f2pack(12582912.0f, 12582912.0f);
+  const uint64_t fl = f2add_rm(y, C);                       // 1.5 * 2^23 + floor(y)
+  const uint64_t d = f2sub(y, f2sub(fl, C));                // y - floor(y), exact
+  const uint64_t m = f2fma(y, f2pack(0x1p-21f, 0x1p-21f), f2pack(S.mrg, S.mrg));
+  const uint64_t om = f2sub(f2pack(1.0f, 1.0f), m);
+  float d0, d1, m0, m1, o0, o1, l0, l1;
+  f2unpack(d, d0, d1);
+  f2unpack(m, m0, m1);
+  f2unpack(om, o0, o1);
+  f2unpack(fl, l0, l1);
+  f0 = __float_as_uint(l0);
+  f1 = __float_as_uint(l1);
+  return (d0 < m0) | (d0 > o0) | (d1 < m1) | (d1 > o1);
+}
+
 template <bool ROW_ONLY, int ST, int LAYOUT>
 __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg& G, const EpiLane& L,
                                              const double* __restrict__ sCol, double rterm, uint8_t* mid0,
@@ -344,7 +403,9 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
       for (int jj = 0; jj < 8; ++jj) t[jj] = v[jj];
     } else {
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) bad |= screen1<ROW_ONLY>(S, v[jj], ROW_ONLY ? 0 : a0[jj], ROW_ONLY ? 0.f : dc[jj], t[jj]);
+      for (int jj = 0; jj < 8; jj += 2)
+        bad |= screen2<ROW_ONLY>(S, v[jj], v[jj + 1], ROW_ONLY ? 0 : a0[jj], ROW_ONLY ? 0 : a0[jj + 1],
+                                 ROW_ONLY ? 0.f : dc[jj], ROW_ONLY ? 0.f : dc[jj + 1], t[jj], t[jj + 1]);
     }
     if (bad) {
       deferred |= 1u << k;
