@@ -121,6 +121,7 @@ struct ScreenRow {
   float dr;         // delta_r
   float alpha;
   float mrg;        // margin; -1: invalid row (never exact), +inf: always exact
+  float hc;         // RN(0.5 - mrg): the flag test is |frac(y) - 1/2| > RN(hc - 2^-21 y)
   float lo, hi;     // clamp bounds: max(q0, 0.5) (ReLU) or 0.5; maxv + 0.5
   const int32_t* sA0;  // per column acc0_c (row-only stages: unused)
   const float* sD;     // per column delta_c
@@ -295,9 +296,12 @@ __device__ __forceinline__ bool screen1(const ScreenRow& S, uint32_t acc, int32_
   y = fminf(fmaxf(y, S.lo), S.hi);
   const float fl = __fadd_rd(y, 12582912.0f);              // 1.5 * 2^23 + floor(y)
   const float d = y - (fl - 12582912.0f);                  // y - floor(y), exact
-  const float m = fmaf(y, 0x1p-21f, S.mrg);                // y >= 0.5 > 0 after the clamp
+  // distance to the nearest integer 1/2 - |d - 1/2| (d - 1/2 exact: d is a multiple of
+  // ulp(y) >= 2^-24) against the margin; h = 1/2 - margin within 2^-25, the margin's slack
+  // over the error bound is >= 2^-23
+  const float h = fmaf(y, -0x1p-21f, S.hc);                // y >= 0.5 > 0 after the clamp
   f = __float_as_uint(fl);
-  return (d < m) | (d > 1.0f - m);
+  return fabsf(d - 0.5f) > h;
 }
 
 // Two elements of screen1 with the fp32 adds/FMAs in packed f32x2 form (FFMA2 / FADD2: one
@@ -347,16 +351,15 @@ __device__ __forceinline__ bool screen2(const ScreenRow& S, uint32_t acc0, uint3
   const uint64_t C = f2pack(12582912.0f, 12582912.0f);
   const uint64_t fl = f2add_rm(y, C);                       // 1.5 * 2^23 + floor(y)
   const uint64_t d = f2sub(y, f2sub(fl, C));                // y - floor(y), exact
-  const uint64_t m = f2fma(y, f2pack(0x1p-21f, 0x1p-21f), f2pack(S.mrg, S.mrg));
-  const uint64_t om = f2sub(f2pack(1.0f, 1.0f), m);
-  float d0, d1, m0, m1, o0, o1, l0, l1;
-  f2unpack(d, d0, d1);
-  f2unpack(m, m0, m1);
-  f2unpack(om, o0, o1);
+  const uint64_t e = f2sub(d, f2pack(0.5f, 0.5f));
+  const uint64_t h = f2fma(y, f2pack(-0x1p-21f, -0x1p-21f), f2pack(S.hc, S.hc));
+  float e0, e1, h0, h1, l0, l1;
+  f2unpack(e, e0, e1);
+  f2unpack(h, h0, h1);
   f2unpack(fl, l0, l1);
   f0 = __float_as_uint(l0);
   f1 = __float_as_uint(l1);
-  return (d0 < m0) | (d0 > o0) | (d1 < m1) | (d1 > o1);
+  return (fabsf(e0) > h0) | (fabsf(e1) > h1);
 }
 
 template <bool ROW_ONLY, int ST, int LAYOUT>
@@ -704,6 +707,7 @@ __device__ __forceinline__ void tile_epilogue(const TiledParams& P, const qg_tse
         S.mrg = !rvalid ? -1.0f
                         : (warp_ok && a0_ok && margin < 0.125 && fabs(q0) < 0x1p20) ? __double2float_ru(margin)
                                                                                     : __int_as_float(0x7f800000);
+        S.hc = 0.5f - S.mrg;
         S.a0r = (int32_t)a0;
         S.dr = (float)(beta + a0 * alpha);
         S.alpha = (float)alpha;
