@@ -50,7 +50,8 @@ struct TiledParams {
   int32_t a_slots, a_col0;  // a_bits 2: TMEM A ring slots (32 columns each) and its first column
   int32_t persist;          // CTAs loop over work items (grid = resident CTAs); the producer
                             // prefetches the next item's first K tiles during the epilogue
-  int32_t dbg;              // QG_EPI_DBG knock-out bits (experiments): 1 no stores, 2 no math, 4 no TMEM loads
+  int32_t dbg;              // QG_EPI_DBG knock-out bits (experiments; screened epilogue only, built with
+                            // -DQG_EPI_KNOCKOUTS): 1 no stores, 2 no math, 4 no TMEM loads
   // chained stage 2 (qg_tiled_args.chain): a dense GEMM over this stage's requantized
   // codes, which never leave shared memory; one CTA per row block (n_tiles 1).
   int32_t chain, bn2, k2, out_layout2;
@@ -285,6 +286,29 @@ __device__ __forceinline__ void epi_store(const EpiLane& L, uint8_t* q_codes, in
   }
 }
 
+// Main-loop store of one full 8-column slice of a VALID row (rows past m and ragged slices
+// go through the deferred pass): per-row bases precomputed by epi_fast, 32-bit column math.
+// LAYOUT 0: shared-memory address (ms0 / ms1: the two 128-column K slots of stage 2's left
+// operand at this row); 1: rowp = this row's left-tiled base, slab = bytes per 128 K
+// columns; 2: rowp = this row's right-tiled base (K = row).
+template <int LAYOUT>
+__device__ __forceinline__ void epi_store_fast(uint8_t* rowp, uint32_t ms0, uint32_t ms1, int64_t slab, int c,
+                                               uint2 w) {
+  if (LAYOUT == 0) {
+    const uint32_t a = ((c >> 7) ? ms1 : ms0) + (uint32_t)(((c & 127) >> 4) * 128 + (c & 15));
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(a), "r"(w.x), "r"(w.y) : "memory");
+  } else if (LAYOUT == 1) {
+    *reinterpret_cast<uint2*>(rowp + (int64_t)(c >> 7) * slab + (((c & 127) >> 4) * 128 + (c & 15))) = w;
+  } else {
+    uint8_t* base = rowp + (int64_t)(c >> 3) * 1024;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      base[jj * 16] = (uint8_t)(w.x >> (8 * jj));
+      base[(jj + 4) * 16] = (uint8_t)(w.y >> (8 * jj));
+    }
+  }
+}
+
 // Screened estimate of one element: clamped fp32 y (floor bits in *f) and whether it is
 // within the per-element margin 2^-21 (|y| + 2 alpha) of an integer (>= 2x the error bound
 // 2^-24 (4 |Y| + 3 alpha) of ScreenRow).
@@ -379,32 +403,51 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
   const int64_t r128 = G.r128;
   const int nval = L.rvalid ? L.nvalid : 0;
   uint32_t rsum = 0, deferred = 0;
+  // loop-invariant per-row bases (the slice loop only adds 32-bit column offsets)
+  uint8_t* const rowp = q_codes + rbase;
+  const int64_t slab = r128 << 7;
+  const int n0i = (int)L.n0;
+  uint32_t ms0 = 0, ms1 = 0;
+  if (LAYOUT == 0) {
+    const uint32_t ro = (uint32_t)((lrow >> 3) * 1024 + (lrow & 7) * 16);
+    ms0 = smem_u32(mid0) + ro;
+    ms1 = smem_u32(mid1) + ro;
+  }
+  const uint32_t sA0 = ROW_ONLY ? 0u : smem_u32(S.sA0), sD = ROW_ONLY ? 0u : smem_u32(S.sD);
   int k = 0;
   for (int sl = L.first; sl < L.nslices; sl += L.step, ++k) {
     const int cl8 = sl * 8;
     uint32_t v[8];
+#ifdef QG_EPI_KNOCKOUTS
     if (P.dbg & 4) {
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) v[jj] = (uint32_t)(cl8 * 131 + jj * 17 + lrow);
-    } else {
+    } else
+#endif
       L.load8(cl8, v);
-    }
     int32_t a0[8];
     float dc[8];
     if (!ROW_ONLY) {
-      const int4 x0 = *reinterpret_cast<const int4*>(S.sA0 + cl8);
-      const int4 x1 = *reinterpret_cast<const int4*>(S.sA0 + cl8 + 4);
-      const float4 z0 = *reinterpret_cast<const float4*>(S.sD + cl8);
-      const float4 z1 = *reinterpret_cast<const float4*>(S.sD + cl8 + 4);
-      a0[0] = x0.x; a0[1] = x0.y; a0[2] = x0.z; a0[3] = x0.w; a0[4] = x1.x; a0[5] = x1.y; a0[6] = x1.z; a0[7] = x1.w;
-      dc[0] = z0.x; dc[1] = z0.y; dc[2] = z0.z; dc[3] = z0.w; dc[4] = z1.x; dc[5] = z1.y; dc[6] = z1.z; dc[7] = z1.w;
+      uint32_t x[8], z[8];
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(sA0 + cl8 * 4));
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]) : "r"(sA0 + cl8 * 4 + 16));
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(z[0]), "=r"(z[1]), "=r"(z[2]), "=r"(z[3]) : "r"(sD + cl8 * 4));
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(z[4]), "=r"(z[5]), "=r"(z[6]), "=r"(z[7]) : "r"(sD + cl8 * 4 + 16));
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        a0[jj] = (int32_t)x[jj];
+        dc[jj] = __uint_as_float(z[jj]);
+      }
     }
     uint32_t t[8];
     bool bad = cl8 + 8 > nval;                               // ragged slice or row past m
+#ifdef QG_EPI_KNOCKOUTS
     if (P.dbg & 2) {
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) t[jj] = v[jj];
-    } else {
+    } else
+#endif
+    {
 #pragma unroll
       for (int jj = 0; jj < 8; jj += 2)
         bad |= screen2<ROW_ONLY>(S, v[jj], v[jj + 1], ROW_ONLY ? 0 : a0[jj], ROW_ONLY ? 0 : a0[jj + 1],
@@ -419,7 +462,10 @@ __device__ __forceinline__ uint32_t epi_fast(const TiledParams& P, const qg_tseg
     w.y = __byte_perm(__byte_perm(t[4], t[5], 0x0040), __byte_perm(t[6], t[7], 0x0040), 0x5410);
     rsum = __dp4a(w.x, 0x01010101u, rsum);
     rsum = __dp4a(w.y, 0x01010101u, rsum);
-    if (!(P.dbg & 1)) epi_store<ROW_ONLY, ST, LAYOUT>(L, q_codes, r128, rbase, lrow, mid0, mid1, cl8, w, true);
+#ifdef QG_EPI_KNOCKOUTS
+    if (P.dbg & 1) continue;
+#endif
+    epi_store_fast<LAYOUT>(rowp, ms0, ms1, slab, n0i + cl8, w);
   }
   // ---- deferred slices (warp-uniform walk: tcgen05.ld is collective): screened codes
   // again, the exact fp64 path only for the flagged elements, zeros past the valid region
