@@ -1613,7 +1613,7 @@ __global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t
 }
 
 // Grouped entry conversion: row-wise feature planes of all batches -> tiled u8 codes.  Unit =
-// 256 rows (8 plane words per column) x 128 columns; thread t < 128 owns column c0 + t and
+// 256 rows (8 plane words per column) x 128 columns; thread t (128 per CTA) owns column c0 + t and
 // reads, per plane, its 8 consecutive row words with two 16-byte loads (one 32-B sector),
 // then expands them into 256 code bytes (bit i of plane p -> bit p of byte i).
 // Right-tiled (K = rows): every 32 rows of column c are two 16-byte K-cores -> direct
@@ -1621,7 +1621,7 @@ __global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t
 // thread stores 16-byte K-cores of rows; row code sums reduce over the unit's 128 columns
 // before one atomic per row.
 template <int kEntryWords>                              // row words (x 32 rows) per unit: 8 or 1
-__global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
+__global__ void __launch_bounds__(128, 4) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
                                                           int nplanes, int right) {
   // the first GEMM (PDL-launched) may start its prologue + static-operand prefetch now;
   // it reads this kernel's output only after griddepcontrol.wait
@@ -1694,9 +1694,9 @@ __global__ void __launch_bounds__(256) entry_tiles_kernel(const qg_entry_seg* __
   }
   if (right) return;
   __syncthreads();
-  // 256 rows x 8 K-cores = 2048 16-byte stores, 8 per thread; the 8 cores of a row are 8
+  // 256 rows x 8 K-cores = 2048 16-byte stores, 16 per thread; the 8 cores of a row are 8
   // consecutive lanes (row sums reduce over them)
-  for (int idx = t; idx < 32 * kEntryWords * 8; idx += 256) {
+  for (int idx = t; idx < 32 * kEntryWords * 8; idx += 128) {
     const int r = idx >> 3, core = idx & 7;
     const int64_t row = vb * 32 + r, k = cg * 128 + core * 16;
     const uint4 q = *reinterpret_cast<const uint4*>(&tile[r][core * 16]);
@@ -1729,7 +1729,7 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
   static const bool pdl = getenv("QG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)total_units);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(128);          // one thread per column of the unit; 4 CTAs per SM
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
