@@ -1974,7 +1974,7 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
   const int tcols = std::max(32, (int)P.slot_bn);     // TMEM allocations are >= 32 columns
   const bool three = !env_budget && !P.chain && tcols <= 128 && a->total_ctas >= 3 * (int64_t)sms &&
                      (P.a_bits != 2 || P.bn <= 64);
-  static const bool wide = getenv("QG_WIDE") == nullptr || atoi(getenv("QG_WIDE")) != 0;
+  static const bool wide = getenv("QG_WIDE") != nullptr && atoi(getenv("QG_WIDE")) != 0;
   const size_t budget = three ? 72 * 1024 : smem_budget();
   P.stages = (int32_t)std::max<size_t>(2, std::min<size_t>(8, (budget - cols) / stage));
   const size_t smem = (size_t)P.stages * stage + cols;
@@ -2029,8 +2029,9 @@ extern "C" int qg_tiled_gemm(const qg_tiled_args* a, void* stream) {
       case 64: launch_tiled<64, 2>(P, grid, smem, st); break;
       case 128: launch_tiled<128, 2>(P, grid, smem, st); break;
       default:
-        // 12 warps for the epilogue-bound dense-left (update) GEMMs: the 128x256 epilogue's
-        // latency-bound fp64 chains spread over 3 warp groups (C4 update stages -3.5%)
+        // QG_WIDE=1: 12 warps (80 registers) for the epilogue-bound dense-left (update) GEMMs.
+        // It paid off for the fp64 epilogue (C4 -3.5%); with the lean screened epilogue the
+        // 8-warp, 128-register variant is faster (C4 first update 1.06 -> 0.96 ms, r04h)
         if (wide && !P.a_blocks && !P.chain && P.mode == QG_GEMM_EPILOGUE) launch_tiled<256, 2, 384>(P, grid, smem, st);
         else launch_tiled<256, 2>(P, grid, smem, st);
         break;

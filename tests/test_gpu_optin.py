@@ -6,7 +6,8 @@ each switch set (the switches are read once at import / first launch).
 * QG_A_BITS=1: packed 2 KB adjacency blocks expanded in shared memory by the GEMM;
 * QG_A_TMEM=0: the default A-from-TMEM stages back on pre-expanded byte blocks;
 * QG_NO_SCREEN=1: every requant element on the exact fp64 path;
-* QG_PERSIST=1: resident CTAs loop over work items with next-item prefetch.
+* QG_PERSIST=1: resident CTAs loop over work items with next-item prefetch;
+* QG_WIDE=1: 12-warp CTAs for the dense update stages.
 """
 
 from __future__ import annotations
@@ -22,7 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("switch,value", [("QG_PAIR_CHAIN", "1"), ("QG_A_BITS", "1"), ("QG_A_TMEM", "0"), ("QG_NO_SCREEN", "1"),
-                                          ("QG_PERSIST", "1")])
+                                          ("QG_PERSIST", "1"), ("QG_WIDE", "1")])
 def test_optin_path_config_parity(switch, value):
     env = dict(os.environ)
     env[switch] = value
