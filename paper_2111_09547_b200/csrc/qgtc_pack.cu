@@ -98,7 +98,7 @@ static __device__ __noinline__ uint32_t requant_slow(SrcT x, double amin, double
 constexpr int kRowTileCols = 32, kRowTileGroups = 8;
 
 template <typename SrcT, int BITS>
-__global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
+__global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
     const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale, double inv,
     int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
     int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base, int single_tile) {
@@ -122,13 +122,26 @@ __global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
   if (v < wpc) {
     const int64_t rbase = v * 32;
     const SrcT* colp = src + rbase * ld + c;
-    for (int i0 = 0; i0 < 32; i0 += 8) {
+    // the loads of kPre 8-row steps are issued before any of them is processed (4 KB per
+    // warp in flight for fp32 sources instead of 1 KB: the kernel is HBM-latency bound)
+    constexpr int kPre = sizeof(SrcT) >= 8 ? 2 : 4;
+#pragma unroll
+    for (int s0 = 0; s0 < 4; s0 += kPre) {
+    SrcT xs[kPre][8];
+#pragma unroll
+    for (int s = 0; s < kPre; ++s) {
+      const int64_t left = rows - (rbase + (s0 + s) * 8);
+      const int nk = left <= 0 ? 0 : (left < 8 ? (int)left : 8);
+      const SrcT* p0 = colp + (int64_t)(s0 + s) * 8 * ld;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xs[s][k] = (cok && k < nk) ? p0[(int64_t)k * ld] : SrcT(0);
+    }
+#pragma unroll
+    for (int s = 0; s < kPre; ++s) {
+      const int i0 = (s0 + s) * 8;
       const int64_t left = rows - (rbase + i0);
       const int nk = left <= 0 ? 0 : (left < 8 ? (int)left : 8);   // valid rows of this step
-      const SrcT* p0 = colp + (int64_t)i0 * ld;
-      SrcT x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) x[k] = (cok && k < nk) ? p0[(int64_t)k * ld] : SrcT(0);
+      const SrcT* x = xs[s];
       uint32_t q[8];
       uint32_t fm = 0u;                                   // elements needing the exact path
 #pragma unroll
@@ -182,6 +195,7 @@ __global__ void __launch_bounds__(256, 4) quantize_pack_row_vec_kernel(
       const uint64_t t = transpose8x8(((uint64_t)hi << 32) | lo);
 #pragma unroll
       for (int p = 0; p < BITS; ++p) word[p] |= (uint32_t)((t >> (8 * p)) & 0xFFu) << i0;
+    }
     }
     if (row_sums) {
       const int64_t r = v * 32 + lane;

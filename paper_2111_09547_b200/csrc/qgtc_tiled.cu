@@ -1621,7 +1621,7 @@ __global__ void tiles_to_codes_kernel(const uint8_t* __restrict__ tiles, int64_t
 // thread stores 16-byte K-cores of rows; row code sums reduce over the unit's 128 columns
 // before one atomic per row.
 template <int kEntryWords>                              // row words (x 32 rows) per unit: 8 or 1
-__global__ void __launch_bounds__(128, 4) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
+__global__ void __launch_bounds__(128, 5) entry_tiles_kernel(const qg_entry_seg* __restrict__ segs, int nsegs,
                                                           int nplanes, int right) {
   // the first GEMM (PDL-launched) may start its prologue + static-operand prefetch now;
   // it reads this kernel's output only after griddepcontrol.wait
@@ -1729,7 +1729,7 @@ extern "C" int qg_entry_tiles(const qg_entry_seg* segs, int32_t nsegs, int32_t n
   static const bool pdl = getenv("QG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)total_units);
-  cfg.blockDim = dim3(128);          // one thread per column of the unit; 4 CTAs per SM
+  cfg.blockDim = dim3(128);          // one thread per column of the unit; 5 CTAs per SM
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -62,7 +62,7 @@ def run_bitqnt(rows: int, cols: int, bits: int, reps: int = 10, hbm_peak: float 
     return {"rows": rows, "cols": cols, "bits": bits, "ms": round(ms, 4), "bytes": nbytes,
             "achieved_gbs": round(gbs, 1), "peak_gbs": hbm_peak, "frac": round(gbs / hbm_peak, 4),
             "row_sums_sampled": "exact" if exact else "MISMATCH",
-            "kernel": "quantize_pack_row_vec_kernel (lane = column, 128-B coalesced row loads 8 deep, division-free exact requant, 8x8 bit transposes, redux.sync row sums, smem-staged 32-B plane stores)"}
+            "kernel": "quantize_pack_row_vec_kernel (lane = column, 128-B coalesced row loads, 32 rows in flight per warp, division-free exact requant, 8x8 bit transposes, redux.sync row sums, smem-staged 32-B plane stores)"}
 
 
 if __name__ == "__main__":
