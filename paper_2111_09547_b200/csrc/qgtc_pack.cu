@@ -101,12 +101,16 @@ template <typename SrcT, int BITS>
 __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
     const SrcT* __restrict__ src, int64_t rows, int64_t cols, int64_t ld, double amin, double scale, double inv,
     int64_t prows, int64_t pcols, uint32_t* __restrict__ planes, uint8_t* __restrict__ codes,
-    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base, int single_tile) {
+    int64_t* __restrict__ row_sums, int64_t* status, int64_t status_base, int64_t ncolt) {
   __shared__ uint32_t sw[BITS][kRowTileCols][kRowTileGroups + 1];
+  const bool single_tile = ncolt == 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wpc = prows >> 5;                          // words per column (row groups)
-  const int64_t v0 = (int64_t)blockIdx.x * kRowTileGroups, v = v0 + warp;
-  const int64_t c = (int64_t)blockIdx.y * kRowTileCols + lane;
+  // 1-D grid, column tiles fastest: the CTAs covering one row band run together, so the
+  // sectors shared by neighbouring (unaligned) column tiles come from L2, not HBM twice
+  const int64_t rt = (int64_t)blockIdx.x / ncolt, ct = (int64_t)blockIdx.x % ncolt;
+  const int64_t v0 = rt * kRowTileGroups, v = v0 + warp;
+  const int64_t c = ct * kRowTileCols + lane;
   const bool cok = c < cols;
   const uint32_t maxv = (1u << BITS) - 1u;
   uint32_t word[BITS];
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
   // scale) (x is exact in fp64); elements within 2^-21 (|y| + |c|) of a code boundary,
   // and non-finite ones, take the exact fp64 path (requant_slow)
   const float inv32 = (float)inv, c32 = (float)(-amin * inv);
-  const float mc = fabsf(c32) * 0x1p-21f + 0x1p-40f, hic = (float)maxv + 0.5f;
+  const float mc = fabsf(c32) * 0x1p-21f + 0x1p-40f, hic = (float)maxv + 0.5f, hc = 0.5f - mc;
   if (v < wpc) {
     const int64_t rbase = v * 32;
     const SrcT* colp = src + rbase * ld + c;
@@ -143,20 +147,72 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
       const int nk = left <= 0 ? 0 : (left < 8 ? (int)left : 8);   // valid rows of this step
       const SrcT* x = xs[s];
       uint32_t q[8];
+      uint32_t lo, hi;
+      if constexpr (sizeof(SrcT) == 4) {
+        // per element: FFMA y, 2 FMNMX, FADD.RM floor, 2 FADD frac, FADD frac - 1/2 (exact:
+        // frac is a multiple of ulp(yc) >= 2^-24), FFMA h = RN(1/2 - mc) - 2^-21 yc (within
+        // 2^-25 of 1/2 - margin; the margin's slack over the error bound is >= 3 * 2^-24),
+        // one FSETP |frac - 1/2| > h; non-finite inputs through an FFMA chain (x * 0 is NaN
+        // iff x is not finite)
+        uint32_t f[8];
+        bool bad = false;
+        float nf = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float y = fmaf((float)x[k], inv32, c32);
+          const float yc = fminf(fmaxf(y, 0.5f), hic);
+          const float fl = __fadd_rd(yc, 12582912.0f);     // 1.5 * 2^23 + floor(yc)
+          const float d = yc - (fl - 12582912.0f);
+          const float h = fmaf(yc, -0x1p-21f, hc);
+          f[k] = __float_as_uint(fl);
+          bad |= fabsf(d - 0.5f) > h;
+          nf = fmaf((float)x[k], 0.f, nf);
+        }
+        bad |= !(nf == 0.f);
+        if (bad && cok) {
+          // rare: recheck per element; near-boundary / out-of-range / non-finite ones take
+          // the exact path (out of line)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float y = fmaf((float)x[k], inv32, c32);
+            const float yc = fminf(fmaxf(y, 0.5f), hic);
+            const float d = yc - (__uint_as_float(f[k]) - 12582912.0f);
+            const bool fk = (fabsf(d - 0.5f) > fmaf(yc, -0x1p-21f, hc)) |
+                            !(fabsf((float)x[k]) <= 3.4028234663852886e38f);
+            if (fk && k < nk)
+              f[k] = (f[k] & ~0xFFFFu) |
+                     requant_slow<SrcT>(x[k], amin, scale, inv, maxv, status, status_base + (rbase + i0 + k) * cols + c);
+          }
+        }
+        if (!(cok && nk == 8)) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (!(cok && k < nk)) f[k] &= ~0xFFFFu;
+        }
+        // the low 16 bits of f are the code (byte 1 is zero): pairs for the row sums, then
+        // the 4-code words
+        uint32_t pr[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pr[k] = __byte_perm(f[2 * k], f[2 * k + 1], 0x5410);
+        lo = __byte_perm(pr[0], pr[1], 0x6420);
+        hi = __byte_perm(pr[2], pr[3], 0x6420);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t sum = __reduce_add_sync(QG_FULL, pr[k]);
+          if (lane == i0 + 2 * k) my_sum = sum & 0xFFFFu;
+          if (lane == i0 + 2 * k + 1) my_sum = sum >> 16;
+        }
+        if (codes) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) q[k] = f[k] & 0xFFu;
+        }
+      } else {
       uint32_t fm = 0u;                                   // elements needing the exact path
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if constexpr (sizeof(SrcT) == 1) {
           q[k] = (uint32_t)x[k];
           fm |= (uint32_t)(q[k] > maxv) << k;
-        } else if constexpr (sizeof(SrcT) == 4) {
-          const float y = fmaf((float)x[k], inv32, c32);
-          const float yc = fminf(fmaxf(y, 0.5f), hic);
-          const float f = __fadd_rd(yc, 12582912.0f);      // 1.5 * 2^23 + floor(yc)
-          const float d = yc - (f - 12582912.0f);
-          const float m = fmaf(yc, 0x1p-21f, mc);
-          q[k] = __float_as_uint(f) & 0x1FFu;
-          fm |= (uint32_t)((d < m) | (d > 1.0f - m) | !(fabsf((float)x[k]) <= 3.4028234663852886e38f)) << k;
         } else {
           const R12 rq = quantize_code_r12_tight((double)x[k], amin, inv, maxv);
           q[k] = rq.code;
@@ -164,14 +220,15 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
         }
       }
       if (fm && cok) {
-        // rare: near-boundary / out-of-range / non-finite elements (out of line)
+        // rare: out-of-range / near-boundary / non-finite elements (out of line)
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (((fm >> k) & 1u) && k < nk)
             q[k] = requant_slow<SrcT>(x[k], amin, scale, inv, maxv, status,
                                       status_base + (rbase + i0 + k) * cols + c);
       }
-      uint32_t lo = 0u, hi = 0u;
+      lo = 0u;
+      hi = 0u;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (!(cok && k < nk)) q[k] = 0u;
@@ -184,6 +241,7 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
         const uint32_t sum = __reduce_add_sync(QG_FULL, q[k] | (q[k + 1] << 16));
         if (lane == i0 + k) my_sum = sum & 0xFFFFu;
         if (lane == i0 + k + 1) my_sum = sum >> 16;
+      }
       }
       if (codes && cok) {
         uint8_t* cp = codes + (rbase + i0) * cols + c;
@@ -209,7 +267,7 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
   for (int p = 0; p < BITS; ++p) sw[p][lane][warp] = word[p];
   __syncthreads();
   // plane p, column c0 + cc, row group v0 + w: word p * wpp + (c0 + cc) * wpc + v0 + w
-  const int64_t wpp = pcols * wpc, c0 = (int64_t)blockIdx.y * kRowTileCols;
+  const int64_t wpp = pcols * wpc, c0 = ct * kRowTileCols;
   for (int idx = threadIdx.x; idx < BITS * kRowTileCols * kRowTileGroups; idx += blockDim.x) {
     const int w = idx & 7, cc = (idx >> 3) & 31, p = idx >> 8;
     const int64_t col = c0 + cc, vg = v0 + w;
@@ -250,11 +308,11 @@ int launch_quantize_pack(const SrcT* src, int64_t rows, int64_t cols, int64_t ld
       quantize_pack_col_kernel<SrcT, BITS><<<(unsigned)blocks, 256, 0, st>>>(
           src, rows, cols, ld, amin, scale, prows, pcols, planes, codes, row_sums, status, status_base);
     else {
-      const dim3 grid((unsigned)(((prows >> 5) + kRowTileGroups - 1) / kRowTileGroups),
-                      (unsigned)((pcols + kRowTileCols - 1) / kRowTileCols));
-      quantize_pack_row_vec_kernel<SrcT, BITS><<<grid, 256, 0, st>>>(
+      const int64_t nrowt = ((prows >> 5) + kRowTileGroups - 1) / kRowTileGroups;
+      const int64_t ncolt = (pcols + kRowTileCols - 1) / kRowTileCols;
+      quantize_pack_row_vec_kernel<SrcT, BITS><<<(unsigned)(nrowt * ncolt), 256, 0, st>>>(
           src, rows, cols, ld, amin, scale, 1.0 / scale, prows, pcols, planes, codes, row_sums, status, status_base,
-          (int)(grid.y == 1));
+          ncolt);
     }
   }
   if (col_sums && cols > 0 && rows > 0)
