@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
   uint32_t word[BITS];
 #pragma unroll
   for (int p = 0; p < BITS; ++p) word[p] = 0u;
-  uint32_t my_sum = 0;                                     // lane i: row 32v + i
+  uint32_t my_pair = 0;                                    // lane i: rows 32v + (i & ~1) + {0, 1}
+  uint32_t tlo[4] = {0u, 0u, 0u, 0u}, thi[4] = {0u, 0u, 0u, 0u};   // transposed 8-row steps
   // fp32 sources: an fp32 screen y = fma(x, RN32(1/scale), RN32(-amin/scale)) with
   // |y - q| <= 2^-24 (2|y| + 2|c|) against the reference quotient q = RN(RN(x - amin) /
   // scale) (x is exact in fp64); elements within 2^-21 (|y| + |c|) of a code boundary,
@@ -199,8 +200,7 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint32_t sum = __reduce_add_sync(QG_FULL, pr[k]);
-          if (lane == i0 + 2 * k) my_sum = sum & 0xFFFFu;
-          if (lane == i0 + 2 * k + 1) my_sum = sum >> 16;
+          if ((lane >> 1) == (i0 >> 1) + k) my_pair = sum;
         }
         if (codes) {
 #pragma unroll
@@ -239,8 +239,7 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
       for (int k = 0; k < 8; k += 2) {
         // rows i0 + k and i0 + k + 1 in the two 16-bit halves (sum <= 32 * 255 < 2^16)
         const uint32_t sum = __reduce_add_sync(QG_FULL, q[k] | (q[k + 1] << 16));
-        if (lane == i0 + k) my_sum = sum & 0xFFFFu;
-        if (lane == i0 + k + 1) my_sum = sum >> 16;
+        if ((lane >> 1) == ((i0 + k) >> 1)) my_pair = sum;
       }
       }
       if (codes && cok) {
@@ -251,10 +250,18 @@ __global__ void __launch_bounds__(256, 3) quantize_pack_row_vec_kernel(
       }
       // byte p of t = plane p of the 8 rows (bit k = row i0 + k)
       const uint64_t t = transpose8x8(((uint64_t)hi << 32) | lo);
+      tlo[s0 + s] = (uint32_t)t;
+      thi[s0 + s] = (uint32_t)(t >> 32);
+    }
+    }
+    // word p = [byte p of step 0 .. step 3]: 3 PRMT per plane
 #pragma unroll
-      for (int p = 0; p < BITS; ++p) word[p] |= (uint32_t)((t >> (8 * p)) & 0xFFu) << i0;
+    for (int p = 0; p < BITS; ++p) {
+      const uint32_t* tv = p < 4 ? tlo : thi;
+      const uint32_t sel = (uint32_t)(p & 3) | ((uint32_t)(4 + (p & 3)) << 4);
+      word[p] = __byte_perm(__byte_perm(tv[0], tv[1], sel), __byte_perm(tv[2], tv[3], sel), 0x5410);
     }
-    }
+    const uint32_t my_sum = (lane & 1) ? my_pair >> 16 : my_pair & 0xFFFFu;
     if (row_sums) {
       const int64_t r = v * 32 + lane;
       if (r < rows && my_sum) {
